@@ -1,0 +1,183 @@
+/*
+ * spechp_b200 — C ABI over the B200 (sm_100a) Collections kernels.
+ *
+ * Drop-in boundary for the spechp Collections hot path.  The reference is
+ * pure Python/numpy (/root/reference/pkg/src/spechp), so there is no
+ * reference FFI; every entry point below replaces the Python routine cited
+ * beside it, and INTEGRATION.md shows the ctypes binding a spechp
+ * maintainer would add to `collections.py` / `assembly.py`.
+ *
+ * Conventions (all mirror the reference):
+ *   - FP64 throughout; blocks are C-contiguous, element-major:
+ *       (E, nmodes) / (E, npoints) / (E, dim, npoints)       collections.py:189-200
+ *   - quad coefficient n = p*m2 + q, point (i,j) -> i*Q2 + j  stdregions.py:1-14
+ *     hex  coefficient n = (p*m2+q)*m3 + r, point ((i*Q2)+j)*Q3 + k (generalised)
+ *   - 1D Modified_A storage boundary-first                    basis.py:111-114
+ *   - all data pointers passed to apply/scatter/assemble are DEVICE pointers
+ *     unless the function name ends in _host; `stream` is a cudaStream_t
+ *     (NULL = legacy default stream).
+ *   - return value: SPHP_OK (0) or a negative SPHP_ERR_*; the message is in
+ *     sphp_last_error() (thread-local), with the reference's wording where
+ *     the reference raises (CollectionError text, collections.py:197-200).
+ *   - handles are immutable after create (except set_lambda) and apply is
+ *     re-entrant on distinct streams; repeated applies are bitwise equal
+ *     (test_collections.py:193-201) — no floating-point atomics anywhere.
+ */
+#ifndef SPECHP_B200_H
+#define SPECHP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPHP_ABI_VERSION 1
+
+/* ---- error codes ------------------------------------------------------ */
+#define SPHP_OK 0
+#define SPHP_ERR_BAD_SHAPE (-1)   /* block shape mismatch (CollectionError) */
+#define SPHP_ERR_BAD_ARG (-2)     /* invalid argument / key               */
+#define SPHP_ERR_UNSUPPORTED (-3) /* valid request this build cannot run  */
+#define SPHP_ERR_CUDA (-4)        /* CUDA runtime failure                 */
+#define SPHP_ERR_ALLOC (-5)       /* device or host allocation failure    */
+
+/* ---- enums (values match the reference Enum order) -------------------- */
+/* stdregions.py:41-44 Shape (+ HEX, the 3D generalisation)               */
+#define SPHP_SHAPE_SEG 0
+#define SPHP_SHAPE_QUAD 1
+#define SPHP_SHAPE_TRI 2 /* declared for parity; kernels: UNSUPPORTED */
+#define SPHP_SHAPE_HEX 3
+/* quadrature.py:19-25 PointsType                                          */
+#define SPHP_POINTS_GAUSS_LEGENDRE 0
+#define SPHP_POINTS_GAUSS_LOBATTO_LEGENDRE 1
+#define SPHP_POINTS_GAUSS_RADAU_M_LEGENDRE 2
+/* basis.py:26-29 BasisType                                                */
+#define SPHP_BASIS_MODIFIED_A 0
+#define SPHP_BASIS_MODIFIED_B 1
+#define SPHP_BASIS_LAGRANGE_GLL 2
+/* collections.py:26-29 OperatorKind (+ the two the north star adds)       */
+#define SPHP_OP_BWD_TRANS 0
+#define SPHP_OP_IPRODUCT_WRT_BASE 1
+#define SPHP_OP_PHYS_DERIV 2
+#define SPHP_OP_IPRODUCT_WRT_DERIV_BASE 3 /* geometry.py:163-168 batched */
+#define SPHP_OP_HELMHOLTZ 4               /* geometry.py:171-184 fused   */
+/* collections.py:32-36 Strategy: the GPU strategies                       */
+#define SPHP_STRATEGY_CUDA_SUMFAC 0 /* staged 1D contractions, fused     */
+#define SPHP_STRATEGY_CUDA_STDMAT 1 /* dense elemental operator, DGEMM   */
+/* geometry encodings (collections.py:110-129 precomputation, on device)   */
+#define SPHP_GEOM_NONE 0   /* standard elements: weights only              */
+#define SPHP_GEOM_AFFINE 1 /* per element: [det, inv (d x d row-major a,k)] */
+#define SPHP_GEOM_POINT 2  /* per element, per point SoA: [wJ, inv_ak...]   */
+#define SPHP_GEOM_METRIC 3 /* per element, per point SoA: symmetric
+                              G_ab = wJ sum_k inv[a,k] inv[b,k] then wJ:
+                              quad [G00,G01,G11,wJ]; hex
+                              [G00,G01,G02,G11,G12,G22,wJ]                 */
+/* analytic structured-grid maps (BASELINE.json configs)                   */
+#define SPHP_MAP_AFFINE 0    /* x' = x                                   */
+#define SPHP_MAP_QUAD_SINE 1 /* cfg2: x'=x+a sin2πy, y'=y+a sin2πx        */
+#define SPHP_MAP_HEX_SINE 2  /* cfg4: x'=x+a sin2πy sin2πz                */
+
+typedef struct sphp_tables sphp_tables;
+typedef struct sphp_coll sphp_coll;
+typedef struct sphp_amap sphp_amap;
+typedef void* sphp_stream; /* cudaStream_t */
+
+/* ---- library ------------------------------------------------------------ */
+int sphp_abi_version(void);
+const char* sphp_last_error(void);
+/* number of SMs of the current device, 0 if none (used by the autotuner)   */
+int sphp_device_sm_count(void);
+
+/* ---- reference elements: StdExpansion tables ----------------------------
+ * replaces stdregions.StdExpansion(shape, basis_keys) (stdregions.py:70-240)
+ * with quadrature.make_rule (quadrature.py:188-214), diff_matrix (:246-260)
+ * and basis tables (basis.py:78-114).  Arrays have one entry per direction. */
+int sphp_tables_create(int shape, const int* nmodes, const int* npoints,
+                       const int* points_type, const int* basis_type,
+                       sphp_tables** out);
+int sphp_tables_destroy(sphp_tables* t);
+/* copy direction `dir`'s tables to host: z,w (Q); B,Bd (m*Q, B[p*Q+i]);
+ * D (Q*Q, D[i*Q+j]).  Any pointer may be NULL.                              */
+int sphp_tables_query(const sphp_tables* t, int dir, double* z, double* w,
+                      double* B, double* Bd, double* D);
+/* sizes: num_modes, num_points, dim                                        */
+int sphp_tables_sizes(const sphp_tables* t, int64_t* nmodes, int64_t* npoints,
+                      int* dim);
+
+/* ---- geometry (geometry.py:115-142 semantics, evaluated on device) ------
+ * Fill per-element geometry for structured-grid elements of an n^dim grid on
+ * [0,L]^dim with an analytic map.  elem_ids: device int64 ids (NULL -> ids
+ * e0 .. e0+E-1).  Element id = ex + n*(ey + n*ez).  Layout is that of
+ * sphp_geom_stride().  Raises BAD_ARG if a Jacobian is non-positive.       */
+int64_t sphp_geom_stride(const sphp_tables* t, int geom_kind);
+int sphp_geom_analytic(const sphp_tables* t, int geom_kind, int mapping,
+                       int n, const double* lengths, double amp, int64_t e0,
+                       int64_t E, const int64_t* elem_ids, double* geom,
+                       sphp_stream stream);
+/* convert reference GeomFactors arrays (device, reference layout:
+ * wj (E,np), inv (E,np,d,d)) into geom_kind layout                         */
+int sphp_geom_from_factors(const sphp_tables* t, int geom_kind, int64_t E,
+                           const double* wj, const double* inv, double* geom,
+                           sphp_stream stream);
+
+/* ---- collections: replaces collections.Collection (collections.py:76-246)
+ * geom: device pointer in `geom_kind` layout, borrowed (must outlive the
+ * handle); NULL with SPHP_GEOM_NONE.  lambda only used by HELMHOLTZ.        */
+int sphp_collection_create(const sphp_tables* t, int op, int strategy,
+                           int64_t E, int geom_kind, const double* geom,
+                           double lambda, sphp_coll** out);
+int sphp_collection_destroy(sphp_coll* c);
+int sphp_collection_set_lambda(sphp_coll* c, double lambda);
+/* input_size / output_size per element, MAC count of one apply
+ * (collections.py:250-273 generalised), algorithmic HBM bytes of one apply */
+int sphp_collection_info(const sphp_coll* c, int64_t* input_size,
+                         int64_t* output_size, int64_t* mac_count,
+                         int64_t* hbm_bytes);
+/* Collection.apply (collections.py:189-246) on device buffers:
+ * in (E, input_size), out (E, output_size).  E must equal the handle's E
+ * (CollectionError "block shape (a, b) does not match (E, n)").            */
+int sphp_apply(sphp_coll* c, int64_t E, int64_t n_in, const double* in,
+               double* out, sphp_stream stream);
+/* same with HOST buffers: copies in -> device, apply, device -> out, all on
+ * `stream`, then synchronises it.  Uses a workspace owned by the handle.   */
+int sphp_apply_host(sphp_coll* c, int64_t E, int64_t n_in, const double* in,
+                    double* out, sphp_stream stream);
+
+/* ---- assembly: replaces assembly.AssemblyMap / assemble / scatter
+ * (assembly.py:44-160) and GlobalSystem.apply (:168-182).
+ * Codes: gid >= 0 (sign +1), -1 pinned (sign 0), -(gid+2) (sign -1).      */
+int sphp_amap_create_explicit(int64_t E, int nmodes, const int64_t* codes_host,
+                              int64_t num_global, sphp_amap** out);
+/* periodic n^3 hex grid, uniform order P: numbering of assembly.py:89-133
+ * generalised (vertices, edges, faces, interiors); indices computed on the
+ * fly on device (no map traffic).                                          */
+int sphp_amap_create_hex_periodic(int n, int P, sphp_amap** out);
+/* periodic n^3 hex grid with per-element orders (host array, n^3 entries):
+ * fills num_global; if codes != NULL also writes per-element codes packed
+ * back to back (element e at offsets[e], offsets has n^3+1 entries).       */
+int sphp_hexmap_variable(int n, const int* orders, int64_t* num_global,
+                         int64_t* offsets, int64_t* codes);
+int sphp_amap_destroy(sphp_amap* a);
+int sphp_amap_info(const sphp_amap* a, int64_t* num_elements, int* nmodes,
+                   int64_t* num_global, int* num_colours);
+/* materialise the map codes (E*nmodes int64, host) — for bit-exact tests   */
+int sphp_amap_codes(const sphp_amap* a, int64_t* codes_host);
+/* assembly.scatter: global (num_global) -> local (E, nmodes), pinned -> 0  */
+int sphp_scatter(const sphp_amap* a, const double* global, double* local,
+                 sphp_stream stream);
+/* assembly.assemble: local (E, nmodes) -> global (num_global), overwritten;
+ * deterministic colour-ordered signed sum (no atomics)                     */
+int sphp_assemble(const sphp_amap* a, const double* local, double* global,
+                  sphp_stream stream);
+/* GlobalSystem.apply for a HELMHOLTZ collection: y = A^T H A x, fused
+ * gather -> elemental Helmholtz -> colour-ordered scatter-add.  When
+ * accumulate != 0, y is added to instead of overwritten (variable-order
+ * meshes: one call per order batch, same y).                              */
+int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x,
+                             double* y, int accumulate, sphp_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECHP_B200_H */

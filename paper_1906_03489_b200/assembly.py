@@ -1,0 +1,170 @@
+"""C0 assembly on the device (drop-in for assembly.py:44-215).
+
+`AssemblyMap` wraps an `sphp_amap` handle:
+  * `AssemblyMap.explicit(codes, num_global)` / `.from_reference(amap)` take
+    the reference's local_to_global + signs (assembly.py:44-56) — bit-exact
+    by construction, encoded as gid / -1 (pinned) / -(gid+2) (sign -1);
+  * `AssemblyMap.hex_periodic(n, P)` is the periodic structured hex map of
+    cfg4 with indices computed on the fly on the device (no map traffic);
+  * `hex_variable_maps(n, orders)` builds the variable-order map of cfg5
+    (edge order = min over the 4 sharing elements, face order = min over 2,
+    excess modes pinned) and splits it into per-order batches.
+
+`scatter` / `assemble` mirror assembly.py:141-160 (assemble is a
+deterministic colour-ordered sum, no atomics); `GlobalHelmholtz.apply` is
+`GlobalSystem.apply` (assembly.py:177-182) with the gather, the elemental
+operator and the scatter-add fused in one kernel per colour.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+class AssemblyError(ValueError):
+    pass
+
+
+def encode(local_to_global, signs):
+    """Reference (l2g, signs) lists -> (E, nm) int64 codes."""
+    rows = []
+    for l2g, sgn in zip(local_to_global, signs):
+        l2g = np.asarray(l2g, dtype=np.int64)
+        sgn = np.asarray(sgn)
+        c = l2g.copy()
+        neg = sgn < 0
+        c[neg] = -(l2g[neg] + 2)
+        c[l2g < 0] = -1
+        rows.append(c)
+    return np.ascontiguousarray(np.stack(rows))
+
+
+def decode(codes):
+    codes = np.asarray(codes, dtype=np.int64)
+    gid = np.where(codes >= 0, codes, np.where(codes == -1, -1, -codes - 2))
+    sgn = np.where(codes >= 0, 1.0, np.where(codes == -1, 0.0, -1.0))
+    return gid, sgn
+
+
+class AssemblyMap:
+    def __init__(self, handle):
+        self._h = handle
+        ne, nm, ng, nc = C.c_int64(), C.c_int(), C.c_int64(), C.c_int()
+        _lib.check(_lib.lib.sphp_amap_info(self._h, C.byref(ne), C.byref(nm), C.byref(ng),
+                                           C.byref(nc)))
+        self.num_elements, self.nmodes = ne.value, nm.value
+        self.num_global, self.num_colours = ng.value, nc.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None and _lib.lib is not None:
+            _lib.lib.sphp_amap_destroy(h)
+            self._h = None
+
+    @classmethod
+    def explicit(cls, codes, num_global):
+        codes = np.ascontiguousarray(codes, dtype=np.int64)
+        E, nm = codes.shape
+        h = C.c_void_p()
+        _lib.check(_lib.lib.sphp_amap_create_explicit(E, nm, _lib.ptr(codes), int(num_global),
+                                                      C.byref(h)), AssemblyError)
+        return cls(h)
+
+    @classmethod
+    def from_reference(cls, amap):
+        """Any object with local_to_global, signs, num_global (assembly.py:44-56)."""
+        return cls.explicit(encode(amap.local_to_global, amap.signs), amap.num_global)
+
+    @classmethod
+    def hex_periodic(cls, n, P):
+        h = C.c_void_p()
+        _lib.check(_lib.lib.sphp_amap_create_hex_periodic(int(n), int(P), C.byref(h)),
+                   AssemblyError)
+        return cls(h)
+
+    def codes(self):
+        out = np.empty((self.num_elements, self.nmodes), dtype=np.int64)
+        _lib.check(_lib.lib.sphp_amap_codes(self._h, _lib.ptr(out)))
+        return out
+
+    @property
+    def local_to_global(self):
+        return list(decode(self.codes())[0])
+
+    @property
+    def signs(self):
+        return list(decode(self.codes())[1])
+
+
+def hex_variable_codes(n, orders):
+    """Full variable-order periodic hex map: (num_global, offsets, codes)."""
+    orders = np.ascontiguousarray(orders, dtype=np.int32)
+    if orders.size != n ** 3:
+        raise AssemblyError(f"need {n ** 3} orders, got {orders.size}")
+    ng = C.c_int64()
+    _lib.check(_lib.lib.sphp_hexmap_variable(int(n), _lib.ptr(orders), C.byref(ng), None, None),
+               AssemblyError)
+    offsets = np.empty(n ** 3 + 1, dtype=np.int64)
+    total = int(np.sum((orders.astype(np.int64) + 1) ** 3))
+    codes = np.empty(total, dtype=np.int64)
+    _lib.check(_lib.lib.sphp_hexmap_variable(int(n), _lib.ptr(orders), C.byref(ng),
+                                             _lib.ptr(offsets), _lib.ptr(codes)), AssemblyError)
+    return ng.value, offsets, codes
+
+
+def hex_variable_maps(n, orders):
+    """Per-order batches of the variable-order map: {P: (elem_ids, AssemblyMap)}."""
+    orders = np.asarray(orders).ravel()
+    ng, offsets, codes = hex_variable_codes(n, orders)
+    out = {}
+    for P in sorted(set(int(p) for p in orders)):
+        ids = np.nonzero(orders == P)[0]
+        nm = (P + 1) ** 3
+        rows = np.stack([codes[offsets[e]:offsets[e] + nm] for e in ids])
+        out[P] = (ids, AssemblyMap.explicit(rows, ng))
+    return ng, out
+
+
+def scatter(amap: AssemblyMap, x, out=None, stream=None):
+    """Global -> local (E, nm), pinned modes -> 0 (assembly.py:150-160)."""
+    if out is None:
+        out = torch.empty((amap.num_elements, amap.nmodes), dtype=torch.float64, device=x.device)
+    _lib.check(_lib.lib.sphp_scatter(amap._h, _lib.ptr(x), _lib.ptr(out), _lib.stream_ptr(stream)))
+    return out
+
+
+def assemble(amap: AssemblyMap, local, out=None, stream=None):
+    """Local (E, nm) -> global, signed, deterministic (assembly.py:141-147)."""
+    if out is None:
+        out = torch.empty(amap.num_global, dtype=torch.float64, device=local.device)
+    _lib.check(_lib.lib.sphp_assemble(amap._h, _lib.ptr(local.contiguous()), _lib.ptr(out),
+                                      _lib.stream_ptr(stream)))
+    return out
+
+
+class GlobalHelmholtz:
+    """Matrix-free assembled Helmholtz y = A^T H A x over one or more
+    per-order batches [(Collection(HELMHOLTZ), AssemblyMap)] that share the
+    global numbering (GlobalSystem.apply, assembly.py:177-182)."""
+
+    def __init__(self, batches, num_global):
+        self.batches = list(batches)
+        self.num_global = int(num_global)
+        for coll, amap in self.batches:
+            if amap.num_global != self.num_global:
+                raise AssemblyError("batches disagree on num_global")
+
+    def apply(self, x, out=None, stream=None):
+        if out is None:
+            out = torch.empty(self.num_global, dtype=torch.float64, device=x.device)
+        for k, (coll, amap) in enumerate(self.batches):
+            rc = _lib.lib.sphp_helmholtz_assembled(coll._handle, amap._h, _lib.ptr(x), _lib.ptr(out),
+                                                   1 if k else 0, _lib.stream_ptr(stream))
+            _lib.check(rc, AssemblyError)
+        return out
+
+    __call__ = apply

@@ -1,0 +1,1002 @@
+// C ABI of spechp_b200 (include/spechp_b200.h): handle management, argument
+// checking with the reference's error wording, strategy dispatch and the
+// assembly-map builders.  Every entry point cites the reference routine it
+// replaces.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/spechp_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "misc.h"
+#include "tables.h"
+
+using namespace sphp;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SPHP_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                         \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+  } while (0)
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+int sm_count() {
+  static int cache[64] = {0};
+  int d = current_device();
+  if (cache[d & 63] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) n = 0;
+    cache[d & 63] = n;
+  }
+  return cache[d & 63];
+}
+
+// per-device one-time upload of the constant-memory table pool
+int ensure_tables_uploaded() {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int d = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  if (!done[d & 63]) {
+    cudaError_t e = upload_all_tables();
+    if (e != cudaSuccess) return cuda_fail(e, "upload constant tables");
+    done[d & 63] = true;
+  }
+  return SPHP_OK;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int dev = -1;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t ensure(size_t b) {
+    if (p && bytes >= b) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, b ? b : 16);
+    if (e == cudaSuccess) bytes = b;
+    return e;
+  }
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// fast-table pool (constant memory image)
+// ---------------------------------------------------------------------------
+namespace sphp {
+const double* fast_table_pool() {
+  static std::vector<double> pool;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    pool.assign(TAB_TOTAL, 0.0);
+    for (int m = FAST_M_MIN; m <= FAST_M_MAX; ++m)
+      for (int q = m + 1; q <= m + 2; ++q) {
+        std::vector<double> z, w, B, Bd, D;
+        make_rule(q, SPHP_POINTS_GAUSS_LOBATTO_LEGENDRE, z, w);
+        basis_table(SPHP_BASIS_MODIFIED_A, m, z, B, Bd);
+        diff_matrix(z, D);
+        double* dst = pool.data() + tab_off(m, q);
+        std::copy(B.begin(), B.end(), dst);
+        std::copy(Bd.begin(), Bd.end(), dst + m * q);
+        std::copy(D.begin(), D.end(), dst + 2 * m * q);
+        std::copy(w.begin(), w.end(), dst + 2 * m * q + q * q);
+      }
+  });
+  return pool.data();
+}
+cudaError_t upload_tables_hex_helm();
+cudaError_t upload_tables_hex_misc();
+cudaError_t upload_tables_quad();
+cudaError_t upload_all_tables() {
+  cudaError_t e = upload_tables_hex_helm();
+  if (e == cudaSuccess) e = upload_tables_hex_misc();
+  if (e == cudaSuccess) e = upload_tables_quad();
+  return e;
+}
+}  // namespace sphp
+
+// ---------------------------------------------------------------------------
+// handles
+// ---------------------------------------------------------------------------
+struct sphp_tables {
+  int shape = 0, dim = 0;
+  int m[3] = {0, 0, 0}, q[3] = {0, 0, 0}, ptype[3] = {0, 0, 0}, btype[3] = {0, 0, 0};
+  std::vector<double> z[3], w[3], B[3], Bd[3], D[3];
+  int64_t nm = 0, np = 0;
+  bool fast = false;  // sum-factorisation kernels available for this key
+  // lazily built device copies
+  std::mutex mu;
+  DevBuf d_z, d_w, d_wstd;
+  std::vector<double> wstd;  // tensor weights, point order
+};
+
+struct sphp_coll {
+  sphp_tables* t = nullptr;
+  int op = 0, strategy = 0, geom_kind = 0;
+  int64_t E = 0, in_size = 0, out_size = 0;
+  const double* geom = nullptr;
+  int64_t gstride = 0, cs = 0;
+  double lam = 0.0;
+  // workspaces
+  DevBuf host_in, host_out;       // apply_host staging
+  DevBuf scratch;                 // StdMat pointwise buffers
+  DevBuf mat_a, mat_b;            // StdMat dense operators
+  DevBuf helm_H;                  // StdMat Helmholtz element matrices
+  DevBuf loc_x, loc_y;            // StdMat assembled path
+};
+
+struct sphp_amap {
+  int periodic = 0, n = 0, P = 0, nm = 0;
+  int64_t E = 0, num_global = 0;
+  int ncolours = 0;
+  std::vector<int64_t> codes_host;  // explicit only
+  std::vector<int64_t> colour_off;  // explicit only (ncolours+1)
+  std::vector<int> elist_host;      // explicit only, element ids by colour
+  std::mutex mu;
+  DevBuf d_codes, d_elist;
+  AmapDev dev() const {
+    AmapDev a;
+    a.periodic = periodic;
+    a.n = n;
+    a.P = P;
+    a.nm = nm;
+    a.E = E;
+    a.num_global = num_global;
+    a.codes = d_codes.as<int>();
+    return a;
+  }
+};
+
+namespace {
+
+int64_t ipow(int64_t b, int e) {
+  int64_t r = 1;
+  while (e--) r *= b;
+  return r;
+}
+
+int tables_device(sphp_tables* t) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  if (t->d_z.p) return SPHP_OK;
+  CK(t->d_z.ensure(sizeof(double) * t->q[0]));
+  CK(t->d_w.ensure(sizeof(double) * t->q[0]));
+  CK(cudaMemcpy(t->d_z.p, t->z[0].data(), sizeof(double) * t->q[0], cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(t->d_w.p, t->w[0].data(), sizeof(double) * t->q[0], cudaMemcpyHostToDevice));
+  CK(t->d_wstd.ensure(sizeof(double) * t->np));
+  CK(cudaMemcpy(t->d_wstd.p, t->wstd.data(), sizeof(double) * t->np, cudaMemcpyHostToDevice));
+  return SPHP_OK;
+}
+
+// dense (Kronecker) operators on host --------------------------------------
+// B[n][i] = prod_a B_a[idx_a(n)][idx_a(i)]   (stdregions.py:189-198)
+std::vector<double> dense_bwd(const sphp_tables* t) {
+  std::vector<double> M((size_t)t->nm * t->np);
+  for (int64_t n = 0; n < t->nm; ++n)
+    for (int64_t i = 0; i < t->np; ++i) {
+      int64_t rn = n, ri = i;
+      double v = 1.0;
+      for (int a = t->dim - 1; a >= 0; --a) {
+        int pn = (int)(rn % t->m[a]), pi = (int)(ri % t->q[a]);
+        rn /= t->m[a];
+        ri /= t->q[a];
+        v *= t->B[a][(size_t)pn * t->q[a] + pi];
+      }
+      M[(size_t)n * t->np + i] = v;
+    }
+  return M;
+}
+// derivative along direction a acting on flattened point vectors:
+// (D_a)[i][j] (stdregions.py:218-235)
+double dense_deriv(const sphp_tables* t, int a, int64_t i, int64_t j) {
+  int64_t ri = i, rj = j;
+  double v = 1.0;
+  for (int b = t->dim - 1; b >= 0; --b) {
+    int ii = (int)(ri % t->q[b]), jj = (int)(rj % t->q[b]);
+    ri /= t->q[b];
+    rj /= t->q[b];
+    if (b == a)
+      v *= t->D[b][(size_t)ii * t->q[b] + jj];
+    else if (ii != jj)
+      return 0.0;
+  }
+  return v;
+}
+
+int64_t geom_record(const sphp_tables* t, int kind) {
+  const int d = t->dim;
+  const int64_t cs = (t->np + 1) & ~1LL;
+  switch (kind) {
+    case SPHP_GEOM_NONE: return 0;
+    case SPHP_GEOM_AFFINE: return d == 3 ? 10 : 6;
+    case SPHP_GEOM_POINT: return (1 + d * d) * cs;
+    case SPHP_GEOM_METRIC: return (d * (d + 1) / 2 + 1) * cs;
+  }
+  return -1;
+}
+
+OpArgs base_args(const sphp_coll* c) {
+  OpArgs a;
+  a.M = c->t->m[0];
+  a.Q = c->t->q[0];
+  a.E = c->E;
+  a.in = nullptr;
+  a.out = nullptr;
+  a.geom = c->geom;
+  a.geom_kind = c->geom_kind;
+  a.gstride = c->gstride;
+  a.lam = c->lam;
+  a.num_sms = sm_count();
+  a.mode = AsmMode::LOCAL;
+  a.xg = nullptr;
+  a.yg = nullptr;
+  a.elist = nullptr;
+  a.nlist = 0;
+  a.codes = nullptr;
+  a.n = 0;
+  a.colour = 0;
+  return a;
+}
+
+cudaError_t sumfac_launch(const sphp_coll* c, const OpArgs& a, cudaStream_t s) {
+  const bool hex = c->t->shape == SPHP_SHAPE_HEX;
+  switch (c->op) {
+    case SPHP_OP_BWD_TRANS: return hex ? hex_bwd(a, s) : quad_bwd(a, s);
+    case SPHP_OP_IPRODUCT_WRT_BASE: return hex ? hex_iprod(a, s) : quad_iprod(a, s);
+    case SPHP_OP_PHYS_DERIV: return hex ? hex_physderiv(a, s) : quad_physderiv(a, s);
+    case SPHP_OP_IPRODUCT_WRT_DERIV_BASE: return hex ? hex_ipderiv(a, s) : quad_ipderiv(a, s);
+    case SPHP_OP_HELMHOLTZ: return hex ? hex_helmholtz(a, s) : quad_helmholtz(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+PointJob point_job(const sphp_coll* c) {
+  PointJob j;
+  j.dim = c->t->dim;
+  j.kind = c->geom_kind;
+  j.E = c->E;
+  j.np = c->t->np;
+  j.cs = c->cs;
+  j.stride = c->gstride;
+  j.geom = c->geom;
+  j.wstd = c->t->d_wstd.as<double>();
+  return j;
+}
+
+// build the StdMat operators of a collection (once)
+int stdmat_prepare(sphp_coll* c, cudaStream_t s) {
+  sphp_tables* t = c->t;
+  const int64_t nm = t->nm, np = t->np;
+  const int d = t->dim;
+  if (c->op == SPHP_OP_HELMHOLTZ) {
+    if (c->helm_H.p) return SPHP_OK;
+    if (!t->fast)
+      return fail(SPHP_ERR_UNSUPPORTED, "stdmat Helmholtz needs a sum-factorisation key to build H_e");
+    const double bytes = 8.0 * c->E * nm * nm;
+    if (bytes > 48e9)
+      return fail(SPHP_ERR_UNSUPPORTED, "stdmat Helmholtz element matrices exceed the 48 GB budget");
+    CK(c->helm_H.ensure((size_t)bytes));
+    CK(c->loc_x.ensure(sizeof(double) * c->E * nm));
+    CK(c->loc_y.ensure(sizeof(double) * c->E * nm));
+    // column n of every H_e = fused Helmholtz applied to unit vector e_n
+    OpArgs a = base_args(c);
+    for (int n = 0; n < nm; ++n) {
+      CK(unit_block(c->E, (int)nm, n, c->loc_x.as<double>(), s));
+      a.in = c->loc_x.as<double>();
+      a.out = c->loc_y.as<double>();
+      cudaError_t e = sumfac_launch(c, a, s);
+      if (e != cudaSuccess) return cuda_fail(e, "stdmat Helmholtz build");
+      CK(store_column(c->E, (int)nm, n, c->loc_y.as<double>(), c->helm_H.as<double>(), s));
+    }
+    CK(symmetrise(c->E, (int)nm, c->helm_H.as<double>(), s));  // geometry.py:184
+    CK(cudaStreamSynchronize(s));
+    return SPHP_OK;
+  }
+  if (c->mat_a.p) return SPHP_OK;
+  std::vector<double> Bm = dense_bwd(t);  // (nm, np)
+  std::vector<double> A;
+  switch (c->op) {
+    case SPHP_OP_BWD_TRANS:
+      A = Bm;  // out = in (E,nm) @ B (nm,np)   collections.py:205
+      break;
+    case SPHP_OP_IPRODUCT_WRT_BASE:
+      A.assign((size_t)np * nm, 0.0);  // B^T (np, nm)   collections.py:218
+      for (int64_t n = 0; n < nm; ++n)
+        for (int64_t i = 0; i < np; ++i) A[(size_t)i * nm + n] = Bm[(size_t)n * np + i];
+      break;
+    case SPHP_OP_PHYS_DERIV:
+      A.assign((size_t)np * d * np, 0.0);  // [D_0^T .. D_{d-1}^T] (np, d*np)   collections.py:228-229
+      for (int a = 0; a < d; ++a)
+        for (int64_t i = 0; i < np; ++i)
+          for (int64_t j = 0; j < np; ++j) A[(size_t)j * d * np + a * np + i] = dense_deriv(t, a, i, j);
+      break;
+    case SPHP_OP_IPRODUCT_WRT_DERIV_BASE: {
+      // stacked B_a^T = D_a B^T (d*np, nm)   geometry.py:163-168
+      A.assign((size_t)d * np * nm, 0.0);
+      for (int a = 0; a < d; ++a)
+        for (int64_t i = 0; i < np; ++i)
+          for (int64_t j = 0; j < np; ++j) {
+            const double v = dense_deriv(t, a, i, j);
+            if (v == 0.0) continue;
+            for (int64_t n = 0; n < nm; ++n) A[((size_t)a * np + i) * nm + n] += v * Bm[(size_t)n * np + j];
+          }
+      break;
+    }
+  }
+  CK(c->mat_a.ensure(sizeof(double) * A.size()));
+  CK(cudaMemcpy(c->mat_a.p, A.data(), sizeof(double) * A.size(), cudaMemcpyHostToDevice));
+  return SPHP_OK;
+}
+
+int stdmat_apply(sphp_coll* c, const double* in, double* out, cudaStream_t s) {
+  int rc = stdmat_prepare(c, s);
+  if (rc) return rc;
+  sphp_tables* t = c->t;
+  const int64_t nm = t->nm, np = t->np;
+  const int d = t->dim;
+  const double* A = c->mat_a.as<double>();
+  switch (c->op) {
+    case SPHP_OP_BWD_TRANS:
+      CK(dgemm(c->E, (int)np, (int)nm, in, A, out, s));
+      break;
+    case SPHP_OP_IPRODUCT_WRT_BASE:
+      CK(c->scratch.ensure(sizeof(double) * c->E * np));
+      CK(pointwise(0, point_job(c), in, c->scratch.as<double>(), s));
+      CK(dgemm(c->E, (int)nm, (int)np, c->scratch.as<double>(), A, out, s));
+      break;
+    case SPHP_OP_PHYS_DERIV:
+      CK(dgemm(c->E, (int)(d * np), (int)np, in, A, out, s));
+      if (c->geom_kind != SPHP_GEOM_NONE) CK(pointwise(1, point_job(c), nullptr, out, s));
+      break;
+    case SPHP_OP_IPRODUCT_WRT_DERIV_BASE:
+      CK(c->scratch.ensure(sizeof(double) * c->E * d * np));
+      CK(pointwise(2, point_job(c), in, c->scratch.as<double>(), s));
+      CK(dgemm(c->E, (int)nm, (int)(d * np), c->scratch.as<double>(), A, out, s));
+      break;
+    case SPHP_OP_HELMHOLTZ:
+      CK(elem_matvec(c->E, (int)nm, c->helm_H.as<double>(), in, out, s));
+      break;
+    default:
+      return fail(SPHP_ERR_BAD_ARG, "unknown operator");
+  }
+  return SPHP_OK;
+}
+
+int64_t mac_count(const sphp_coll* c) {
+  const sphp_tables* t = c->t;
+  const int d = t->dim;
+  const int64_t m = t->m[0], Q = t->q[0], nm = t->nm, np = t->np, E = c->E;
+  const bool geo = c->geom_kind != SPHP_GEOM_NONE;
+  const bool sm = c->strategy == SPHP_STRATEGY_CUDA_STDMAT;
+  int64_t staged = (d == 2) ? m * m * Q + m * Q * Q : m * m * m * Q + m * m * Q * Q + m * Q * Q * Q;
+  const int64_t dense = nm * np;
+  int64_t per = 0;
+  switch (c->op) {
+    case SPHP_OP_BWD_TRANS: per = sm ? dense : staged; break;
+    case SPHP_OP_IPRODUCT_WRT_BASE: per = np + (sm ? dense : staged); break;
+    case SPHP_OP_PHYS_DERIV: per = (sm ? d * np * np : d * ipow(Q, d + 1)) + (geo ? d * d * np : 0); break;
+    case SPHP_OP_IPRODUCT_WRT_DERIV_BASE:
+      per = (sm ? d * np * nm : d * ipow(Q, d + 1) + staged) + (d * d + d) * np;
+      break;
+    case SPHP_OP_HELMHOLTZ:
+      per = sm ? nm * nm : 2 * staged + 2 * d * ipow(Q, d + 1) + (d * d + d + 2) * np;
+      break;
+  }
+  return E * per;
+}
+
+int64_t hbm_bytes(const sphp_coll* c) {
+  const sphp_tables* t = c->t;
+  const int d = t->dim;
+  const int64_t nm = t->nm, np = t->np, E = c->E;
+  int64_t io = 8 * E * (c->in_size + c->out_size);
+  int64_t g = 0;
+  const bool pt = c->geom_kind == SPHP_GEOM_POINT || c->geom_kind == SPHP_GEOM_METRIC;
+  switch (c->op) {
+    case SPHP_OP_IPRODUCT_WRT_BASE: g = c->geom_kind == SPHP_GEOM_NONE ? 0 : (pt ? np : 1); break;
+    case SPHP_OP_PHYS_DERIV: g = c->geom_kind == SPHP_GEOM_NONE ? 0 : (pt ? d * d * np : d * d); break;
+    case SPHP_OP_IPRODUCT_WRT_DERIV_BASE:
+      g = c->geom_kind == SPHP_GEOM_NONE ? 0 : (pt ? (1 + d * d) * np : 1 + d * d);
+      break;
+    case SPHP_OP_HELMHOLTZ:
+      if (c->strategy == SPHP_STRATEGY_CUDA_STDMAT)
+        g = nm * nm;
+      else
+        g = c->geom_kind == SPHP_GEOM_METRIC ? (d * (d + 1) / 2 + 1) * np : 1 + d * d;
+      break;
+  }
+  return io + 8 * E * g;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int sphp_abi_version(void) { return SPHP_ABI_VERSION; }
+const char* sphp_last_error(void) { return g_err.c_str(); }
+int sphp_device_sm_count(void) { return sm_count(); }
+
+// stdregions.StdExpansion (stdregions.py:70-240)
+int sphp_tables_create(int shape, const int* nmodes, const int* npoints, const int* points_type,
+                       const int* basis_type, sphp_tables** out) {
+  if (!out || !nmodes || !npoints || !points_type || !basis_type)
+    return fail(SPHP_ERR_BAD_ARG, "null argument");
+  int dim;
+  switch (shape) {
+    case SPHP_SHAPE_SEG: dim = 1; break;
+    case SPHP_SHAPE_QUAD: dim = 2; break;
+    case SPHP_SHAPE_HEX: dim = 3; break;
+    case SPHP_SHAPE_TRI:
+      return fail(SPHP_ERR_UNSUPPORTED, "triangle (Modified_B) collections are not built yet");
+    default: return fail(SPHP_ERR_BAD_ARG, "unknown shape");
+  }
+  auto* t = new sphp_tables();
+  t->shape = shape;
+  t->dim = dim;
+  try {
+    for (int a = 0; a < dim; ++a) {
+      t->m[a] = nmodes[a];
+      t->q[a] = npoints[a];
+      t->ptype[a] = points_type[a];
+      t->btype[a] = basis_type[a];
+      if (nmodes[a] < 1) throw std::invalid_argument("num_modes must be positive");
+      if (npoints[a] < 1) throw std::invalid_argument("num_points must be a positive integer");
+      if (basis_type[a] == SPHP_BASIS_MODIFIED_B)
+        throw std::invalid_argument("collapsed-direction basis is only valid on triangles");
+      make_rule(npoints[a], points_type[a], t->z[a], t->w[a]);
+      basis_table(basis_type[a], nmodes[a], t->z[a], t->B[a], t->Bd[a]);
+      diff_matrix(t->z[a], t->D[a]);
+    }
+  } catch (const std::exception& ex) {
+    delete t;
+    return fail(SPHP_ERR_BAD_ARG, ex.what());
+  }
+  t->nm = 1;
+  t->np = 1;
+  for (int a = 0; a < dim; ++a) {
+    t->nm *= t->m[a];
+    t->np *= t->q[a];
+  }
+  bool uniform = true;
+  for (int a = 1; a < dim; ++a)
+    uniform = uniform && t->m[a] == t->m[0] && t->q[a] == t->q[0] && t->ptype[a] == t->ptype[0] &&
+              t->btype[a] == t->btype[0];
+  t->fast = uniform && (shape == SPHP_SHAPE_QUAD || shape == SPHP_SHAPE_HEX) &&
+            t->ptype[0] == SPHP_POINTS_GAUSS_LOBATTO_LEGENDRE && t->btype[0] == SPHP_BASIS_MODIFIED_A &&
+            fast_key(t->m[0], t->q[0]) && (shape == SPHP_SHAPE_QUAD || t->m[0] <= 9);
+  // tensor weights in point order (stdregions.py:113-121)
+  t->wstd.assign(t->np, 1.0);
+  for (int64_t i = 0; i < t->np; ++i) {
+    int64_t r = i;
+    double w = 1.0;
+    int idx[3] = {0, 0, 0};
+    for (int a = dim - 1; a >= 0; --a) {
+      idx[a] = (int)(r % t->q[a]);
+      r /= t->q[a];
+    }
+    for (int a = 0; a < dim; ++a) w *= t->w[a][idx[a]];
+    t->wstd[i] = w;
+  }
+  *out = t;
+  return SPHP_OK;
+}
+
+int sphp_tables_destroy(sphp_tables* t) {
+  delete t;
+  return SPHP_OK;
+}
+
+int sphp_tables_query(const sphp_tables* t, int dir, double* z, double* w, double* B, double* Bd,
+                      double* D) {
+  if (!t || dir < 0 || dir >= t->dim) return fail(SPHP_ERR_BAD_ARG, "bad direction");
+  const size_t q = t->q[dir], m = t->m[dir];
+  if (z) std::memcpy(z, t->z[dir].data(), sizeof(double) * q);
+  if (w) std::memcpy(w, t->w[dir].data(), sizeof(double) * q);
+  if (B) std::memcpy(B, t->B[dir].data(), sizeof(double) * m * q);
+  if (Bd) std::memcpy(Bd, t->Bd[dir].data(), sizeof(double) * m * q);
+  if (D) std::memcpy(D, t->D[dir].data(), sizeof(double) * q * q);
+  return SPHP_OK;
+}
+
+int sphp_tables_sizes(const sphp_tables* t, int64_t* nmodes, int64_t* npoints, int* dim) {
+  if (!t) return fail(SPHP_ERR_BAD_ARG, "null tables");
+  if (nmodes) *nmodes = t->nm;
+  if (npoints) *npoints = t->np;
+  if (dim) *dim = t->dim;
+  return SPHP_OK;
+}
+
+int64_t sphp_geom_stride(const sphp_tables* t, int kind) {
+  if (!t) return -1;
+  return geom_record(t, kind);
+}
+
+// geometry.geom_factors (geometry.py:125-142) for analytic structured maps
+int sphp_geom_analytic(const sphp_tables* tc, int kind, int mapping, int n, const double* lengths,
+                       double amp, int64_t e0, int64_t E, const int64_t* ids, double* geom,
+                       sphp_stream stream) {
+  sphp_tables* t = const_cast<sphp_tables*>(tc);
+  if (!t || !geom || n < 1 || E < 0) return fail(SPHP_ERR_BAD_ARG, "bad geometry arguments");
+  if (t->dim < 2) return fail(SPHP_ERR_UNSUPPORTED, "analytic geometry needs quad or hex");
+  for (int a = 1; a < t->dim; ++a)
+    if (t->q[a] != t->q[0]) return fail(SPHP_ERR_UNSUPPORTED, "analytic geometry needs equal Q per direction");
+  if (kind != SPHP_GEOM_AFFINE && kind != SPHP_GEOM_POINT && kind != SPHP_GEOM_METRIC)
+    return fail(SPHP_ERR_BAD_ARG, "unknown geometry encoding");
+  if (kind == SPHP_GEOM_AFFINE && mapping != SPHP_MAP_AFFINE)
+    return fail(SPHP_ERR_BAD_ARG, "AFFINE encoding needs an affine map (constant Jacobian)");
+  if ((mapping == SPHP_MAP_QUAD_SINE && t->dim != 2) || (mapping == SPHP_MAP_HEX_SINE && t->dim != 3))
+    return fail(SPHP_ERR_BAD_ARG, "mapping does not match the element dimension");
+  int rc = tables_device(t);
+  if (rc) return rc;
+  GeomJob j;
+  j.dim = t->dim;
+  j.Q = t->q[0];
+  j.n = n;
+  j.kind = kind;
+  j.mapping = mapping;
+  j.E = E;
+  j.e0 = e0;
+  j.npts = t->np;
+  j.cs = (t->np + 1) & ~1LL;
+  j.stride = geom_record(t, kind);
+  j.ids = ids;
+  j.z = t->d_z.as<double>();
+  j.w = t->d_w.as<double>();
+  for (int a = 0; a < 3; ++a) j.L[a] = lengths ? lengths[a < t->dim ? a : 0] : 1.0;
+  j.amp = amp;
+  j.out = geom;
+  int* bad = nullptr;
+  CK(cudaMalloc(&bad, sizeof(int)));
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int), s);
+  if (e == cudaSuccess) e = geom_analytic(j, bad, s);
+  int hbad = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(bad);
+  if (e != cudaSuccess) return cuda_fail(e, "sphp_geom_analytic");
+  if (hbad)  // geometry.py:133-136 GeometryError wording
+    return fail(SPHP_ERR_BAD_ARG, "non-positive Jacobian at quadrature point(s); invalid element");
+  return SPHP_OK;
+}
+
+int sphp_geom_from_factors(const sphp_tables* tc, int kind, int64_t E, const double* wj,
+                           const double* inv, double* geom, sphp_stream stream) {
+  sphp_tables* t = const_cast<sphp_tables*>(tc);
+  if (!t || !wj || !inv || !geom) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  if (kind != SPHP_GEOM_POINT && kind != SPHP_GEOM_METRIC)
+    return fail(SPHP_ERR_BAD_ARG, "from_factors produces POINT or METRIC encodings");
+  GeomJob j;
+  std::memset(&j, 0, sizeof(j));
+  j.dim = t->dim;
+  j.kind = kind;
+  j.E = E;
+  j.npts = t->np;
+  j.cs = (t->np + 1) & ~1LL;
+  j.stride = geom_record(t, kind);
+  j.out = geom;
+  int* bad = nullptr;
+  CK(cudaMalloc(&bad, sizeof(int)));
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int), s);
+  if (e == cudaSuccess) e = geom_convert(j, wj, inv, bad, s);
+  int hbad = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(bad);
+  if (e != cudaSuccess) return cuda_fail(e, "sphp_geom_from_factors");
+  if (hbad) return fail(SPHP_ERR_BAD_ARG, "non-positive world weight (w*|J|) in GeomFactors");
+  return SPHP_OK;
+}
+
+// collections.Collection.__init__ (collections.py:79-129)
+int sphp_collection_create(const sphp_tables* tc, int op, int strategy, int64_t E, int geom_kind,
+                           const double* geom, double lambda, sphp_coll** out) {
+  sphp_tables* t = const_cast<sphp_tables*>(tc);
+  if (!t || !out) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  if (E < 1) return fail(SPHP_ERR_BAD_ARG, "empty element group");  // collections.py:63-64
+  if (op < SPHP_OP_BWD_TRANS || op > SPHP_OP_HELMHOLTZ) return fail(SPHP_ERR_BAD_ARG, "unknown operator");
+  if (strategy != SPHP_STRATEGY_CUDA_SUMFAC && strategy != SPHP_STRATEGY_CUDA_STDMAT)
+    return fail(SPHP_ERR_BAD_ARG, "strategy must be concrete");  // collections.py:80-81
+  if (t->dim < 2) return fail(SPHP_ERR_UNSUPPORTED, "segment collections are not built on the GPU");
+  if (geom_kind < SPHP_GEOM_NONE || geom_kind > SPHP_GEOM_METRIC)
+    return fail(SPHP_ERR_BAD_ARG, "unknown geometry encoding");
+  if (geom_kind != SPHP_GEOM_NONE && !geom) return fail(SPHP_ERR_BAD_ARG, "geometry pointer is null");
+  if (op == SPHP_OP_HELMHOLTZ) {
+    if (geom_kind != SPHP_GEOM_METRIC && geom_kind != SPHP_GEOM_AFFINE)
+      return fail(SPHP_ERR_BAD_ARG, "Helmholtz needs METRIC or AFFINE geometry");
+  } else if (geom_kind == SPHP_GEOM_METRIC) {
+    return fail(SPHP_ERR_BAD_ARG, "METRIC geometry is specific to the Helmholtz operator");
+  }
+  if (op == SPHP_OP_BWD_TRANS && geom_kind != SPHP_GEOM_NONE) geom_kind = SPHP_GEOM_NONE;
+  if (strategy == SPHP_STRATEGY_CUDA_SUMFAC && !t->fast)
+    return fail(SPHP_ERR_UNSUPPORTED,
+                "sumfac kernels cover Modified_A/GLL with Q = P+2 or P+3 (hex P <= 8, quad P <= 9); "
+                "use the stdmat strategy for this key");
+  int rc = ensure_tables_uploaded();
+  if (rc) return rc;
+  rc = tables_device(t);
+  if (rc) return rc;
+  auto* c = new sphp_coll();
+  c->t = t;
+  c->op = op;
+  c->strategy = strategy;
+  c->E = E;
+  c->geom_kind = geom_kind;
+  c->geom = geom;
+  c->gstride = geom_record(t, geom_kind);
+  c->cs = (t->np + 1) & ~1LL;
+  c->lam = lambda;
+  const int d = t->dim;
+  switch (op) {
+    case SPHP_OP_BWD_TRANS: c->in_size = t->nm; c->out_size = t->np; break;
+    case SPHP_OP_IPRODUCT_WRT_BASE: c->in_size = t->np; c->out_size = t->nm; break;
+    case SPHP_OP_PHYS_DERIV: c->in_size = t->np; c->out_size = d * t->np; break;
+    case SPHP_OP_IPRODUCT_WRT_DERIV_BASE: c->in_size = d * t->np; c->out_size = t->nm; break;
+    case SPHP_OP_HELMHOLTZ: c->in_size = t->nm; c->out_size = t->nm; break;
+  }
+  *out = c;
+  return SPHP_OK;
+}
+
+int sphp_collection_destroy(sphp_coll* c) {
+  delete c;
+  return SPHP_OK;
+}
+
+int sphp_collection_set_lambda(sphp_coll* c, double lambda) {
+  if (!c) return fail(SPHP_ERR_BAD_ARG, "null collection");
+  if (c->strategy == SPHP_STRATEGY_CUDA_STDMAT && c->helm_H.p && lambda != c->lam) {
+    cudaFree(c->helm_H.p);  // dense H_e depends on lambda: rebuild lazily
+    c->helm_H.p = nullptr;
+    c->helm_H.bytes = 0;
+  }
+  c->lam = lambda;
+  return SPHP_OK;
+}
+
+int sphp_collection_info(const sphp_coll* c, int64_t* in_size, int64_t* out_size, int64_t* macs,
+                         int64_t* bytes) {
+  if (!c) return fail(SPHP_ERR_BAD_ARG, "null collection");
+  if (in_size) *in_size = c->in_size;
+  if (out_size) *out_size = c->out_size;
+  if (macs) *macs = mac_count(c);
+  if (bytes) *bytes = hbm_bytes(c);
+  return SPHP_OK;
+}
+
+// collections.Collection.apply (collections.py:189-246)
+int sphp_apply(sphp_coll* c, int64_t E, int64_t n_in, const double* in, double* out, sphp_stream stream) {
+  if (!c) return fail(SPHP_ERR_BAD_ARG, "null collection");
+  if (E != c->E || n_in != c->in_size) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "block shape (%lld, %lld) does not match (%lld, %lld)", (long long)E,
+                  (long long)n_in, (long long)c->E, (long long)c->in_size);
+    return fail(SPHP_ERR_BAD_SHAPE, buf);
+  }
+  if (!in || !out) return fail(SPHP_ERR_BAD_ARG, "null buffer");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c->strategy == SPHP_STRATEGY_CUDA_STDMAT) return stdmat_apply(c, in, out, s);
+  OpArgs a = base_args(c);
+  a.in = in;
+  a.out = out;
+  cudaError_t e = sumfac_launch(c, a, s);
+  if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no sum-factorisation kernel for this key");
+  if (e != cudaSuccess) return cuda_fail(e, "sphp_apply");
+  return SPHP_OK;
+}
+
+int sphp_apply_host(sphp_coll* c, int64_t E, int64_t n_in, const double* in, double* out,
+                    sphp_stream stream) {
+  if (!c) return fail(SPHP_ERR_BAD_ARG, "null collection");
+  if (E != c->E || n_in != c->in_size) return sphp_apply(c, E, n_in, in, out, stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bi = sizeof(double) * c->E * c->in_size, bo = sizeof(double) * c->E * c->out_size;
+  CK(c->host_in.ensure(bi));
+  CK(c->host_out.ensure(bo));
+  CK(cudaMemcpyAsync(c->host_in.p, in, bi, cudaMemcpyHostToDevice, s));
+  int rc = sphp_apply(c, E, n_in, c->host_in.as<double>(), c->host_out.as<double>(), stream);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out, c->host_out.p, bo, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return SPHP_OK;
+}
+
+// ---- assembly ---------------------------------------------------------------
+static int amap_colour_and_upload(sphp_amap* a) {
+  // greedy colouring in element order: elements sharing a global dof get
+  // distinct colours (deterministic)
+  std::vector<uint64_t> mask(a->num_global, 0);
+  std::vector<int> col(a->E, 0);
+  int ncol = 0;
+  for (int64_t e = 0; e < a->E; ++e) {
+    uint64_t used = 0;
+    for (int k = 0; k < a->nm; ++k) {
+      int64_t c = a->codes_host[e * a->nm + k];
+      int64_t g = c >= 0 ? c : (c == -1 ? -1 : -c - 2);
+      if (g >= 0) used |= mask[g];
+    }
+    int cc = 0;
+    while (cc < 64 && (used >> cc) & 1) ++cc;
+    if (cc == 64) return fail(SPHP_ERR_UNSUPPORTED, "element graph needs more than 64 colours");
+    col[e] = cc;
+    ncol = std::max(ncol, cc + 1);
+    for (int k = 0; k < a->nm; ++k) {
+      int64_t c = a->codes_host[e * a->nm + k];
+      int64_t g = c >= 0 ? c : (c == -1 ? -1 : -c - 2);
+      if (g >= 0) mask[g] |= (1ull << cc);
+    }
+  }
+  a->ncolours = ncol;
+  a->colour_off.assign(ncol + 1, 0);
+  for (int64_t e = 0; e < a->E; ++e) a->colour_off[col[e] + 1]++;
+  for (int c = 0; c < ncol; ++c) a->colour_off[c + 1] += a->colour_off[c];
+  std::vector<int> elist(a->E);
+  std::vector<int64_t> fill(a->colour_off.begin(), a->colour_off.end() - 1);
+  for (int64_t e = 0; e < a->E; ++e) elist[fill[col[e]]++] = (int)e;
+  a->elist_host = std::move(elist);
+  return SPHP_OK;
+}
+
+// device copies of an explicit map, made on first device use
+static int amap_device(const sphp_amap* ac) {
+  sphp_amap* a = const_cast<sphp_amap*>(ac);
+  if (a->periodic || a->d_codes.p) return SPHP_OK;
+  std::lock_guard<std::mutex> lk(a->mu);
+  if (a->d_codes.p) return SPHP_OK;
+  std::vector<int> codes32(a->codes_host.size());
+  for (size_t i = 0; i < codes32.size(); ++i) codes32[i] = (int)a->codes_host[i];
+  CK(a->d_elist.ensure(sizeof(int) * a->elist_host.size()));
+  CK(cudaMemcpy(a->d_elist.p, a->elist_host.data(), sizeof(int) * a->elist_host.size(),
+                cudaMemcpyHostToDevice));
+  DevBuf tmp;
+  CK(tmp.ensure(sizeof(int) * codes32.size()));
+  CK(cudaMemcpy(tmp.p, codes32.data(), sizeof(int) * codes32.size(), cudaMemcpyHostToDevice));
+  std::swap(a->d_codes.p, tmp.p);
+  std::swap(a->d_codes.bytes, tmp.bytes);
+  return SPHP_OK;
+}
+
+int sphp_amap_create_explicit(int64_t E, int nmodes, const int64_t* codes, int64_t num_global,
+                              sphp_amap** out) {
+  if (!out || !codes || E < 1 || nmodes < 1 || num_global < 0) return fail(SPHP_ERR_BAD_ARG, "bad map arguments");
+  if (num_global > 2147483645LL) return fail(SPHP_ERR_UNSUPPORTED, "more than 2^31-3 global dofs");
+  for (int64_t i = 0; i < E * nmodes; ++i) {
+    int64_t c = codes[i];
+    int64_t g = c >= 0 ? c : (c == -1 ? -1 : -c - 2);
+    if (g >= num_global) return fail(SPHP_ERR_BAD_ARG, "map code outside [0, num_global)");
+  }
+  auto* a = new sphp_amap();
+  a->nm = nmodes;
+  a->E = E;
+  a->num_global = num_global;
+  a->codes_host.assign(codes, codes + E * nmodes);
+  int rc = amap_colour_and_upload(a);
+  if (rc) {
+    delete a;
+    return rc;
+  }
+  *out = a;
+  return SPHP_OK;
+}
+
+int sphp_amap_create_hex_periodic(int n, int P, sphp_amap** out) {
+  if (!out || n < 1 || P < 1) return fail(SPHP_ERR_BAD_ARG, "bad periodic map arguments");
+  if (n % 2) return fail(SPHP_ERR_UNSUPPORTED, "parity colouring of a periodic grid needs even n");
+  auto* a = new sphp_amap();
+  a->periodic = 1;
+  a->n = n;
+  a->P = P;
+  a->nm = (P + 1) * (P + 1) * (P + 1);
+  a->E = (int64_t)n * n * n;
+  a->num_global = ipow((int64_t)n * P, 3);
+  a->ncolours = 8;
+  *out = a;
+  return SPHP_OK;
+}
+
+// numbering of oracle/assembly.py hex_periodic + build_map, variable order
+int sphp_hexmap_variable(int n, const int* orders, int64_t* num_global, int64_t* offsets, int64_t* codes) {
+  if (n < 1 || !orders || !num_global) return fail(SPHP_ERR_BAD_ARG, "bad arguments");
+  const int64_t N3 = (int64_t)n * n * n;
+  auto vid = [n](int i, int j, int k) -> int64_t {
+    i %= n;
+    j %= n;
+    k %= n;
+    return i + (int64_t)n * (j + (int64_t)n * k);
+  };
+  for (int64_t e = 0; e < N3; ++e)
+    if (orders[e] < 1) return fail(SPHP_ERR_BAD_ARG, "orders must be >= 1");
+  std::vector<int> eord(3 * N3, 1 << 30), ford(3 * N3, 1 << 30);
+  for (int ez = 0; ez < n; ++ez)
+    for (int ey = 0; ey < n; ++ey)
+      for (int ex = 0; ex < n; ++ex) {
+        const int P = orders[ex + (int64_t)n * (ey + (int64_t)n * ez)];
+        const int b[3] = {ex, ey, ez};
+        for (int d = 0; d < 3; ++d) {
+          for (int s = 0; s < 2; ++s)
+            for (int t2 = 0; t2 < 2; ++t2) {
+              int o[3];
+              int oo[2] = {s, t2}, c = 0;
+              for (int a = 0; a < 3; ++a) o[a] = (a == d) ? 0 : oo[c++];
+              int64_t eid = d * N3 + vid(b[0] + o[0], b[1] + o[1], b[2] + o[2]);
+              eord[eid] = std::min(eord[eid], P);
+            }
+          for (int side = 0; side < 2; ++side) {
+            int o[3] = {0, 0, 0};
+            o[d] = side;
+            int64_t fid = d * N3 + vid(b[0] + o[0], b[1] + o[1], b[2] + o[2]);
+            ford[fid] = std::min(ford[fid], P);
+          }
+        }
+      }
+  std::vector<int64_t> eoff(3 * N3 + 1, 0), foff(3 * N3 + 1, 0);
+  for (int64_t i = 0; i < 3 * N3; ++i) {
+    eoff[i + 1] = eoff[i] + std::max(0, eord[i] - 1);
+    foff[i + 1] = foff[i] + (int64_t)std::max(0, ford[i] - 1) * std::max(0, ford[i] - 1);
+  }
+  const int64_t ebase = N3, fbase = N3 + eoff[3 * N3], ibase = fbase + foff[3 * N3];
+  int64_t gid = ibase;
+  int64_t off = 0;
+  for (int ez = 0; ez < n; ++ez)
+    for (int ey = 0; ey < n; ++ey)
+      for (int ex = 0; ex < n; ++ex) {
+        const int64_t e = ex + (int64_t)n * (ey + (int64_t)n * ez);
+        const int P = orders[e], m = P + 1;
+        const int b[3] = {ex, ey, ez};
+        if (offsets) offsets[e] = off;
+        for (int p = 0; p < m; ++p)
+          for (int q = 0; q < m; ++q)
+            for (int r = 0; r < m; ++r) {
+              const int idx[3] = {p, q, r};
+              const int nb = (p >= 2) + (q >= 2) + (r >= 2);
+              int64_t g = -1;
+              if (nb == 0) {
+                g = vid(ex + p, ey + q, ez + r);
+              } else if (nb == 1) {
+                const int d = (p >= 2) ? 0 : ((q >= 2) ? 1 : 2);
+                int c[3];
+                for (int a = 0; a < 3; ++a) c[a] = b[a] + (a == d ? 0 : idx[a]);
+                const int64_t eid = d * N3 + vid(c[0], c[1], c[2]);
+                if (idx[d] <= eord[eid]) g = ebase + eoff[eid] + (idx[d] - 2);
+              } else if (nb == 2) {
+                const int d = (p < 2) ? 0 : ((q < 2) ? 1 : 2);
+                int c[3];
+                for (int a = 0; a < 3; ++a) c[a] = b[a] + (a == d ? idx[a] : 0);
+                const int64_t fid = d * N3 + vid(c[0], c[1], c[2]);
+                const int k1 = (d == 0) ? q : p, k2 = (d == 2) ? q : r;
+                const int pf = ford[fid];
+                if (k1 <= pf && k2 <= pf) g = fbase + foff[fid] + (int64_t)(k1 - 2) * (pf - 1) + (k2 - 2);
+              } else {
+                g = -2;  // interior: numbered below in local order
+              }
+              if (g == -2) g = gid++;
+              if (codes) codes[off] = g;  // signs are all +1 on the structured grid
+              ++off;
+            }
+      }
+  if (offsets) offsets[N3] = off;
+  *num_global = gid;
+  return SPHP_OK;
+}
+
+int sphp_amap_destroy(sphp_amap* a) {
+  delete a;
+  return SPHP_OK;
+}
+
+int sphp_amap_info(const sphp_amap* a, int64_t* ne, int* nm, int64_t* ng, int* nc) {
+  if (!a) return fail(SPHP_ERR_BAD_ARG, "null map");
+  if (ne) *ne = a->E;
+  if (nm) *nm = a->nm;
+  if (ng) *ng = a->num_global;
+  if (nc) *nc = a->ncolours;
+  return SPHP_OK;
+}
+
+int sphp_amap_codes(const sphp_amap* a, int64_t* codes) {
+  if (!a || !codes) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  if (!a->periodic) {
+    std::memcpy(codes, a->codes_host.data(), sizeof(int64_t) * a->codes_host.size());
+    return SPHP_OK;
+  }
+  std::vector<int> orders((size_t)a->E, a->P);
+  int64_t ng;
+  return sphp_hexmap_variable(a->n, orders.data(), &ng, nullptr, codes);
+}
+
+int sphp_scatter(const sphp_amap* a, const double* g, double* loc, sphp_stream stream) {
+  if (!a || !g || !loc) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  if (int rc = amap_device(a)) return rc;
+  CK(amap_scatter(a->dev(), g, loc, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int sphp_assemble(const sphp_amap* a, const double* loc, double* g, sphp_stream stream) {
+  if (!a || !g || !loc) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  if (int rc = amap_device(a)) return rc;
+  CK(amap_assemble(a->dev(), loc, g, a->ncolours, a->d_elist.as<int>(), a->colour_off.data(), 0,
+                   (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+// assembly.GlobalSystem.apply (assembly.py:177-182), fused
+int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, double* y, int accumulate,
+                             sphp_stream stream) {
+  if (!c || !a || !x || !y) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  if (c->op != SPHP_OP_HELMHOLTZ) return fail(SPHP_ERR_BAD_ARG, "collection is not a Helmholtz operator");
+  if (a->E != c->E || a->nm != c->t->nm)
+    return fail(SPHP_ERR_BAD_SHAPE, "assembly map and collection disagree on (E, nmodes)");
+  if (a->periodic && c->t->shape != SPHP_SHAPE_HEX)
+    return fail(SPHP_ERR_BAD_ARG, "periodic analytic maps are hexahedral");
+  if (int rc = amap_device(a)) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c->strategy == SPHP_STRATEGY_CUDA_STDMAT) {
+    int rc = stdmat_prepare(c, s);
+    if (rc) return rc;
+    CK(c->loc_x.ensure(sizeof(double) * c->E * c->t->nm));
+    CK(c->loc_y.ensure(sizeof(double) * c->E * c->t->nm));
+    CK(amap_scatter(a->dev(), x, c->loc_x.as<double>(), s));
+    CK(elem_matvec(c->E, (int)c->t->nm, c->helm_H.as<double>(), c->loc_x.as<double>(), c->loc_y.as<double>(), s));
+    CK(amap_assemble(a->dev(), c->loc_y.as<double>(), y, a->ncolours, a->d_elist.as<int>(),
+                     a->colour_off.data(), accumulate, s));
+    return SPHP_OK;
+  }
+  if (!accumulate) CK(cudaMemsetAsync(y, 0, sizeof(double) * a->num_global, s));
+  OpArgs o = base_args(c);
+  o.xg = x;
+  o.yg = y;
+  for (int col = 0; col < a->ncolours; ++col) {
+    if (a->periodic) {
+      o.mode = AsmMode::PERIODIC;
+      o.n = a->n;
+      o.colour = col;
+      o.nlist = (int64_t)(a->n / 2) * (a->n / 2) * (a->n / 2);
+    } else {
+      o.mode = AsmMode::EXPLICIT;
+      o.codes = a->d_codes.as<int>();
+      o.elist = a->d_elist.as<int>() + a->colour_off[col];
+      o.nlist = a->colour_off[col + 1] - a->colour_off[col];
+    }
+    cudaError_t e = sumfac_launch(c, o, s);
+    if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no assembled kernel for this key");
+    if (e != cudaSuccess) return cuda_fail(e, "sphp_helmholtz_assembled");
+  }
+  return SPHP_OK;
+}
+
+}  // extern "C"

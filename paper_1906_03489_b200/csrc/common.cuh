@@ -1,0 +1,133 @@
+// Shared device-side machinery for the spechp B200 kernels:
+//   * the constant-memory table pool for the fast (GLL, Modified_A) keys,
+//   * TMA bulk-copy (cp.async.bulk) + mbarrier helpers for sm_100a,
+//   * the pencil contraction used by every sum-factorisation stage.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sphp {
+
+// ---------------------------------------------------------------------------
+// Fast-path key set: Modified_A modes M per direction with GLL Q = M+1
+// (the reference default, stdregions.py:376-381) or Q = M+2 (the BASELINE
+// configs).  Each key's tables live in __constant__ memory so the unrolled
+// contractions take their coefficients as DFMA constant operands.
+// ---------------------------------------------------------------------------
+constexpr int FAST_M_MIN = 2;
+constexpr int FAST_M_MAX = 10;
+
+__host__ __device__ constexpr int tab_size(int M, int Q) { return 2 * M * Q + Q * Q + Q; }
+__host__ __device__ constexpr bool fast_key(int M, int Q) {
+  return M >= FAST_M_MIN && M <= FAST_M_MAX && (Q == M + 1 || Q == M + 2);
+}
+__host__ __device__ constexpr int tab_off(int M, int Q) {
+  int off = 0;
+  for (int m = FAST_M_MIN; m <= FAST_M_MAX; ++m)
+    for (int q = m + 1; q <= m + 2; ++q) {
+      if (m == M && q == Q) return off;
+      off += tab_size(m, q);
+    }
+  return -1;
+}
+constexpr int TAB_TOTAL = tab_off(FAST_M_MAX, FAST_M_MAX + 2) + tab_size(FAST_M_MAX, FAST_M_MAX + 2);
+
+// layout inside one key: B[M][Q], Bd[M][Q], D[Q][Q], w[Q]
+template <int M, int Q>
+struct Tab {
+  static constexpr int B = tab_off(M, Q);
+  static constexpr int BD = B + M * Q;
+  static constexpr int D = BD + M * Q;
+  static constexpr int W = D + Q * Q;
+};
+
+// host: the full pool (computed once, uploaded to every TU's bank)
+const double* fast_table_pool();
+
+// ---------------------------------------------------------------------------
+// PTX helpers (sm_90+ bulk async copies; SASS UBLKCP / SYNCS)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0,
+// both addresses 16-byte aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// shared -> global bulk copy (bulk_group completion)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
+// Pencil contraction: out[o*OS] (+)= sum_l T(o,l) in[l*IS], T(o,l) read from
+// constant memory at TOFF + o*TSO + l*TSI.  Summation order l = 0..NIN-1
+// (fixed, so repeated applies are bitwise identical).
+// ---------------------------------------------------------------------------
+template <int NIN, int NOUT, int TOFF, int TSO, int TSI, int IS, int OS, bool ACC>
+__device__ __forceinline__ void pencil(const double* tab, const double* __restrict__ in,
+                                       double* __restrict__ out) {
+  double x[NIN];
+#pragma unroll
+  for (int l = 0; l < NIN; ++l) x[l] = in[l * IS];
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o) {
+    double acc = ACC ? out[o * OS] : 0.0;
+#pragma unroll
+    for (int l = 0; l < NIN; ++l) acc = fma(tab[TOFF + o * TSO + l * TSI], x[l], acc);
+    out[o * OS] = acc;
+  }
+}
+
+__host__ __device__ constexpr int odd_up(int x) { return x | 1; }
+
+}  // namespace sphp
+
+// every kernel TU declares its own constant bank with this macro and
+// registers an uploader that the host calls once per device
+#define SPHP_DECLARE_TABLE_BANK(NAME)                                              \
+  static __constant__ double c_tab[sphp::TAB_TOTAL];                               \
+  namespace sphp {                                                                 \
+  cudaError_t upload_tables_##NAME() {                                             \
+    return cudaMemcpyToSymbol(c_tab, fast_table_pool(), sizeof(double) * TAB_TOTAL); \
+  }                                                                                \
+  }

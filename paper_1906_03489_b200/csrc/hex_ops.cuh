@@ -1,0 +1,484 @@
+// Hexahedral sum-factorisation operators (the 3D generalisation of
+// collections.py:133-185 and geometry.py:145-184).
+//
+// Per-element layouts (first direction slowest, stdregions.py:1-14):
+//   coefficients c[(p*M + q)*M + r], points u[(i*Q + j)*Q + k].
+// Shared-memory work tensors use an odd row pitch QK = Q|1 in the fastest
+// direction so pencil reads along k are bank-conflict free for FP64.
+//
+// Tables (B, Bd = dB/dxi, D, w) are read from __constant__ memory with
+// compile-time indices (c_tab must be declared by the including TU).
+#pragma once
+#include "pipeline.cuh"
+
+namespace sphp {
+
+// per-element geometry record sizes (see sphp_geom_stride)
+__host__ __device__ constexpr int pt_stride(int npts) { return even_up(npts); }
+
+// work-item loop: items are distributed over the CTA's NT threads
+#define SPHP_FOR_ITEMS(NITEMS, w) for (int w = threadIdx.x; w < (NITEMS); w += NT)
+
+// ===========================================================================
+// Fused matrix-free Helmholtz (K4): y = sum_ab B_a^T G_ab B_b uhat + lam B^T wJ B uhat
+// stages S1..S9; no quadrature data leaves shared memory.
+// GK: SPHP_GEOM_METRIC (7 per-point comps) or SPHP_GEOM_AFFINE (det, inv).
+// ===========================================================================
+template <int M_, int Q_, int GK, int NE_, int NT_>
+struct HexHelm {
+  static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
+  static constexpr int IN = M3, OUT = M3;
+  static constexpr int CS = pt_stride(Q3);
+  static constexpr int GEO = (GK == SPHP_GEOM_METRIC) ? 7 * CS : 10;
+  static constexpr int QK = odd_up(Q);
+  static constexpr int SW = odd_up(Q * Q * QK);
+  static constexpr int WORK = 3 * SW;
+  using T = Tab<M, Q>;
+
+  template <class R, class W>
+  __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
+                                 double* __restrict__ work, double* __restrict__ out, double lam,
+                                 R release, W pre_out, const double* tab) {
+    double* W0 = work;            // T1 (M,M,QK) | u / t (Q,Q,QK)
+    double* W1 = work + NE * SW;  // T2 (M,Q,QK) | d2 / f2
+    double* W2 = work + 2 * NE * SW;  // d0 / f0
+
+    // S1: r-contraction  c[p,q,r] -> T1[p,q,k]
+    SPHP_FOR_ITEMS(NE * M * M, w) {
+      int e = w / (M * M), pq = w - e * (M * M);
+      pencil<M, Q, T::B, 1, Q, 1, 1, false>(tab, cin + e * M3 + pq * M, W0 + e * SW + pq * QK);
+    }
+    __syncthreads();
+    // S2: q-contraction  T1[p,q,k] -> T2[p,j,k]
+    SPHP_FOR_ITEMS(NE * M * Q, w) {
+      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
+      pencil<M, Q, T::B, 1, Q, QK, QK, false>(tab, W0 + e * SW + p * M * QK + k,
+                                              W1 + e * SW + p * Q * QK + k);
+    }
+    __syncthreads();
+    // S3: p-contraction  T2 -> u (W0) and d0 = Bd-contraction (W2)
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
+      const double* src = W1 + e * SW + j * QK + k;
+      double x[M];
+#pragma unroll
+      for (int p = 0; p < M; ++p) x[p] = src[p * Q * QK];
+      double* du = W0 + e * SW + j * QK + k;
+      double* d0 = W2 + e * SW + j * QK + k;
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int p = 0; p < M; ++p) {
+          a = fma(tab[T::B + p * Q + i], x[p], a);
+          b = fma(tab[T::BD + p * Q + i], x[p], b);
+        }
+        du[i * Q * QK] = a;
+        d0[i * Q * QK] = b;
+      }
+    }
+    __syncthreads();
+    // S4: d2 = D along k of u
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), ij = w - e * (Q * Q);
+      pencil<Q, Q, T::D, Q, 1, 1, 1, false>(tab, W0 + e * SW + ij * QK, W1 + e * SW + ij * QK);
+    }
+    __syncthreads();
+    // S5: pencil along j: d1 = D u, fluxes f = G grad u, t = lam wJ u + D1^T f1
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
+      const int base = e * SW + i * Q * QK + k;
+      double u[Q], f1[Q];
+#pragma unroll
+      for (int j = 0; j < Q; ++j) u[j] = W0[base + j * QK];
+      const double* g = geo + e * GEO;
+      double a00, a01, a02, a11, a12, a22, adet;
+      if (GK == SPHP_GEOM_AFFINE) {
+        // G_ab = det * sum_k inv[a,k] inv[b,k] (point weights applied below)
+        const double det = g[0];
+        const double* iv = g + 1;
+        a00 = det * (iv[0] * iv[0] + iv[1] * iv[1] + iv[2] * iv[2]);
+        a01 = det * (iv[0] * iv[3] + iv[1] * iv[4] + iv[2] * iv[5]);
+        a02 = det * (iv[0] * iv[6] + iv[1] * iv[7] + iv[2] * iv[8]);
+        a11 = det * (iv[3] * iv[3] + iv[4] * iv[4] + iv[5] * iv[5]);
+        a12 = det * (iv[3] * iv[6] + iv[4] * iv[7] + iv[5] * iv[8]);
+        a22 = det * (iv[6] * iv[6] + iv[7] * iv[7] + iv[8] * iv[8]);
+        adet = det;
+      }
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        double d1 = 0.0;
+#pragma unroll
+        for (int l = 0; l < Q; ++l) d1 = fma(tab[T::D + j * Q + l], u[l], d1);
+        const double d0 = W2[base + j * QK];
+        const double d2 = W1[base + j * QK];
+        double G00, G01, G02, G11, G12, G22, wj;
+        if (GK == SPHP_GEOM_METRIC) {
+          const int pt = (i * Q + j) * Q + k;
+          G00 = g[0 * CS + pt];
+          G01 = g[1 * CS + pt];
+          G02 = g[2 * CS + pt];
+          G11 = g[3 * CS + pt];
+          G12 = g[4 * CS + pt];
+          G22 = g[5 * CS + pt];
+          wj = g[6 * CS + pt];
+        } else {
+          const double wq = tab[T::W + i] * tab[T::W + j] * tab[T::W + k];
+          G00 = wq * a00;
+          G01 = wq * a01;
+          G02 = wq * a02;
+          G11 = wq * a11;
+          G12 = wq * a12;
+          G22 = wq * a22;
+          wj = wq * adet;
+        }
+        const double f0 = G00 * d0 + G01 * d1 + G02 * d2;
+        f1[j] = G01 * d0 + G11 * d1 + G12 * d2;
+        const double f2 = G02 * d0 + G12 * d1 + G22 * d2;
+        W2[base + j * QK] = f0;
+        W1[base + j * QK] = f2;
+        u[j] = lam * wj * u[j];  // mass term, reuses u's registers
+      }
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        double t = u[j];
+#pragma unroll
+        for (int l = 0; l < Q; ++l) t = fma(tab[T::D + l * Q + j], f1[l], t);
+        W0[base + j * QK] = t;
+      }
+    }
+    __syncthreads();
+    release();
+    // S6: t += D2^T f2 along k
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), ij = w - e * (Q * Q);
+      pencil<Q, Q, T::D, 1, Q, 1, 1, true>(tab, W1 + e * SW + ij * QK, W0 + e * SW + ij * QK);
+    }
+    __syncthreads();
+    // S7: i -> p: T2'[p,j,k] = sum_i B[p,i] t + Bd[p,i] f0   (into W1)
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
+      const int base = e * SW + j * QK + k;
+      double t[Q], f0[Q];
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        t[i] = W0[base + i * Q * QK];
+        f0[i] = W2[base + i * Q * QK];
+      }
+#pragma unroll
+      for (int p = 0; p < M; ++p) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          acc = fma(tab[T::B + p * Q + i], t[i], acc);
+          acc = fma(tab[T::BD + p * Q + i], f0[i], acc);
+        }
+        W1[e * SW + p * Q * QK + j * QK + k] = acc;
+      }
+    }
+    __syncthreads();
+    // S8: j -> q  (W1 -> W0)
+    SPHP_FOR_ITEMS(NE * M * Q, w) {
+      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
+      pencil<Q, M, T::B, Q, 1, QK, QK, false>(tab, W1 + e * SW + p * Q * QK + k,
+                                              W0 + e * SW + p * M * QK + k);
+    }
+    pre_out();
+    __syncthreads();
+    // S9: k -> r  (W0 -> out, dense)
+    SPHP_FOR_ITEMS(NE * M * M, w) {
+      int e = w / (M * M), pq = w - e * (M * M);
+      pencil<Q, M, T::B, Q, 1, 1, 1, false>(tab, W0 + e * SW + pq * QK, out + e * M3 + pq * M);
+    }
+  }
+};
+
+// ===========================================================================
+// BwdTrans (K1): u = (B x B x B)^T c   (collections.py:133-150)
+// ===========================================================================
+template <int M_, int Q_, int NE_, int NT_>
+struct HexBwd {
+  static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
+  static constexpr int IN = M3, OUT = Q3, GEO = 0;
+  static constexpr int QK = odd_up(Q);
+  static constexpr int SA = odd_up(M * M * QK), SB = odd_up(M * Q * QK);
+  static constexpr int WORK = SA + SB;
+  using T = Tab<M, Q>;
+
+  template <class R, class W>
+  __device__ static void compute(const double* __restrict__ cin, const double* __restrict__,
+                                 double* __restrict__ work, double* __restrict__ out, double,
+                                 R release, W pre_out, const double* tab) {
+    double* A = work;
+    double* Bb = work + NE * SA;
+    SPHP_FOR_ITEMS(NE * M * M, w) {
+      int e = w / (M * M), pq = w - e * (M * M);
+      pencil<M, Q, T::B, 1, Q, 1, 1, false>(tab, cin + e * M3 + pq * M, A + e * SA + pq * QK);
+    }
+    __syncthreads();
+    release();
+    SPHP_FOR_ITEMS(NE * M * Q, w) {
+      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
+      pencil<M, Q, T::B, 1, Q, QK, QK, false>(tab, A + e * SA + p * M * QK + k,
+                                              Bb + e * SB + p * Q * QK + k);
+    }
+    pre_out();
+    __syncthreads();
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
+      pencil<M, Q, T::B, 1, Q, Q * QK, Q * Q, false>(tab, Bb + e * SB + j * QK + k,
+                                                     out + e * Q3 + j * Q + k);
+    }
+  }
+};
+
+// ===========================================================================
+// IProductWRTBase (K2): c = (B x B x B) (W u)   (collections.py:152-167, 215-224)
+// GK: NONE (reference weights), AFFINE (w * det_e), POINT (staged wJ comp)
+// ===========================================================================
+template <int M_, int Q_, int GK, int NE_, int NT_>
+struct HexIprod {
+  static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
+  static constexpr int IN = Q3, OUT = M3;
+  static constexpr int CS = pt_stride(Q3);
+  static constexpr int GEO = (GK == SPHP_GEOM_POINT) ? CS : (GK == SPHP_GEOM_AFFINE ? 10 : 0);
+  static constexpr int QK = odd_up(Q);
+  static constexpr int SA = odd_up(M * M * QK), SB = odd_up(M * Q * QK);
+  static constexpr int WORK = SA + SB;
+  using T = Tab<M, Q>;
+
+  template <class R, class W>
+  __device__ static void compute(const double* __restrict__ uin, const double* __restrict__ geo,
+                                 double* __restrict__ work, double* __restrict__ out, double,
+                                 R release, W pre_out, const double* tab) {
+    double* A = work;
+    double* Bb = work + NE * SA;
+    // i -> p with the weights folded in (wu = W*u, collections.py:216)
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
+      double x[Q];
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        const int pt = (i * Q + j) * Q + k;
+        double wt;
+        if (GK == SPHP_GEOM_POINT)
+          wt = geo[e * GEO + pt];
+        else if (GK == SPHP_GEOM_AFFINE)
+          wt = tab[T::W + i] * tab[T::W + j] * tab[T::W + k] * geo[e * GEO];
+        else
+          wt = tab[T::W + i] * tab[T::W + j] * tab[T::W + k];
+        x[i] = wt * uin[e * Q3 + pt];
+      }
+#pragma unroll
+      for (int p = 0; p < M; ++p) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) acc = fma(tab[T::B + p * Q + i], x[i], acc);
+        Bb[e * SB + (p * Q + j) * QK + k] = acc;
+      }
+    }
+    __syncthreads();
+    release();
+    SPHP_FOR_ITEMS(NE * M * Q, w) {
+      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
+      pencil<Q, M, T::B, Q, 1, QK, QK, false>(tab, Bb + e * SB + p * Q * QK + k,
+                                              A + e * SA + p * M * QK + k);
+    }
+    pre_out();
+    __syncthreads();
+    SPHP_FOR_ITEMS(NE * M * M, w) {
+      int e = w / (M * M), pq = w - e * (M * M);
+      pencil<Q, M, T::B, Q, 1, 1, 1, false>(tab, A + e * SA + pq * QK, out + e * M3 + pq * M);
+    }
+  }
+};
+
+// ===========================================================================
+// PhysDeriv (K3): d_a = D_a u ; world dx_k = sum_a inv[a,k] d_a
+// (collections.py:169-185, 226-241).  Output (3, Q3) per element.
+// GK: NONE (reference components), AFFINE, POINT (staged inv comps 1..9)
+// ===========================================================================
+template <int M_, int Q_, int GK, int NE_, int NT_>
+struct HexPhysDeriv {
+  static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int Q3 = Q * Q * Q;
+  static constexpr int IN = Q3, OUT = 3 * Q3;
+  static constexpr int CS = pt_stride(Q3);
+  static constexpr int GEO = (GK == SPHP_GEOM_POINT) ? 9 * CS : (GK == SPHP_GEOM_AFFINE ? 10 : 0);
+  static constexpr int QK = odd_up(Q);
+  static constexpr int SW = odd_up(Q * Q * QK);
+  static constexpr int WORK = 2 * SW;
+  using T = Tab<M, Q>;
+
+  template <class R, class W>
+  __device__ static void compute(const double* __restrict__ uin, const double* __restrict__ geo,
+                                 double* __restrict__ work, double* __restrict__ out, double,
+                                 R release, W pre_out, const double* tab) {
+    double* W0 = work;
+    double* W1 = work + NE * SW;
+    // d0 (pencils along i) and d1 (pencils along j) in one stage
+    SPHP_FOR_ITEMS(2 * NE * Q * Q, w) {
+      const int half = w >= NE * Q * Q;
+      const int v = half ? w - NE * Q * Q : w;
+      int e = v / (Q * Q), ab = v - e * (Q * Q), a = ab / Q, b = ab - a * Q;
+      if (!half) {  // pencil along i at (j=a, k=b)
+        pencil<Q, Q, T::D, Q, 1, Q * Q, Q * Q * QK / Q, false>(
+            tab, uin + e * Q3 + a * Q + b, W0 + e * SW + a * QK + b);
+      } else {  // pencil along j at (i=a, k=b)
+        pencil<Q, Q, T::D, Q, 1, Q, QK, false>(tab, uin + e * Q3 + a * Q * Q + b,
+                                               W1 + e * SW + a * Q * QK + b);
+      }
+    }
+    pre_out();
+    __syncthreads();
+    // pencil along k: d2 in registers, metric transform, write 3 comps
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), ij = w - e * (Q * Q), i = ij / Q, j = ij - i * Q;
+      double x[Q];
+#pragma unroll
+      for (int k = 0; k < Q; ++k) x[k] = uin[e * Q3 + ij * Q + k];
+      const double* g = geo + e * GEO;
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        double d2 = 0.0;
+#pragma unroll
+        for (int l = 0; l < Q; ++l) d2 = fma(tab[T::D + k * Q + l], x[l], d2);
+        const double d0 = W0[e * SW + ij * QK + k];
+        const double d1 = W1[e * SW + ij * QK + k];
+        const int pt = ij * Q + k;
+        double o0 = d0, o1 = d1, o2 = d2;
+        if (GK != SPHP_GEOM_NONE) {
+          double iv[9];
+#pragma unroll
+          for (int c = 0; c < 9; ++c) iv[c] = (GK == SPHP_GEOM_POINT) ? g[c * CS + pt] : g[1 + c];
+          // dx_k = sum_a inv[a,k] d_a ; inv row-major [a*3 + k]
+          o0 = iv[0] * d0 + iv[3] * d1 + iv[6] * d2;
+          o1 = iv[1] * d0 + iv[4] * d1 + iv[7] * d2;
+          o2 = iv[2] * d0 + iv[5] * d1 + iv[8] * d2;
+        }
+        out[e * OUT + 0 * Q3 + pt] = o0;
+        out[e * OUT + 1 * Q3 + pt] = o1;
+        out[e * OUT + 2 * Q3 + pt] = o2;
+      }
+    }
+    __syncthreads();
+    release();
+  }
+};
+
+// ===========================================================================
+// IProductWRTDerivBase: c = sum_a B_a [ wJ sum_k inv[a,k] f_k ]
+// (geometry.py:163-168; batched form solvers.py:361-365).  Input (3, Q3).
+// GK: NONE (g_a = w f_a), AFFINE, POINT (staged comps 0..9 = wJ, inv)
+// ===========================================================================
+template <int M_, int Q_, int GK, int NE_, int NT_>
+struct HexIPDeriv {
+  static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
+  static constexpr int IN = 3 * Q3, OUT = M3;
+  static constexpr int CS = pt_stride(Q3);
+  static constexpr int GEO = (GK == SPHP_GEOM_POINT) ? 10 * CS : (GK == SPHP_GEOM_AFFINE ? 10 : 0);
+  static constexpr int QK = odd_up(Q);
+  static constexpr int SW = odd_up(Q * Q * QK);
+  static constexpr int WORK = 3 * SW;
+  using T = Tab<M, Q>;
+
+  template <class R, class W>
+  __device__ static void compute(const double* __restrict__ fin, const double* __restrict__ geo,
+                                 double* __restrict__ work, double* __restrict__ out, double,
+                                 R release, W pre_out, const double* tab) {
+    double* W0 = work;            // t
+    double* W1 = work + NE * SW;  // g0 | later T2'
+    double* W2 = work + 2 * NE * SW;  // g1 | later T1'
+    // pencil along k: g = wJ inv f ; t = D2^T g2
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), ij = w - e * (Q * Q), i = ij / Q, j = ij - i * Q;
+      const double* g = geo + e * GEO;
+      double g2[Q];
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        const int pt = ij * Q + k;
+        const double fx = fin[e * IN + pt], fy = fin[e * IN + Q3 + pt], fz = fin[e * IN + 2 * Q3 + pt];
+        double a0, a1, a2;
+        if (GK == SPHP_GEOM_NONE) {
+          const double wq = tab[T::W + i] * tab[T::W + j] * tab[T::W + k];
+          a0 = wq * fx;
+          a1 = wq * fy;
+          a2 = wq * fz;
+        } else {
+          double wj;
+          double iv[9];
+          if (GK == SPHP_GEOM_POINT) {
+            wj = g[pt];
+#pragma unroll
+            for (int c = 0; c < 9; ++c) iv[c] = g[(1 + c) * CS + pt];
+          } else {
+            wj = tab[T::W + i] * tab[T::W + j] * tab[T::W + k] * g[0];
+#pragma unroll
+            for (int c = 0; c < 9; ++c) iv[c] = g[1 + c];
+          }
+          a0 = wj * (iv[0] * fx + iv[1] * fy + iv[2] * fz);
+          a1 = wj * (iv[3] * fx + iv[4] * fy + iv[5] * fz);
+          a2 = wj * (iv[6] * fx + iv[7] * fy + iv[8] * fz);
+        }
+        W1[e * SW + ij * QK + k] = a0;
+        W2[e * SW + ij * QK + k] = a1;
+        g2[k] = a2;
+      }
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        double t = 0.0;
+#pragma unroll
+        for (int l = 0; l < Q; ++l) t = fma(tab[T::D + l * Q + k], g2[l], t);
+        W0[e * SW + ij * QK + k] = t;
+      }
+    }
+    __syncthreads();
+    release();
+    // t += D1^T g1 along j
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
+      pencil<Q, Q, T::D, 1, Q, QK, QK, true>(tab, W2 + e * SW + i * Q * QK + k,
+                                             W0 + e * SW + i * Q * QK + k);
+    }
+    __syncthreads();
+    // i -> p : T2'[p,j,k] = sum_i B t + Bd g0  (into W2)
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
+      const int base = e * SW + j * QK + k;
+      double t[Q], g0[Q];
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        t[i] = W0[base + i * Q * QK];
+        g0[i] = W1[base + i * Q * QK];
+      }
+#pragma unroll
+      for (int p = 0; p < M; ++p) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          acc = fma(tab[T::B + p * Q + i], t[i], acc);
+          acc = fma(tab[T::BD + p * Q + i], g0[i], acc);
+        }
+        W2[e * SW + (p * Q + j) * QK + k] = acc;
+      }
+    }
+    __syncthreads();
+    SPHP_FOR_ITEMS(NE * M * Q, w) {
+      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
+      pencil<Q, M, T::B, Q, 1, QK, QK, false>(tab, W2 + e * SW + p * Q * QK + k,
+                                              W0 + e * SW + p * M * QK + k);
+    }
+    pre_out();
+    __syncthreads();
+    SPHP_FOR_ITEMS(NE * M * M, w) {
+      int e = w / (M * M), pq = w - e * (M * M);
+      pencil<Q, M, T::B, Q, 1, 1, 1, false>(tab, W0 + e * SW + pq * QK, out + e * M3 + pq * M);
+    }
+  }
+};
+
+}  // namespace sphp

@@ -1,0 +1,53 @@
+// Host interface of misc.cu (geometry, assembly, StdMat helpers).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sphp {
+
+struct GeomJob {
+  int dim, Q, n, kind, mapping;
+  int64_t E, e0, npts, cs, stride;
+  const int64_t* ids;  // device, may be null
+  const double* z;     // device (Q)
+  const double* w;     // device (Q)
+  double L[3];
+  double amp;
+  double* out;
+};
+
+struct AmapDev {
+  int periodic;  // 1: analytic periodic hex numbering
+  int n, P;      // periodic grid
+  int nm;
+  int64_t E;
+  int64_t num_global;
+  const int* codes;  // explicit: (E, nm)
+};
+
+struct PointJob {
+  int dim, kind;
+  int64_t E, np, cs, stride;
+  const double* geom;
+  const double* wstd;  // device (np) standard weights
+};
+
+cudaError_t geom_analytic(const GeomJob& j, int* bad, cudaStream_t s);
+cudaError_t geom_convert(const GeomJob& j, const double* wj, const double* inv, int* bad,
+                         cudaStream_t s);
+cudaError_t amap_scatter(const AmapDev& m, const double* g, double* loc, cudaStream_t s);
+cudaError_t amap_assemble(const AmapDev& m, const double* loc, double* g, int ncolours,
+                          const int* elist_dev, const int64_t* colour_off, int accumulate,
+                          cudaStream_t s);
+cudaError_t dgemm(int64_t R, int N, int K, const double* A, const double* B, double* C,
+                  cudaStream_t s);
+// which: 0 = weights (IProduct), 1 = metric transform in place (PhysDeriv),
+//        2 = flux (IProductWRTDerivBase)
+cudaError_t pointwise(int which, const PointJob& j, const double* in, double* out, cudaStream_t s);
+cudaError_t elem_matvec(int64_t E, int nm, const double* H, const double* x, double* y,
+                        cudaStream_t s);
+cudaError_t unit_block(int64_t E, int nm, int n, double* x, cudaStream_t s);
+cudaError_t store_column(int64_t E, int nm, int n, const double* y, double* H, cudaStream_t s);
+cudaError_t symmetrise(int64_t E, int nm, double* H, cudaStream_t s);
+
+}  // namespace sphp
