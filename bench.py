@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark of the matrix-free hex Helmholtz operator (BASELINE.json cfg4).
+
+One step = one assembled matrix-free Helmholtz apply y = A^T H A x on the
+64^3 periodic deformed hex mesh (x' = x + 0.03 sin 2πy sin 2πz), P=4, Q=6
+GLL, lambda = 1, per-point geometric factors stored (6 metric terms + |J|):
+fused gather -> BwdTrans -> PhysDeriv -> metric -> IProductWRTDerivBase +
+lambda IProductWRTBase -> colour-ordered C0 scatter-add.  `value` is local
+DoF/s (E (P+1)^3 / step time); global DoF/s is reported too.
+
+Arms:
+  default            the CUDA path (libspechp_b200.so) through the public API
+  --impl reference   the reference algorithm's CPU port (oracle/, numpy,
+                     all host threads) on a bounded sample of the same
+                     workload (the reference itself is Python with no hex
+                     path)
+
+Multi-GPU (torchrun): every rank runs an independent 64^3 mesh (weak
+scaling: elemental operators shard by element with no data-path exchange);
+time = max over ranks of the CUDA-event time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SEED = int(os.environ.get("SPECHP_SEED", "20240801"))
+AMP = 0.03
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--P", type=int, default=4)
+    ap.add_argument("--n", type=int, default=64)
+    ap.add_argument("--sweep", action="store_true", help="also time P=2..8 (extra JSON key)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def metric_name(P, n):
+    return (f"matrix-free Helmholtz DoF/s (assembled, hex P={P}, {n}^3 deformed periodic, "
+            "FP64, 1 B200 per rank)")
+
+
+def workload_bytes(P, n):
+    """Algorithmic HBM bytes of one assembled apply:
+    geometry 7 Q^3 doubles per element + x read + y written (global)."""
+    E = n ** 3
+    Q = P + 2
+    ng = (n * P) ** 3
+    return 8 * (7 * Q ** 3 * E + 2 * ng)
+
+
+def local_bytes(P, E):
+    m, Q = P + 1, P + 2
+    return 8 * (2 * m ** 3 + 7 * Q ** 3) * E
+
+
+def helm_flops(P, E):
+    m, Q = P + 1, P + 2
+    staged = m ** 3 * Q + m * m * Q * Q + m * Q ** 3
+    return 2 * E * (2 * staged + 6 * Q ** 4 + 11 * Q ** 3)
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi, during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower().startswith("active"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port; test infrastructure, timed here as the baseline)
+# ---------------------------------------------------------------------------
+def cpu_port_assembled(P, n_sample, seconds, seed=SEED):
+    """The reference algorithm (GlobalSystem.apply = scatter -> elemental
+    Helmholtz -> assemble, assembly.py:177-182, with the sum-factorised
+    elemental operator of collections.py restated for hex) on an
+    n_sample^3 periodic sub-mesh with the same mapping; numpy, BLAS threads
+    = all host cores.  Returns (local DoF/s, runs, seconds, cores)."""
+    from oracle import assembly as oa
+    from oracle import geometry as og
+    from oracle import ops as oo
+
+    oe = oo.Expansion("hex", P, P + 2)
+    E = n_sample ** 3
+    _, _, inv, wj = og.factors(oe, n_sample, np.arange(E), og.MAP_HEX_SINE, AMP)
+    G = oo.metric_from_inv(wj, inv)
+    om = oa.hex_periodic_map(n_sample, P)
+    codes = oa.pack_map(om)
+    x = np.random.default_rng(seed).uniform(-1, 1, om.num_global)
+
+    def step():
+        loc = x[codes]                                  # signed gather (all +1)
+        yl = oo.helmholtz(oe, loc, 1.0, G, wj)
+        y = np.zeros(om.num_global)
+        np.add.at(y, codes.ravel(), yl.ravel())        # assemble (np.add.at)
+        return y
+
+    step()
+    runs, t0 = 0, time.perf_counter()
+    while True:
+        step()
+        runs += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return runs * E * (P + 1) ** 3 / el, runs, el, os.cpu_count() or 1, E
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n_s = 12 if args.P <= 4 else 8
+    times = []
+    # each step = one bounded sample (assembled apply on an n_s^3 sub-mesh)
+    from oracle import assembly as oa  # noqa: F401
+    for i in range(args.warmup + args.steps):
+        v, runs, el, cores, E = cpu_port_assembled(args.P, n_s, 0.0)
+        if i >= args.warmup:
+            times.append(el / runs)
+    t = statistics.median(times)
+    value = n_s ** 3 * (args.P + 1) ** 3 / t
+    sample = f"assembled apply on a {n_s}^3 periodic sub-mesh (same map, P={args.P}), one per step"
+    line = {
+        "metric": metric_name(args.P, args.n), "value": value, "unit": "DoF/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded, SPECHP_SEED)",
+        "config": {"workload": f"cfg4 hex Helmholtz P={args.P} n={args.n} (sampled {n_s}^3)",
+                   "P": args.P, "Q": args.P + 2, "n": args.n, "lambda": 1.0},
+        "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1906_03489_b200 as sp
+    from paper_1906_03489_b200 import _lib
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    P, n = args.P, args.n
+    E = n ** 3
+    m = P + 1
+
+    def build(P):
+        exp = sp.make_hex(P, P + 2)
+        batch = sp.ElementBatch.structured(exp, n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE,
+                                           amp=AMP, device=dev)
+        coll = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC, lam=1.0)
+        amap = sp.AssemblyMap.hex_periodic(n, P)
+        return exp, batch, coll, amap
+
+    exp, batch, coll, amap = build(P)
+    op = sp.GlobalHelmholtz([(coll, amap)], amap.num_global)
+    ng = amap.num_global
+    rng = np.random.default_rng(SEED + rank)
+    x_host = torch.from_numpy(rng.uniform(-1, 1, ng)).pin_memory()
+    y_host = torch.empty(ng, dtype=torch.float64).pin_memory()
+    x = x_host.to(dev)
+    y = torch.empty(ng, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize(dev)
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms / steps
+
+    # ---- headline: assembled apply, inputs resident ------------------------
+    clocks = Clocks(local_rank)
+    for _ in range(args.warmup):
+        op.apply(x, y)
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    ms = timed(lambda: op.apply(x, y), args.steps, 0)
+    clk = clocks.stop()
+    value = world * E * m ** 3 / (ms * 1e-3)
+
+    # ---- e2e: the C-ABI host-buffer call (H2D x, apply, D2H y, sync) -------
+    def e2e_step():
+        rc = _lib.lib.sphp_helmholtz_assembled_host(coll._handle, amap._h, _lib.ptr(x_host),
+                                                    _lib.ptr(y_host), _lib.stream_ptr(stream))
+        _lib.check(rc)
+
+    e2e_ms = timed(e2e_step, max(3, args.steps // 2), 2)
+    e2e_value = world * E * m ** 3 / (e2e_ms * 1e-3)
+
+    # ---- dominant kernel: the fused local Helmholtz, timed alone -----------
+    c = torch.as_tensor(np.random.default_rng(SEED).uniform(-1, 1, (E, m ** 3)), device=dev)
+    yl = torch.empty_like(c)
+    k_ms = timed(lambda: coll.apply(c, yl), args.steps, args.warmup)
+    peak, peak_kind = measured_peaks()
+    kb = local_bytes(P, E)
+    achieved = kb / (k_ms * 1e-3) / 1e9
+    # assembled apply as a whole against the same roofline
+    ab = workload_bytes(P, n)
+    a_achieved = ab / (ms * 1e-3) / 1e9
+    del c, yl
+
+    sweep = None
+    if args.sweep:
+        sweep = {}
+        for Ps in range(2, 9):
+            if Ps == P:
+                sweep[str(Ps)] = {"assembled_ms": ms, "local_ms": k_ms}
+                continue
+            _, b2, c2, a2 = build(Ps)
+            op2 = sp.GlobalHelmholtz([(c2, a2)], a2.num_global)
+            x2 = torch.as_tensor(np.random.default_rng(Ps).uniform(-1, 1, a2.num_global), device=dev)
+            y2 = torch.empty_like(x2)
+            t_as = timed(lambda: op2.apply(x2, y2), max(5, args.steps // 2), 3)
+            cc = torch.as_tensor(np.random.default_rng(Ps).uniform(-1, 1, (E, (Ps + 1) ** 3)), device=dev)
+            yy = torch.empty_like(cc)
+            t_lo = timed(lambda: c2.apply(cc, yy), max(5, args.steps // 2), 3)
+            lb = local_bytes(Ps, E)
+            sweep[str(Ps)] = {
+                "assembled_ms": t_as, "local_ms": t_lo,
+                "assembled_local_dof_s": E * (Ps + 1) ** 3 / (t_as * 1e-3),
+                "local_dof_s": E * (Ps + 1) ** 3 / (t_lo * 1e-3),
+                "local_hbm_gbs": lb / (t_lo * 1e-3) / 1e9,
+                "local_roofline_frac": lb / (t_lo * 1e-3) / 1e9 / peak,
+                "local_fp64_tflops": helm_flops(Ps, E) / (t_lo * 1e-3) / 1e12,
+            }
+            del b2, c2, a2, op2, x2, y2, cc, yy
+            torch.cuda.empty_cache()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n_s = 12 if P <= 4 else 8
+        v, runs, el, cores, Es = cpu_port_assembled(P, n_s, args.cpu_seconds)
+        cpu = {"value": v, "unit": "DoF/s", "cores": cores, "kind": "port",
+               "sample": f"{runs} assembled applies on a {n_s}^3 periodic sub-mesh ({Es} elements, "
+                         f"same map, P={P}) in {el:.1f} s, numpy with BLAS threads = all cores"}
+
+    if rank != 0:
+        return
+    line = {
+        "metric": metric_name(P, n), "value": value, "unit": "DoF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SPECHP_SEED; analytic deformed mesh)",
+        "config": {"workload": f"cfg4: assembled matrix-free hex Helmholtz P={P} Q={P + 2} n={n} "
+                               "periodic deformed, lambda=1", "P": P, "Q": P + 2, "n": n,
+                   "elements_per_rank": E, "global_dofs_per_rank": ng,
+                   "local_dofs_per_rank": E * m ** 3, "parallelism": f"replicas x{world} (weak)",
+                   "l2": "inputs larger than L2 (geometry 3.2 GB/apply at P=4)"},
+        "global_dof_s": world * ng / (ms * 1e-3),
+        "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": 8 * ng,
+                "d2h_bytes_per_step": 8 * ng, "ms_per_step": e2e_ms},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "pipe_kernel<HexHelm> (fused local Helmholtz, one launch)",
+                     "bytes_per_launch": kb, "launch_ms": k_ms,
+                     "fp64_tflops": helm_flops(P, E) / (k_ms * 1e-3) / 1e12,
+                     "assembled_achieved": a_achieved, "assembled_frac": a_achieved / peak,
+                     "assembled_bytes_per_step": ab},
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "gpu_launches": args.steps * amap.num_colours,
+    }
+    if sweep is not None:
+        line["sweep"] = sweep
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if world > 1 and rank != 0:
+            return
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -176,6 +176,11 @@ int sphp_assemble(const sphp_amap* a, const double* local, double* global,
  * meshes: one call per order batch, same y).                              */
 int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x,
                              double* y, int accumulate, sphp_stream stream);
+/* same with HOST vectors (num_global each): copies in, applies, copies out
+ * on `stream` and synchronises it (the end-to-end path)                    */
+int sphp_helmholtz_assembled_host(sphp_coll* c, const sphp_amap* a,
+                                  const double* x, double* y,
+                                  sphp_stream stream);
 
 #ifdef __cplusplus
 }

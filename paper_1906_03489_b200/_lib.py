@@ -83,6 +83,7 @@ _SIGS = {
     "sphp_scatter": (_i, [_p, _p, _p, _p]),
     "sphp_assemble": (_i, [_p, _p, _p, _p]),
     "sphp_helmholtz_assembled": (_i, [_p, _p, _p, _p, _i, _p]),
+    "sphp_helmholtz_assembled_host": (_i, [_p, _p, _p, _p, _p]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

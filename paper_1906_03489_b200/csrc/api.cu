@@ -999,4 +999,21 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
   return SPHP_OK;
 }
 
+// e2e path with HOST vectors: x (num_global) -> device, fused assembled
+// apply, y -> host; staging buffers owned by the collection; synchronises.
+int sphp_helmholtz_assembled_host(sphp_coll* c, const sphp_amap* a, const double* x, double* y,
+                                  sphp_stream stream) {
+  if (!c || !a || !x || !y) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t b = sizeof(double) * a->num_global;
+  CK(c->host_in.ensure(b));
+  CK(c->host_out.ensure(b));
+  CK(cudaMemcpyAsync(c->host_in.p, x, b, cudaMemcpyHostToDevice, s));
+  int rc = sphp_helmholtz_assembled(c, a, c->host_in.as<double>(), c->host_out.as<double>(), 0, stream);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(y, c->host_out.p, b, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return SPHP_OK;
+}
+
 }  // extern "C"

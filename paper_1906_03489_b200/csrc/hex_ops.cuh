@@ -106,11 +106,17 @@ struct HexHelm {
         a22 = det * (iv[6] * iv[6] + iv[7] * iv[7] + iv[8] * iv[8]);
         adet = det;
       }
+      double d1v[Q];
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
-        double d1 = 0.0;
+        double acc = 0.0;
 #pragma unroll
-        for (int l = 0; l < Q; ++l) d1 = fma(tab[T::D + j * Q + l], u[l], d1);
+        for (int l = 0; l < Q; ++l) acc = fma(tab[T::D + j * Q + l], u[l], acc);
+        d1v[j] = acc;
+      }
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        const double d1 = d1v[j];
         const double d0 = W2[base + j * QK];
         const double d2 = W1[base + j * QK];
         double G00, G01, G02, G11, G12, G22, wj;

@@ -124,7 +124,12 @@ struct Scaffold {
   static constexpr int STAGE = IN_T + GEO_T;
   static constexpr int OUT_T = even_up(NE * Op::OUT);
   static constexpr int WORK_T = even_up(NE * Op::WORK);
-  static constexpr size_t SMEM_BYTES = sizeof(double) * (2 * STAGE + OUT_T + WORK_T) + 2 * sizeof(uint64_t);
+  // two input stages when they fit in 227 KB, else one (the next tile's copy
+  // then overlaps only the part of the compute after the release point)
+  static constexpr size_t BYTES2 = sizeof(double) * (2 * STAGE + OUT_T + WORK_T) + 2 * sizeof(uint64_t);
+  static constexpr int NST = BYTES2 <= 227 * 1024 ? 2 : 1;
+  static constexpr size_t SMEM_BYTES = sizeof(double) * (NST * STAGE + OUT_T + WORK_T) + 2 * sizeof(uint64_t);
+  static_assert(SMEM_BYTES <= 227 * 1024, "one pipeline stage does not fit in shared memory");
 };
 
 template <class Op, int MODE>
@@ -133,7 +138,8 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
   constexpr int NE = Op::NE, NT = Op::NT, IN = Op::IN, OUT = Op::OUT, GEO = Op::GEO;
   extern __shared__ __align__(128) double smem[];
   double* stage_base = smem;
-  double* out_s = smem + 2 * S::STAGE;
+  constexpr int NST = S::NST;
+  double* out_s = smem + NST * S::STAGE;
   double* work = out_s + S::OUT_T;
   uint64_t* bar = reinterpret_cast<uint64_t*>(work + S::WORK_T);
   const int tid = threadIdx.x;
@@ -213,12 +219,12 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
   uint32_t phase = 0;  // bit s = parity to wait for on stage s
   if (tid == 0) {
     issue(blockIdx.x, 0);
-    issue(blockIdx.x + G, 1);
+    if (NST == 2) issue(blockIdx.x + G, 1);
   }
 
   int it = 0;
   for (int t = blockIdx.x; t < ntiles; t += G, ++it) {
-    const int s = it & 1;
+    const int s = (NST == 2) ? (it & 1) : 0;
     double* in_s = stage_base + s * S::STAGE;
     double* geo_s = in_s + S::IN_T;
     const int64_t w0 = (int64_t)t * NE;
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
       // last read of the stage: hand the stage to the copy engine
       if (tid == 0) {
         fence_proxy_async();
-        issue(t + 2 * G, s);
+        issue(t + NST * G, s);
       }
     };
     auto pre_out = [&]() {};

@@ -66,11 +66,17 @@ struct QuadHelm {
         a11 = det * (g[3] * g[3] + g[4] * g[4]);
         adet = det;
       }
+      double d1v[Q];
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
-        double d1 = 0.0;
+        double acc = 0.0;
 #pragma unroll
-        for (int l = 0; l < Q; ++l) d1 = fma(tab[T::D + j * Q + l], u[l], d1);
+        for (int l = 0; l < Q; ++l) acc = fma(tab[T::D + j * Q + l], u[l], acc);
+        d1v[j] = acc;
+      }
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        const double d1 = d1v[j];
         const double d0 = W2[base + j];
         double G00, G01, G11, wj;
         if (GK == SPHP_GEOM_METRIC) {
