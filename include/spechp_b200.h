@@ -159,6 +159,16 @@ int sphp_amap_create_hex_periodic(int n, int P, sphp_amap** out);
 int sphp_hexmap_variable(int n, const int* orders, int64_t* num_global,
                          int64_t* offsets, int64_t* codes);
 int sphp_amap_destroy(sphp_amap* a);
+/* assembly algorithm of sphp_assemble / sphp_helmholtz_assembled, both
+ * deterministic (bitwise reproducible) and atomic-free:
+ *   OWNER  (default) gather -> elemental operator -> local block, then one
+ *          owner-computes pass that sums each global dof in a fixed order;
+ *   COLOUR colour classes (parity colours on periodic grids, greedy
+ *          colouring of explicit maps) fused gather/scatter-add, one launch
+ *          per colour in a fixed colour order.                            */
+#define SPHP_ASSEMBLY_OWNER 0
+#define SPHP_ASSEMBLY_COLOUR 1
+int sphp_amap_set_algorithm(sphp_amap* a, int alg);
 int sphp_amap_info(const sphp_amap* a, int64_t* num_elements, int* nmodes,
                    int64_t* num_global, int* num_colours);
 /* materialise the map codes (E*nmodes int64, host) — for bit-exact tests   */

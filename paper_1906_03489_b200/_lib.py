@@ -28,6 +28,7 @@ OP_BWD_TRANS, OP_IPRODUCT_WRT_BASE, OP_PHYS_DERIV, OP_IPRODUCT_WRT_DERIV_BASE, O
 STRATEGY_CUDA_SUMFAC, STRATEGY_CUDA_STDMAT = 0, 1
 GEOM_NONE, GEOM_AFFINE, GEOM_POINT, GEOM_METRIC = 0, 1, 2, 3
 MAP_AFFINE, MAP_QUAD_SINE, MAP_HEX_SINE = 0, 1, 2
+ASSEMBLY_OWNER, ASSEMBLY_COLOUR = 0, 1
 
 
 class LibraryError(RuntimeError):
@@ -78,6 +79,7 @@ _SIGS = {
     "sphp_amap_create_hex_periodic": (_i, [_i, _i, _pp]),
     "sphp_hexmap_variable": (_i, [_i, _p, _i64p, _p, _p]),
     "sphp_amap_destroy": (_i, [_p]),
+    "sphp_amap_set_algorithm": (_i, [_p, _i]),
     "sphp_amap_info": (_i, [_p, _i64p, _ip, _i64p, _ip]),
     "sphp_amap_codes": (_i, [_p, _p]),
     "sphp_scatter": (_i, [_p, _p, _p, _p]),

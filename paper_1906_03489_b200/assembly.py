@@ -10,10 +10,14 @@
     (edge order = min over the 4 sharing elements, face order = min over 2,
     excess modes pinned) and splits it into per-order batches.
 
-`scatter` / `assemble` mirror assembly.py:141-160 (assemble is a
-deterministic colour-ordered sum, no atomics); `GlobalHelmholtz.apply` is
-`GlobalSystem.apply` (assembly.py:177-182) with the gather, the elemental
-operator and the scatter-add fused in one kernel per colour.
+`scatter` / `assemble` mirror assembly.py:141-160; `GlobalHelmholtz.apply`
+is `GlobalSystem.apply` (assembly.py:177-182).  Two deterministic,
+atomic-free assembly algorithms (`AssemblyMap.set_algorithm`):
+  "owner"  (default) one kernel gathers x, applies the fused elemental
+           operator and writes the local block; a second sums every global
+           dof from its contributions in a fixed order (owner computes);
+  "colour" one fused gather -> operator -> scatter-add kernel per colour
+           class, colours in a fixed order.
 """
 from __future__ import annotations
 
@@ -58,6 +62,7 @@ class AssemblyMap:
                                            C.byref(nc)))
         self.num_elements, self.nmodes = ne.value, nm.value
         self.num_global, self.num_colours = ng.value, nc.value
+        self.algorithm = "owner"
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -85,6 +90,14 @@ class AssemblyMap:
         _lib.check(_lib.lib.sphp_amap_create_hex_periodic(int(n), int(P), C.byref(h)),
                    AssemblyError)
         return cls(h)
+
+    def set_algorithm(self, alg):
+        """'owner' (default: gather -> local -> owner-computes sum) or
+        'colour' (fused colour-ordered scatter-add)."""
+        code = {"owner": _lib.ASSEMBLY_OWNER, "colour": _lib.ASSEMBLY_COLOUR}[alg]
+        _lib.check(_lib.lib.sphp_amap_set_algorithm(self._h, code), AssemblyError)
+        self.algorithm = alg
+        return self
 
     def codes(self):
         out = np.empty((self.num_elements, self.nmodes), dtype=np.int64)

@@ -166,8 +166,9 @@ struct sphp_amap {
   std::vector<int64_t> codes_host;  // explicit only
   std::vector<int64_t> colour_off;  // explicit only (ncolours+1)
   std::vector<int> elist_host;      // explicit only, element ids by colour
+  int alg = SPHP_ASSEMBLY_OWNER;
   std::mutex mu;
-  DevBuf d_codes, d_elist;
+  DevBuf d_codes, d_elist, d_rowp, d_ent;  // explicit: codes, colour lists, CSR
   AmapDev dev() const {
     AmapDev a;
     a.periodic = periodic;
@@ -783,11 +784,46 @@ static int amap_device(const sphp_amap* ac) {
   CK(a->d_elist.ensure(sizeof(int) * a->elist_host.size()));
   CK(cudaMemcpy(a->d_elist.p, a->elist_host.data(), sizeof(int) * a->elist_host.size(),
                 cudaMemcpyHostToDevice));
+  // owner-computes CSR: per global dof, its local entries in element order
+  std::vector<int64_t> rowp(a->num_global + 1, 0);
+  for (int64_t c : a->codes_host)
+    if (c != -1) rowp[(c >= 0 ? c : -c - 2) + 1]++;
+  for (int64_t g = 0; g < a->num_global; ++g) rowp[g + 1] += rowp[g];
+  std::vector<int> ent(rowp[a->num_global]);
+  std::vector<int64_t> fill(rowp.begin(), rowp.end() - 1);
+  for (int64_t i = 0; i < (int64_t)a->codes_host.size(); ++i) {
+    const int64_t c = a->codes_host[i];
+    if (c == -1) continue;
+    const int64_t g = c >= 0 ? c : -c - 2;
+    ent[fill[g]++] = c >= 0 ? (int)i : -(int)i - 1;
+  }
+  CK(a->d_rowp.ensure(sizeof(int64_t) * rowp.size()));
+  CK(cudaMemcpy(a->d_rowp.p, rowp.data(), sizeof(int64_t) * rowp.size(), cudaMemcpyHostToDevice));
+  CK(a->d_ent.ensure(sizeof(int) * (ent.size() + 1)));
+  if (!ent.empty())
+    CK(cudaMemcpy(a->d_ent.p, ent.data(), sizeof(int) * ent.size(), cudaMemcpyHostToDevice));
   DevBuf tmp;
   CK(tmp.ensure(sizeof(int) * codes32.size()));
   CK(cudaMemcpy(tmp.p, codes32.data(), sizeof(int) * codes32.size(), cudaMemcpyHostToDevice));
   std::swap(a->d_codes.p, tmp.p);
   std::swap(a->d_codes.bytes, tmp.bytes);
+  return SPHP_OK;
+}
+
+// local (E, nm) -> global with the map's algorithm; accumulate adds to g
+static int amap_assemble_any(const sphp_amap* a, const double* loc, double* g, int accumulate,
+                             cudaStream_t s) {
+  if (a->alg == SPHP_ASSEMBLY_OWNER) {
+    if (a->periodic) {
+      CK(owner_assemble_periodic(a->n, a->P, loc, g, accumulate, s));
+    } else {
+      CK(owner_assemble_csr(a->num_global, a->d_rowp.as<int64_t>(), a->d_ent.as<int>(), loc, g,
+                            accumulate, s));
+    }
+    return SPHP_OK;
+  }
+  CK(amap_assemble(a->dev(), loc, g, a->ncolours, a->d_elist.as<int>(), a->colour_off.data(),
+                   accumulate, s));
   return SPHP_OK;
 }
 
@@ -825,6 +861,10 @@ int sphp_amap_create_hex_periodic(int n, int P, sphp_amap** out) {
   a->E = (int64_t)n * n * n;
   a->num_global = ipow((int64_t)n * P, 3);
   a->ncolours = 8;
+  if (a->num_global > 2147483645LL) {
+    delete a;
+    return fail(SPHP_ERR_UNSUPPORTED, "periodic map with more than 2^31-3 global dofs");
+  }
   *out = a;
   return SPHP_OK;
 }
@@ -914,6 +954,14 @@ int sphp_hexmap_variable(int n, const int* orders, int64_t* num_global, int64_t*
   return SPHP_OK;
 }
 
+int sphp_amap_set_algorithm(sphp_amap* a, int alg) {
+  if (!a) return fail(SPHP_ERR_BAD_ARG, "null map");
+  if (alg != SPHP_ASSEMBLY_OWNER && alg != SPHP_ASSEMBLY_COLOUR)
+    return fail(SPHP_ERR_BAD_ARG, "unknown assembly algorithm");
+  a->alg = alg;
+  return SPHP_OK;
+}
+
 int sphp_amap_destroy(sphp_amap* a) {
   delete a;
   return SPHP_OK;
@@ -949,9 +997,7 @@ int sphp_scatter(const sphp_amap* a, const double* g, double* loc, sphp_stream s
 int sphp_assemble(const sphp_amap* a, const double* loc, double* g, sphp_stream stream) {
   if (!a || !g || !loc) return fail(SPHP_ERR_BAD_ARG, "null argument");
   if (int rc = amap_device(a)) return rc;
-  CK(amap_assemble(a->dev(), loc, g, a->ncolours, a->d_elist.as<int>(), a->colour_off.data(), 0,
-                   (cudaStream_t)stream));
-  return SPHP_OK;
+  return amap_assemble_any(a, loc, g, 0, (cudaStream_t)stream);
 }
 
 // assembly.GlobalSystem.apply (assembly.py:177-182), fused
@@ -972,14 +1018,29 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
     CK(c->loc_y.ensure(sizeof(double) * c->E * c->t->nm));
     CK(amap_scatter(a->dev(), x, c->loc_x.as<double>(), s));
     CK(elem_matvec(c->E, (int)c->t->nm, c->helm_H.as<double>(), c->loc_x.as<double>(), c->loc_y.as<double>(), s));
-    CK(amap_assemble(a->dev(), c->loc_y.as<double>(), y, a->ncolours, a->d_elist.as<int>(),
-                     a->colour_off.data(), accumulate, s));
-    return SPHP_OK;
+    return amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s);
   }
-  if (!accumulate) CK(cudaMemsetAsync(y, 0, sizeof(double) * a->num_global, s));
   OpArgs o = base_args(c);
   o.xg = x;
   o.yg = y;
+  if (a->alg == SPHP_ASSEMBLY_OWNER) {
+    // gather -> fused elemental operator -> local block, then the
+    // owner-computes sum (two launches, no colour passes)
+    CK(c->loc_y.ensure(sizeof(double) * c->E * c->t->nm));
+    o.out = c->loc_y.as<double>();
+    if (a->periodic) {
+      o.mode = AsmMode::PERIODIC_GATHER;
+      o.n = a->n;
+    } else {
+      o.mode = AsmMode::EXPLICIT_GATHER;
+      o.codes = a->d_codes.as<int>();
+    }
+    cudaError_t e = sumfac_launch(c, o, s);
+    if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no assembled kernel for this key");
+    if (e != cudaSuccess) return cuda_fail(e, "sphp_helmholtz_assembled");
+    return amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s);
+  }
+  if (!accumulate) CK(cudaMemsetAsync(y, 0, sizeof(double) * a->num_global, s));
   for (int col = 0; col < a->ncolours; ++col) {
     if (a->periodic) {
       o.mode = AsmMode::PERIODIC;

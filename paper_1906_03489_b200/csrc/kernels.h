@@ -8,7 +8,10 @@
 
 namespace sphp {
 
-enum class AsmMode : int { LOCAL = 0, PERIODIC = 1, EXPLICIT = 2 };
+// LOCAL: block in/out.  PERIODIC / EXPLICIT: one colour class, gather in,
+// scatter-add out.  PERIODIC_GATHER / EXPLICIT_GATHER: all elements, gather
+// in, local block out (the owner-computes assembly then sums it).
+enum class AsmMode : int { LOCAL = 0, PERIODIC = 1, EXPLICIT = 2, PERIODIC_GATHER = 3, EXPLICIT_GATHER = 4 };
 
 struct OpArgs {
   int M, Q;          // modes / points per direction

@@ -73,7 +73,7 @@ cudaError_t launch_pipe(const OpArgs& oa, int64_t gstride, int64_t goff, cudaStr
   a.codes = oa.codes;
   a.n = oa.n;
   a.colour = oa.colour;
-  const int64_t count = (MODE == 0) ? oa.E : oa.nlist;
+  const int64_t count = (MODE == 0 || MODE >= 3) ? oa.E : oa.nlist;
   if (count <= 0) return cudaSuccess;
   const int64_t ntiles = (count + Op::NE - 1) / Op::NE;
   int64_t grid = (int64_t)oa.num_sms * c.occ;
@@ -100,6 +100,10 @@ cudaError_t launch_mode(const OpArgs& oa, int64_t gstride, int64_t goff, cudaStr
       return launch_pipe<Op, 1>(oa, gstride, goff, s);
     case AsmMode::EXPLICIT:
       return launch_pipe<Op, 2>(oa, gstride, goff, s);
+    case AsmMode::PERIODIC_GATHER:
+      return launch_pipe<Op, 3>(oa, gstride, goff, s);
+    case AsmMode::EXPLICIT_GATHER:
+      return launch_pipe<Op, 4>(oa, gstride, goff, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -479,4 +479,107 @@ cudaError_t symmetrise(int64_t E, int nm, double* H, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// owner-computes assembly (deterministic, no atomics, no colour passes):
+// every global dof is summed by one thread from its contributing local
+// entries in a fixed order.  Periodic hex: element (ex,ey,ez) owns its
+// lower vertex, the 3 edges and 3 faces leaving it, and its interior —
+// P^3 dofs — and threads walk elements in id order so the neighbour
+// blocks they read stay in L2.
+// ---------------------------------------------------------------------------
+__global__ void owner_periodic_kernel(int n, int P, const double* __restrict__ loc,
+                                      double* __restrict__ y, int accumulate) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t N3 = (int64_t)n * n * n;
+  const int b = P - 1, m = P + 1, nm = m * m * m;
+  const int per = P * P * P;
+  if (tid >= N3 * per) return;
+  const int64_t e = tid / per;
+  int o = (int)(tid - e * per);
+  const int ex = (int)(e % n), ey = (int)((e / n) % n), ez = (int)(e / ((int64_t)n * n));
+  auto wrapm = [n](int i) { return i < 0 ? i + n : i; };
+  auto eid = [&](int i, int j, int k) -> int64_t {
+    return wrapm(i) + (int64_t)n * (wrapm(j) + (int64_t)n * wrapm(k));
+  };
+  auto flat = [m](int p, int q, int r) { return (p * m + q) * m + r; };
+  double acc = 0.0;
+  int64_t gid;
+  if (o == 0) {  // vertex (ex,ey,ez): 8 elements, local corner (a,b,c)
+    gid = e;
+    for (int a = 0; a < 2; ++a)
+      for (int bb = 0; bb < 2; ++bb)
+        for (int c = 0; c < 2; ++c)
+          acc += loc[eid(ex - a, ey - bb, ez - c) * nm + flat(a, bb, c)];
+  } else if ((o -= 1) < 3 * b) {  // edge leaving the vertex along d, degree k
+    const int d = o / b, k = o % b + 2;
+    gid = N3 + (d * N3 + e) * b + (k - 2);
+    for (int s = 0; s < 2; ++s)
+      for (int t = 0; t < 2; ++t) {
+        int c[3] = {ex, ey, ez}, idx[3];
+        int st[2] = {s, t}, w = 0;
+        for (int a = 0; a < 3; ++a) {
+          if (a == d) {
+            idx[a] = k;
+          } else {
+            c[a] -= st[w];
+            idx[a] = st[w++];
+          }
+        }
+        acc += loc[eid(c[0], c[1], c[2]) * nm + flat(idx[0], idx[1], idx[2])];
+      }
+  } else if ((o -= 3 * b) < 3 * b * b) {  // face normal d at the vertex, degrees (k1,k2)
+    const int d = o / (b * b), r2 = o % (b * b);
+    const int k1 = r2 / b + 2, k2 = r2 % b + 2;
+    gid = N3 + 3 * N3 * b + (d * N3 + e) * b * b + (int64_t)(k1 - 2) * b + (k2 - 2);
+    for (int side = 0; side < 2; ++side) {
+      int c[3] = {ex, ey, ez}, idx[3], kk[2] = {k1, k2}, w = 0;
+      for (int a = 0; a < 3; ++a) {
+        if (a == d) {
+          c[a] -= side;
+          idx[a] = side;
+        } else {
+          idx[a] = kk[w++];
+        }
+      }
+      acc += loc[eid(c[0], c[1], c[2]) * nm + flat(idx[0], idx[1], idx[2])];
+    }
+  } else {  // interior
+    o -= 3 * b * b;
+    const int p = o / (b * b) + 2, q = (o / b) % b + 2, r = o % b + 2;
+    gid = N3 * (1 + 3 * (int64_t)b + 3 * (int64_t)b * b) + e * b * b * b + o;
+    acc = loc[e * nm + flat(p, q, r)];
+  }
+  y[gid] = accumulate ? y[gid] + acc : acc;
+}
+
+// explicit maps: CSR rows over global dofs, entries = local index, negative
+// (-(idx+1)) for sign -1; rows sorted by local index (element order)
+__global__ void owner_csr_kernel(int64_t ng, const int64_t* __restrict__ rowp,
+                                 const int* __restrict__ ent, const double* __restrict__ loc,
+                                 double* __restrict__ y, int accumulate) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  double acc = 0.0;
+  for (int64_t k = rowp[g]; k < rowp[g + 1]; ++k) {
+    const int c = ent[k];
+    acc += c >= 0 ? loc[c] : -loc[-(int64_t)c - 1];
+  }
+  y[g] = accumulate ? y[g] + acc : acc;
+}
+
+cudaError_t owner_assemble_periodic(int n, int P, const double* loc, double* y, int accumulate,
+                                    cudaStream_t s) {
+  const int64_t total = (int64_t)n * n * n * P * P * P;
+  if (total == 0) return cudaSuccess;
+  owner_periodic_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(n, P, loc, y, accumulate);
+  return cudaGetLastError();
+}
+
+cudaError_t owner_assemble_csr(int64_t ng, const int64_t* rowp, const int* ent, const double* loc,
+                               double* y, int accumulate, cudaStream_t s) {
+  if (ng == 0) return cudaSuccess;
+  owner_csr_kernel<<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(ng, rowp, ent, loc, y, accumulate);
+  return cudaGetLastError();
+}
+
 }  // namespace sphp

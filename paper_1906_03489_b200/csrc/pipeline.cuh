@@ -45,76 +45,93 @@ struct DevArgs {
   int colour;
 };
 
-// periodic n^3 hex numbering (assembly.py:89-133 generalised; identical to
-// oracle/assembly.py hex_periodic + build_map for uniform order P)
-__device__ __forceinline__ int64_t hex_periodic_gid(int n, int P, int ex, int ey, int ez, int p,
-                                                    int q, int r) {
-  const int64_t N3 = (int64_t)n * n * n;
-  const int64_t b = P - 1;
-  int idx[3] = {p, q, r};
-  int base[3] = {ex, ey, ez};
-  int nb = (p >= 2) + (q >= 2) + (r >= 2);
-  auto wrap = [n](int i) { return i >= n ? i - n : i; };
+// ---------------------------------------------------------------------------
+// Periodic hex numbering by entity (assembled modes): every local mode maps
+// to one of 27 entities of its element (8 vertices, 12 edges, 6 faces, the
+// interior) plus an offset; the per-mode (entity, offset) table is built
+// once per CTA, the 27 entity bases once per element, so a gather/scatter
+// index costs one shared load and one add.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int mode_code(int M, int nl) {
+  const int b = M - 2;  // bubbles per edge (P - 1)
+  const int p = nl / (M * M), q = (nl / M) % M, r = nl % M;
+  const int idx[3] = {p, q, r};
+  const int nb = (p >= 2) + (q >= 2) + (r >= 2);
+  int cls, off;
   if (nb == 0) {
-    return wrap(ex + p) + (int64_t)n * (wrap(ey + q) + (int64_t)n * wrap(ez + r));
-  }
-  if (nb == 1) {
-    int d = (p >= 2) ? 0 : ((q >= 2) ? 1 : 2);
-    int c[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) c[a] = wrap(base[a] + (a == d ? 0 : idx[a]));
-    int64_t eid = d * N3 + c[0] + (int64_t)n * (c[1] + (int64_t)n * c[2]);
-    return N3 + eid * b + (idx[d] - 2);
-  }
-  if (nb == 2) {
-    int d = (p < 2) ? 0 : ((q < 2) ? 1 : 2);
-    int c[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) c[a] = wrap(base[a] + (a == d ? idx[a] : 0));
-    int64_t fid = d * N3 + c[0] + (int64_t)n * (c[1] + (int64_t)n * c[2]);
-    int k1 = (d == 0) ? q : p;
-    int k2 = (d == 2) ? q : r;
-    return N3 + 3 * N3 * b + fid * b * b + (k1 - 2) * b + (k2 - 2);
-  }
-  int64_t e = ex + (int64_t)n * (ey + (int64_t)n * ez);
-  return N3 * (1 + 3 * b + 3 * b * b) + e * b * b * b + ((int64_t)(p - 2) * b + (q - 2)) * b + (r - 2);
-}
-
-// element of colour `colour` at list position w (n even): parity colouring
-__device__ __forceinline__ void periodic_colour_elem(int n, int colour, int64_t w, int& ex, int& ey,
-                                                     int& ez) {
-  int h = n >> 1;
-  ex = 2 * (int)(w % h) + (colour & 1);
-  ey = 2 * (int)((w / h) % h) + ((colour >> 1) & 1);
-  ez = 2 * (int)(w / ((int64_t)h * h)) + ((colour >> 2) & 1);
-}
-
-__device__ __forceinline__ void decode_code(int c, int64_t& gid, double& sgn) {
-  if (c >= 0) {
-    gid = c;
-    sgn = 1.0;
-  } else if (c == -1) {
-    gid = -1;
-    sgn = 0.0;
+    cls = p * 4 + q * 2 + r;
+    off = 0;
+  } else if (nb == 1) {
+    const int d = (p >= 2) ? 0 : ((q >= 2) ? 1 : 2);
+    int o[2], c = 0;
+    for (int a = 0; a < 3; ++a)
+      if (a != d) o[c++] = idx[a];
+    cls = 8 + d * 4 + o[0] * 2 + o[1];
+    off = idx[d] - 2;
+  } else if (nb == 2) {
+    const int d = (p < 2) ? 0 : ((q < 2) ? 1 : 2);
+    int k[2], c = 0;
+    for (int a = 0; a < 3; ++a)
+      if (a != d) k[c++] = idx[a];
+    cls = 20 + d * 2 + idx[d];
+    off = (k[0] - 2) * b + (k[1] - 2);
   } else {
-    gid = -(int64_t)c - 2;
-    sgn = -1.0;
+    cls = 26;
+    off = ((p - 2) * b + (q - 2)) * b + (r - 2);
   }
+  return cls | (off << 5);
 }
 
-struct Hooks {
-  // set by the scaffold
-  int tile_next;  // tile to load into the released stage (or -1)
-  int stage;
-  bool released;
-};
+__device__ __forceinline__ int entity_base(int n, int P, int ex, int ey, int ez, int k) {
+  const int N3 = n * n * n, b = P - 1;
+  auto wrap = [n](int i) { return i >= n ? i - n : i; };
+  auto vid = [&](int i, int j, int l) { return wrap(i) + n * (wrap(j) + n * wrap(l)); };
+  const int base[3] = {ex, ey, ez};
+  if (k < 8) return vid(ex + (k >> 2), ey + ((k >> 1) & 1), ez + (k & 1));
+  if (k < 20) {
+    const int j = k - 8, d = j >> 2;
+    const int st[2] = {(j >> 1) & 1, j & 1};
+    int c[3], m = 0;
+    for (int a = 0; a < 3; ++a) c[a] = base[a] + (a == d ? 0 : st[m++]);
+    return N3 + (d * N3 + vid(c[0], c[1], c[2])) * b;
+  }
+  if (k < 26) {
+    const int j = k - 20, d = j >> 1, side = j & 1;
+    int c[3] = {ex, ey, ez};
+    c[d] += side;
+    return N3 + 3 * N3 * b + (d * N3 + vid(c[0], c[1], c[2])) * b * b;
+  }
+  return N3 * (1 + 3 * b + 3 * b * b) + (ex + n * (ey + n * ez)) * b * b * b;
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // ---------------------------------------------------------------------------
-// The scaffold.  Op supplies: NE, NT, IN, OUT, GEO (staged doubles/element),
-// WORK (work doubles/element), NMODE (dofs/element for assembled modes,
-// i.e. IN == OUT == NMODE), and
-//   template <class R, class W> static void compute(in_s, geo_s, work,
-//        out_s, lam, R release, W pre_out)
+// The scaffold.  Op supplies: M, NE, NT, IN, OUT, GEO (staged doubles per
+// element), WORK (work doubles per element) and
+//   template <class R, class W> static void compute(in, geo, work, out, lam,
+//        R release, W pre_out, const double* tab)
+// MODE 0: local (block in, block out).
+// MODE 1: periodic hex, colour class: gather in, scatter-add out.
+// MODE 2: explicit map, colour class: gather in, scatter-add out.
+// MODE 3: periodic hex, all elements in order: gather in, local block out.
+// MODE 4: explicit map, all elements in order: gather in, local block out.
+// Gathering modes need IN == OUT == nmodes.
+template <int MODE>
+struct ModeTraits {
+  static constexpr bool GATHER = MODE != 0;
+  static constexpr bool PERIODIC = MODE == 1 || MODE == 3;
+  static constexpr bool EXPLICIT = MODE == 2 || MODE == 4;
+  static constexpr bool SCATTER = MODE == 1 || MODE == 2;
+  static constexpr bool CONTIG = MODE == 0 || MODE >= 3;
+};
 // ---------------------------------------------------------------------------
 template <class Op, int MODE>
 struct Scaffold {
@@ -124,51 +141,52 @@ struct Scaffold {
   static constexpr int STAGE = IN_T + GEO_T;
   static constexpr int OUT_T = even_up(NE * Op::OUT);
   static constexpr int WORK_T = even_up(NE * Op::WORK);
+  // assembled-mode integer tables (in doubles): per stage ids + entities,
+  // current-tile copies, and the per-mode code table
+  static constexpr int ENT = ModeTraits<MODE>::PERIODIC ? 27 : 0;
+  static constexpr int ITAB = (MODE == 0) ? 0 : even_up(NE * (1 + ENT)) / 2 + 1;
+  static constexpr int MTAB = ModeTraits<MODE>::PERIODIC ? even_up(Op::IN) / 2 + 1 : 0;
+  static constexpr size_t fixed_bytes(int nst) {
+    return sizeof(double) * (nst * (STAGE + ITAB) + OUT_T + WORK_T + ITAB + MTAB) + 2 * sizeof(uint64_t);
+  }
   // two input stages when they fit in 227 KB, else one (the next tile's copy
   // then overlaps only the part of the compute after the release point)
-  static constexpr size_t BYTES2 = sizeof(double) * (2 * STAGE + OUT_T + WORK_T) + 2 * sizeof(uint64_t);
-  static constexpr int NST = BYTES2 <= 227 * 1024 ? 2 : 1;
-  static constexpr size_t SMEM_BYTES = sizeof(double) * (NST * STAGE + OUT_T + WORK_T) + 2 * sizeof(uint64_t);
+  static constexpr int NST = fixed_bytes(2) <= 227 * 1024 ? 2 : 1;
+  static constexpr size_t SMEM_BYTES = fixed_bytes(NST);
   static_assert(SMEM_BYTES <= 227 * 1024, "one pipeline stage does not fit in shared memory");
 };
 
 template <class Op, int MODE>
 __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
   using S = Scaffold<Op, MODE>;
+  using MT = ModeTraits<MODE>;
   constexpr int NE = Op::NE, NT = Op::NT, IN = Op::IN, OUT = Op::OUT, GEO = Op::GEO;
+  constexpr int NST = S::NST, ENT = S::ENT;
   extern __shared__ __align__(128) double smem[];
   double* stage_base = smem;
-  constexpr int NST = S::NST;
   double* out_s = smem + NST * S::STAGE;
   double* work = out_s + S::OUT_T;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(work + S::WORK_T);
+  int* itab = reinterpret_cast<int*>(work + S::WORK_T);      // NST stages of [ids NE | ent NE*27]
+  int* icur = itab + NST * 2 * S::ITAB;                       // current tile copy
+  int* mtab = icur + 2 * S::ITAB;                             // per-mode codes (MODE 1)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(mtab + 2 * S::MTAB);
   const int tid = threadIdx.x;
 
-  const int64_t count = (MODE == 0) ? a.E : a.nlist;
+  const int64_t count = MT::CONTIG ? a.E : a.nlist;
   const int ntiles = (int)((count + NE - 1) / NE);
   const int G = gridDim.x;
-
-  // element id of list position w (assembled modes) / tile element (local)
-  auto elem_of = [&](int64_t w, int& ex, int& ey, int& ez) -> int64_t {
-    if (MODE == 1) {
-      periodic_colour_elem(a.n, a.colour, w, ex, ey, ez);
-      return ex + (int64_t)a.n * (ey + (int64_t)a.n * ez);
-    } else if (MODE == 2) {
-      return a.elist[w];
-    }
-    return w;
-  };
 
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
+  if (MT::PERIODIC)
+    for (int i = tid; i < IN; i += NT) mtab[i] = mode_code(Op::M, i);
   __syncthreads();
 
-  // byte window of tile t's input block, widened to 16-byte boundaries so a
-  // single bulk copy can move it whatever the element size (the data then
-  // starts 0 or 1 doubles into the stage buffer)
+  // ---- local mode: byte window of tile t's input block, widened to 16-byte
+  // boundaries so one bulk copy moves it whatever the element size
   const int64_t in_total = count * (int64_t)IN * (int64_t)sizeof(double);
   auto in_window = [&](int t, int64_t& a0, int64_t& a1, int& off) -> bool {
     const int64_t w0 = (int64_t)t * NE;
@@ -180,46 +198,107 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     return a.use_tma && a1 <= in_total;
   };
 
-  // issue the asynchronous part of tile t's input into stage s (thread 0)
-  auto issue = [&](int t, int s) {
+  // thread 0: TMA bulk copies of tile t into stage s (local mode)
+  auto issue_local = [&](int t, int s) {
     if (t >= ntiles) return;
     double* in_s = stage_base + s * S::STAGE;
     double* geo_s = in_s + S::IN_T;
     const int64_t w0 = (int64_t)t * NE;
     const int r = (int)((count - w0) < NE ? (count - w0) : NE);
-    if (MODE == 0) {
-      int64_t a0, a1;
-      int off;
-      if (!in_window(t, a0, a1, off)) return;  // synchronous at consumption
-      uint32_t bytes_in = (uint32_t)(a1 - a0);
-      uint32_t bytes_g = (uint32_t)(sizeof(double) * r * GEO);
-      mbar_expect_tx(&bar[s], bytes_in + bytes_g);
-      bulk_g2s(in_s, reinterpret_cast<const char*>(a.in) + a0, bytes_in, &bar[s]);
-      if (GEO > 0) {
-        if (a.gstride == GEO && a.goff == 0) {
-          bulk_g2s(geo_s, a.geom + w0 * a.gstride, bytes_g, &bar[s]);
-        } else {
-          for (int e = 0; e < r; ++e)
-            bulk_g2s(geo_s + e * GEO, a.geom + (w0 + e) * a.gstride + a.goff,
-                     (uint32_t)(sizeof(double) * GEO), &bar[s]);
-        }
-      }
-    } else {
-      if (GEO == 0) return;
-      mbar_expect_tx(&bar[s], (uint32_t)(sizeof(double) * r * GEO));
-      for (int e = 0; e < r; ++e) {
-        int ex, ey, ez;
-        int64_t id = elem_of(w0 + e, ex, ey, ez);
-        bulk_g2s(geo_s + e * GEO, a.geom + id * a.gstride + a.goff, (uint32_t)(sizeof(double) * GEO),
-                 &bar[s]);
+    int64_t a0, a1;
+    int off;
+    if (!in_window(t, a0, a1, off)) return;  // synchronous at consumption
+    uint32_t bytes_in = (uint32_t)(a1 - a0);
+    uint32_t bytes_g = (uint32_t)(sizeof(double) * r * GEO);
+    mbar_expect_tx(&bar[s], bytes_in + bytes_g);
+    bulk_g2s(in_s, reinterpret_cast<const char*>(a.in) + a0, bytes_in, &bar[s]);
+    if (GEO > 0) {
+      if (a.gstride == GEO && a.goff == 0) {
+        bulk_g2s(geo_s, a.geom + w0 * a.gstride, bytes_g, &bar[s]);
+      } else {
+        for (int e = 0; e < r; ++e)
+          bulk_g2s(geo_s + e * GEO, a.geom + (w0 + e) * a.gstride + a.goff,
+                   (uint32_t)(sizeof(double) * GEO), &bar[s]);
       }
     }
   };
 
+  // all threads: element ids / entity bases, geometry TMA (thread 0) and the
+  // signed gather as cp.async 8-byte copies (assembled modes).  Commits one
+  // cp.async group per call, always.
+  auto issue_asm = [&](int t, int s) {
+    double* in_s = stage_base + s * S::STAGE;
+    double* geo_s = in_s + S::IN_T;
+    int* ids = itab + s * 2 * S::ITAB;
+    int* ent = ids + NE;
+    const int64_t w0 = (int64_t)t * NE;
+    const int r = (t < ntiles) ? (int)((count - w0) < NE ? (count - w0) : NE) : 0;
+    if (MT::PERIODIC) {
+      const int h = a.n >> 1;
+      for (int i = tid; i < NE * 27; i += NT) {
+        const int e = i / 27, k = i - e * 27;
+        int v = 0;
+        if (e < r) {
+          const int w = (int)(w0 + e);
+          int ex, ey, ez;
+          if (MODE == 1) {
+            ex = 2 * (w % h) + (a.colour & 1);
+            ey = 2 * ((w / h) % h) + ((a.colour >> 1) & 1);
+            ez = 2 * (w / (h * h)) + ((a.colour >> 2) & 1);
+          } else {
+            ex = w % a.n;
+            ey = (w / a.n) % a.n;
+            ez = w / (a.n * a.n);
+          }
+          v = entity_base(a.n, Op::M - 1, ex, ey, ez, k);
+          if (k == 0) ids[e] = ex + a.n * (ey + a.n * ez);
+        }
+        ent[i] = v;
+      }
+    } else if (MT::CONTIG) {
+      for (int e = tid; e < NE; e += NT) ids[e] = (e < r) ? (int)(w0 + e) : -1;
+    } else {
+      for (int e = tid; e < NE; e += NT) ids[e] = (e < r) ? a.elist[w0 + e] : -1;
+    }
+    __syncthreads();
+    if (tid == 0 && GEO > 0 && r > 0) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar[s], (uint32_t)(sizeof(double) * r * GEO));
+      for (int e = 0; e < r; ++e)
+        bulk_g2s(geo_s + e * GEO, a.geom + (int64_t)ids[e] * a.gstride + a.goff,
+                 (uint32_t)(sizeof(double) * GEO), &bar[s]);
+    }
+    for (int i = tid; i < NE * IN; i += NT) {
+      const int e = i / IN, nl = i - e * IN;
+      if (e >= r) {
+        in_s[i] = 0.0;
+        continue;
+      }
+      int gid;
+      if (MT::PERIODIC) {
+        const int c = mtab[nl];
+        gid = ent[e * 27 + (c & 31)] + (c >> 5);
+      } else {
+        const int c = a.codes[(int64_t)ids[e] * IN + nl];
+        gid = c >= 0 ? c : (c == -1 ? -1 : -c - 2);
+      }
+      if (gid >= 0)
+        cp_async8(in_s + i, a.xg + gid);
+      else
+        in_s[i] = 0.0;
+    }
+    cp_async_commit();
+  };
+
   uint32_t phase = 0;  // bit s = parity to wait for on stage s
-  if (tid == 0) {
-    issue(blockIdx.x, 0);
-    if (NST == 2) issue(blockIdx.x + G, 1);
+  if (MODE == 0) {
+    if (tid == 0) {
+      issue_local(blockIdx.x, 0);
+      if (NST == 2) issue_local(blockIdx.x + G, 1);
+    }
+  } else {
+    issue_asm(blockIdx.x, 0);
+    if (NST == 2) issue_asm(blockIdx.x + G, 1);
   }
 
   int it = 0;
@@ -253,29 +332,19 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
       if (GEO > 0)
         for (int i = r * GEO + tid; i < NE * GEO; i += NT) geo_s[i] = 0.0;
     } else {
+      cp_async_wait<NST - 1>();
       if (GEO > 0) {
         mbar_wait(&bar[s], (phase >> s) & 1);
         phase ^= (1u << s);
       }
-      // signed gather (assembly.py:150-160)
-      for (int i = tid; i < NE * IN; i += NT) {
-        int e = i / IN, nl = i - e * IN;
-        double v = 0.0;
-        if (e < r) {
-          int ex, ey, ez;
-          int64_t id = elem_of(w0 + e, ex, ey, ez);
-          if (MODE == 1) {
-            int p = nl / (Op::M * Op::M), q = (nl / Op::M) % Op::M, rr = nl % Op::M;
-            v = a.xg[hex_periodic_gid(a.n, Op::M - 1, ex, ey, ez, p, q, rr)];
-          } else {
-            int64_t gid;
-            double sg;
-            decode_code(a.codes[id * IN + nl], gid, sg);
-            v = (gid >= 0) ? sg * a.xg[gid] : 0.0;
-          }
+      const int* ids = itab + s * 2 * S::ITAB;
+      if (MT::EXPLICIT) {  // sign -1 entries: negate the gathered value (own items)
+        for (int i = tid; i < r * IN; i += NT) {
+          const int e = i / IN, nl = i - e * IN;
+          if (a.codes[(int64_t)ids[e] * IN + nl] <= -2) in_s[i] = -in_s[i];
         }
-        in_s[i] = v;
       }
+      for (int i = tid; i < NE * (1 + ENT); i += NT) icur[i] = ids[i];
       if (GEO > 0)
         for (int i = r * GEO + tid; i < NE * GEO; i += NT) geo_s[i] = 0.0;
     }
@@ -284,10 +353,14 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     // ---- compute ---------------------------------------------------------
     auto release = [&]() {
       // all threads call this right after a __syncthreads that follows the
-      // last read of the stage: hand the stage to the copy engine
-      if (tid == 0) {
-        fence_proxy_async();
-        issue(t + NST * G, s);
+      // last read of the stage: hand the stage to the copy engines
+      if (MODE == 0) {
+        if (tid == 0) {
+          fence_proxy_async();
+          issue_local(t + NST * G, s);
+        }
+      } else {
+        issue_asm(t + NST * G, s);
       }
     };
     auto pre_out = [&]() {};
@@ -295,27 +368,44 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     __syncthreads();
 
     // ---- write back ------------------------------------------------------
-    if (MODE == 0) {
+    if (!MT::SCATTER) {
       for (int i = tid; i < r * OUT; i += NT) a.out[w0 * OUT + i] = out_s[i];
     } else {
-      // signed scatter-add of one colour class: exclusive ownership
-      for (int i = tid; i < r * OUT; i += NT) {
-        int e = i / OUT, nl = i - e * OUT;
-        int ex, ey, ez;
-        int64_t id = elem_of(w0 + e, ex, ey, ez);
-        if (MODE == 1) {
-          int p = nl / (Op::M * Op::M), q = (nl / Op::M) % Op::M, rr = nl % Op::M;
-          int64_t gid = hex_periodic_gid(a.n, Op::M - 1, ex, ey, ez, p, q, rr);
-          a.yg[gid] += out_s[i];
-        } else {
-          int64_t gid;
-          double sg;
-          decode_code(a.codes[id * OUT + nl], gid, sg);
-          if (gid >= 0) a.yg[gid] += sg * out_s[i];
+      // signed scatter-add of one colour class: every global dof touched by
+      // this launch belongs to exactly one element, so plain read-add-write
+      // is race free; loads are batched ahead of the stores
+      const int* ent = icur + NE;
+      constexpr int U = 4;
+      for (int i0 = tid; i0 < r * OUT; i0 += U * NT) {
+        int g[U];
+        double v[U], yv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * NT;
+          g[u] = -1;
+          v[u] = 0.0;
+          if (i < r * OUT) {
+            const int e = i / OUT, nl = i - e * OUT;
+            if (MT::PERIODIC) {
+              const int c = mtab[nl];
+              g[u] = ent[e * 27 + (c & 31)] + (c >> 5);
+              v[u] = out_s[i];
+            } else {
+              const int c = a.codes[(int64_t)icur[e] * OUT + nl];
+              g[u] = c >= 0 ? c : (c == -1 ? -1 : -c - 2);
+              v[u] = c >= 0 ? out_s[i] : -out_s[i];
+            }
+          }
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u) yv[u] = g[u] >= 0 ? a.yg[g[u]] : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (g[u] >= 0) a.yg[g[u]] = yv[u] + v[u];
       }
     }
   }
+  if (MODE != 0) cp_async_wait<0>();
 }
 
 }  // namespace sphp

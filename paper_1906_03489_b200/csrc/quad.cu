@@ -17,6 +17,7 @@ static cudaError_t qgo(const OpArgs& oa, int64_t goff, cudaStream_t s) {
   if (oa.mode == AsmMode::LOCAL) return launch_pipe<Op, 0>(oa, rec, goff, s);
   if constexpr (ASM) {
     if (oa.mode == AsmMode::EXPLICIT) return launch_pipe<Op, 2>(oa, rec, goff, s);
+    if (oa.mode == AsmMode::EXPLICIT_GATHER) return launch_pipe<Op, 4>(oa, rec, goff, s);
   }
   return cudaErrorNotSupported;
 }

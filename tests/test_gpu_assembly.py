@@ -30,14 +30,18 @@ def oracle_assembled(amap, oe_by_el, coeff_x, lam, G_by_el, wj_by_el):
     return oa.assemble(amap, out)
 
 
+ALGS = ("owner", "colour")
+
+
+@pytest.mark.parametrize("alg", ALGS)
 @pytest.mark.parametrize("P", [2, 3, 4, 5, 6, 7, 8])
-def test_periodic_hex_assembled(sp, P):
+def test_periodic_hex_assembled(sp, P, alg):
     n = 4
     E = n ** 3
     exp = sp.make_hex(P, P + 2)
     batch = sp.ElementBatch.structured(exp, n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE, amp=0.03)
     coll = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC, lam=1.0)
-    amap = sp.AssemblyMap.hex_periodic(n, P)
+    amap = sp.AssemblyMap.hex_periodic(n, P).set_algorithm(alg)
     assert amap.num_global == (n * P) ** 3
     op = sp.GlobalHelmholtz([(coll, amap)], amap.num_global)
     x = np.random.default_rng(P).uniform(-1, 1, amap.num_global)
@@ -52,10 +56,11 @@ def test_periodic_hex_assembled(sp, P):
     assert y.tobytes() == y2.tobytes()
 
 
-def test_scatter_assemble_duality(sp):
+@pytest.mark.parametrize("alg", ALGS)
+def test_scatter_assemble_duality(sp, alg):
     """<A x, v> == <x, A^T v> (test_assembly.py:120-129) on the device."""
     n, P = 4, 3
-    amap = sp.AssemblyMap.hex_periodic(n, P)
+    amap = sp.AssemblyMap.hex_periodic(n, P).set_algorithm(alg)
     rng = np.random.default_rng(11)
     x = torch.as_tensor(rng.standard_normal(amap.num_global), device="cuda")
     v = torch.as_tensor(rng.standard_normal((amap.num_elements, amap.nmodes)), device="cuda")
@@ -72,7 +77,8 @@ def test_scatter_assemble_duality(sp):
     assert_parity(atv.cpu().numpy(), ref_g, what="assemble")
 
 
-def test_explicit_quad_map_dirichlet_variable(sp):
+@pytest.mark.parametrize("alg", ALGS)
+def test_explicit_quad_map_dirichlet_variable(sp, alg):
     """2D explicit map with Dirichlet block, variable order and pinned modes
     (reference numbering, assembly.py:72-138) through the fused assembled
     kernel, one collection per order."""
@@ -91,7 +97,7 @@ def test_explicit_quad_map_dirichlet_variable(sp):
                                            amp=0.05, elem_ids=ids)
         coll = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC, lam=2.0)
         amap = sp.AssemblyMap.explicit(np.stack([codes[e] for e in ids]), om.num_global)
-        batches.append((coll, amap))
+        batches.append((coll, amap.set_algorithm(alg)))
         oe, inv, wj = oracle_geometry("quad", int(P), int(P) + 2, nx, ids, 1, 0.05)
         G = oo.metric_from_inv(wj, inv)
         for k, e in enumerate(ids):
@@ -104,7 +110,8 @@ def test_explicit_quad_map_dirichlet_variable(sp):
     assert_parity(y, ref, what="explicit quad variable order")
 
 
-def test_hex_variable_order(sp):
+@pytest.mark.parametrize("alg", ALGS)
+def test_hex_variable_order(sp, alg):
     n = 4
     rng = np.random.default_rng(9)
     orders = rng.integers(3, 8, n ** 3)
@@ -118,7 +125,8 @@ def test_hex_variable_order(sp):
         exp = sp.make_hex(P, P + 2)
         batch = sp.ElementBatch.structured(exp, n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE,
                                            amp=0.03, elem_ids=ids)
-        batches.append((sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC), amap))
+        batches.append((sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC),
+                        amap.set_algorithm(alg)))
         oe, inv, wj = oracle_geometry("hex", P, P + 2, n, ids, 2, 0.03)
         G = oo.metric_from_inv(wj, inv)
         for k, e in enumerate(ids):
@@ -131,14 +139,39 @@ def test_hex_variable_order(sp):
     assert_parity(y, ref, what="hex variable order")
 
 
-def test_stdmat_assembled_matches_sumfac(sp):
+@pytest.mark.parametrize("alg", ALGS)
+def test_stdmat_assembled_matches_sumfac(sp, alg):
     n, P = 4, 2
     exp = sp.make_hex(P, P + 2)
     batch = sp.ElementBatch.structured(exp, n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE, amp=0.03)
-    amap = sp.AssemblyMap.hex_periodic(n, P)
+    amap = sp.AssemblyMap.hex_periodic(n, P).set_algorithm(alg)
     x = torch.as_tensor(np.random.default_rng(2).uniform(-1, 1, amap.num_global), device="cuda")
     ys = []
     for strat in (sp.Strategy.CUDA_SUMFAC, sp.Strategy.CUDA_STDMAT):
         coll = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, strat)
         ys.append(sp.GlobalHelmholtz([(coll, amap)], amap.num_global).apply(x).cpu().numpy())
     assert_parity(ys[1], ys[0], what="stdmat vs sumfac assembled")
+
+
+def test_reference_map_signs_explicit(sp):
+    """Sign -1 entries (reversed edges, assembly.py:126-127) through both
+    algorithms: flip the orientation of a few odd-degree edge dofs in a
+    valid map by negating their codes consistently across elements."""
+    nx = ny = 4
+    P = 3
+    om = oa.quad_structured_map(nx, ny, P, ())
+    flip = {g for g in range(om.num_global) if g % 7 == 3}
+    signs = [np.where(np.isin(l, list(flip)), -s, s) for l, s in zip(om.local_to_global, om.signs)]
+    om2 = type(om)(om.local_to_global, signs, om.num_global, 0, {}, {})
+    codes = np.stack([oa.element_codes(om2, e) for e in range(nx * ny)])
+    exp = sp.make_quad(P, P + 2)
+    batch = sp.ElementBatch.structured(exp, nx, kind=sp.GEOM_METRIC, mapping=sp.MAP_QUAD_SINE, amp=0.05)
+    oe, inv, wj = oracle_geometry("quad", P, P + 2, nx, np.arange(nx * ny), 1, 0.05)
+    Gm = oo.metric_from_inv(wj, inv)
+    x = np.random.default_rng(4).uniform(-1, 1, om.num_global)
+    ref = oracle_assembled(om2, [oe] * (nx * ny), x, 1.0, Gm, wj)
+    for alg in ALGS:
+        coll = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC)
+        amap = sp.AssemblyMap.explicit(codes, om.num_global).set_algorithm(alg)
+        y = sp.GlobalHelmholtz([(coll, amap)], om.num_global).apply(torch.as_tensor(x, device="cuda"))
+        assert_parity(y.cpu().numpy(), ref, what=f"signed explicit map {alg}")
