@@ -487,69 +487,87 @@ cudaError_t symmetrise(int64_t E, int nm, double* H, cudaStream_t s) {
 // P^3 dofs — and threads walk elements in id order so the neighbour
 // blocks they read stay in L2.
 // ---------------------------------------------------------------------------
-__global__ void owner_periodic_kernel(int n, int P, const double* __restrict__ loc,
-                                      double* __restrict__ y, int accumulate) {
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t N3 = (int64_t)n * n * n;
-  const int b = P - 1, m = P + 1, nm = m * m * m;
-  const int per = P * P * P;
-  if (tid >= N3 * per) return;
-  const int64_t e = tid / per;
-  int o = (int)(tid - e * per);
-  const int ex = (int)(e % n), ey = (int)((e / n) % n), ez = (int)(e / ((int64_t)n * n));
+__global__ void __launch_bounds__(256) owner_periodic_kernel(int n, int P, const double* __restrict__ loc,
+                                                             double* __restrict__ y, int accumulate) {
+  // block = 32 consecutive elements along x (lanes) for one (ey, ez) row
+  // segment; warp w walks owned dofs o = w, w+8, ...: every warp-level branch
+  // below is uniform, and the neighbour blocks a CTA reads stay in L1/L2
+  const int segs = (n + 31) / 32;
+  const int seg = blockIdx.x % segs;
+  const int row = blockIdx.x / segs;  // ey + n*ez
+  const int ey = row % n, ez = row / n;
+  const int ex = seg * 32 + (threadIdx.x & 31);
+  if (ex >= n) return;
+  const int N3 = n * n * n, b = P - 1, m = P + 1, nm = m * m * m, per = P * P * P;
+  const int e = ex + n * row;
   auto wrapm = [n](int i) { return i < 0 ? i + n : i; };
-  auto eid = [&](int i, int j, int k) -> int64_t {
-    return wrapm(i) + (int64_t)n * (wrapm(j) + (int64_t)n * wrapm(k));
-  };
+  auto eid = [&](int i, int j, int k) { return wrapm(i) + n * (wrapm(j) + n * wrapm(k)); };
   auto flat = [m](int p, int q, int r) { return (p * m + q) * m + r; };
-  double acc = 0.0;
-  int64_t gid;
-  if (o == 0) {  // vertex (ex,ey,ez): 8 elements, local corner (a,b,c)
-    gid = e;
-    for (int a = 0; a < 2; ++a)
-      for (int bb = 0; bb < 2; ++bb)
-        for (int c = 0; c < 2; ++c)
-          acc += loc[eid(ex - a, ey - bb, ez - c) * nm + flat(a, bb, c)];
-  } else if ((o -= 1) < 3 * b) {  // edge leaving the vertex along d, degree k
-    const int d = o / b, k = o % b + 2;
-    gid = N3 + (d * N3 + e) * b + (k - 2);
-    for (int s = 0; s < 2; ++s)
-      for (int t = 0; t < 2; ++t) {
-        int c[3] = {ex, ey, ez}, idx[3];
-        int st[2] = {s, t}, w = 0;
+  const int base[3] = {ex, ey, ez};
+  for (int o = threadIdx.x >> 5; o < per; o += blockDim.x >> 5) {
+    double acc = 0.0;
+    int gid;
+    int oo = o;
+    if (oo == 0) {  // vertex: 8 elements, local corner (a, bb, c)
+      gid = e;
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            acc += loc[(size_t)eid(ex - a, ey - bb, ez - c) * nm + flat(a, bb, c)];
+    } else if ((oo -= 1) < 3 * b) {  // edge leaving the vertex along d, degree k
+      const int d = oo / b, k = oo - d * b + 2;
+      gid = N3 + (d * N3 + e) * b + (k - 2);
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          int c[3], idx[3];
+          const int st[2] = {s, t};
+          int w = 0;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            if (a == d) {
+              c[a] = base[a];
+              idx[a] = k;
+            } else {
+              c[a] = base[a] - st[w];
+              idx[a] = st[w++];
+            }
+          }
+          acc += loc[(size_t)eid(c[0], c[1], c[2]) * nm + flat(idx[0], idx[1], idx[2])];
+        }
+    } else if ((oo -= 3 * b) < 3 * b * b) {  // face normal d at the vertex
+      const int d = oo / (b * b), r2 = oo - d * b * b;
+      const int k1 = r2 / b + 2, k2 = r2 - (k1 - 2) * b + 2;
+      gid = N3 + 3 * N3 * b + (d * N3 + e) * b * b + (k1 - 2) * b + (k2 - 2);
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        int c[3], idx[3];
+        const int kk[2] = {k1, k2};
+        int w = 0;
+#pragma unroll
         for (int a = 0; a < 3; ++a) {
           if (a == d) {
-            idx[a] = k;
+            c[a] = base[a] - side;
+            idx[a] = side;
           } else {
-            c[a] -= st[w];
-            idx[a] = st[w++];
+            c[a] = base[a];
+            idx[a] = kk[w++];
           }
         }
-        acc += loc[eid(c[0], c[1], c[2]) * nm + flat(idx[0], idx[1], idx[2])];
+        acc += loc[(size_t)eid(c[0], c[1], c[2]) * nm + flat(idx[0], idx[1], idx[2])];
       }
-  } else if ((o -= 3 * b) < 3 * b * b) {  // face normal d at the vertex, degrees (k1,k2)
-    const int d = o / (b * b), r2 = o % (b * b);
-    const int k1 = r2 / b + 2, k2 = r2 % b + 2;
-    gid = N3 + 3 * N3 * b + (d * N3 + e) * b * b + (int64_t)(k1 - 2) * b + (k2 - 2);
-    for (int side = 0; side < 2; ++side) {
-      int c[3] = {ex, ey, ez}, idx[3], kk[2] = {k1, k2}, w = 0;
-      for (int a = 0; a < 3; ++a) {
-        if (a == d) {
-          c[a] -= side;
-          idx[a] = side;
-        } else {
-          idx[a] = kk[w++];
-        }
-      }
-      acc += loc[eid(c[0], c[1], c[2]) * nm + flat(idx[0], idx[1], idx[2])];
+    } else {  // interior, owned by the element alone
+      oo -= 3 * b * b;
+      const int p = oo / (b * b) + 2, q = (oo / b) % b + 2, r = oo % b + 2;
+      gid = N3 * (1 + 3 * b + 3 * b * b) + e * b * b * b + oo;
+      acc = loc[(size_t)e * nm + flat(p, q, r)];
     }
-  } else {  // interior
-    o -= 3 * b * b;
-    const int p = o / (b * b) + 2, q = (o / b) % b + 2, r = o % b + 2;
-    gid = N3 * (1 + 3 * (int64_t)b + 3 * (int64_t)b * b) + e * b * b * b + o;
-    acc = loc[e * nm + flat(p, q, r)];
+    y[gid] = accumulate ? y[gid] + acc : acc;
   }
-  y[gid] = accumulate ? y[gid] + acc : acc;
 }
 
 // explicit maps: CSR rows over global dofs, entries = local index, negative
@@ -569,9 +587,9 @@ __global__ void owner_csr_kernel(int64_t ng, const int64_t* __restrict__ rowp,
 
 cudaError_t owner_assemble_periodic(int n, int P, const double* loc, double* y, int accumulate,
                                     cudaStream_t s) {
-  const int64_t total = (int64_t)n * n * n * P * P * P;
-  if (total == 0) return cudaSuccess;
-  owner_periodic_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(n, P, loc, y, accumulate);
+  if (n == 0) return cudaSuccess;
+  const int64_t blocks = (int64_t)((n + 31) / 32) * n * n;
+  owner_periodic_kernel<<<(unsigned)blocks, 256, 0, s>>>(n, P, loc, y, accumulate);
   return cudaGetLastError();
 }
 

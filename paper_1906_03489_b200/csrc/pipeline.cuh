@@ -144,7 +144,7 @@ struct Scaffold {
   // assembled-mode integer tables (in doubles): per stage ids + entities,
   // current-tile copies, and the per-mode code table
   static constexpr int ENT = ModeTraits<MODE>::PERIODIC ? 27 : 0;
-  static constexpr int ITAB = (MODE == 0) ? 0 : even_up(NE * (1 + ENT)) / 2 + 1;
+  static constexpr int ITAB = (MODE == 0) ? 0 : even_up(NE * (2 + ENT)) / 2 + 1;
   static constexpr int MTAB = ModeTraits<MODE>::PERIODIC ? even_up(Op::IN) / 2 + 1 : 0;
   static constexpr size_t fixed_bytes(int nst) {
     return sizeof(double) * (nst * (STAGE + ITAB) + OUT_T + WORK_T + ITAB + MTAB) + 2 * sizeof(uint64_t);
@@ -231,13 +231,15 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     double* geo_s = in_s + S::IN_T;
     int* ids = itab + s * 2 * S::ITAB;
     int* ent = ids + NE;
+    int* crd = ent + NE * ENT;
     const int64_t w0 = (int64_t)t * NE;
     const int r = (t < ntiles) ? (int)((count - w0) < NE ? (count - w0) : NE) : 0;
     if (MT::PERIODIC) {
+      // element coordinates once per element (packed 10 bits each, n <= 1024),
+      // then the 27 entity bases per element
       const int h = a.n >> 1;
-      for (int i = tid; i < NE * 27; i += NT) {
-        const int e = i / 27, k = i - e * 27;
-        int v = 0;
+      for (int e = tid; e < NE; e += NT) {
+        int packed = -1;
         if (e < r) {
           const int w = (int)(w0 + e);
           int ex, ey, ez;
@@ -250,10 +252,16 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
             ey = (w / a.n) % a.n;
             ez = w / (a.n * a.n);
           }
-          v = entity_base(a.n, Op::M - 1, ex, ey, ez, k);
-          if (k == 0) ids[e] = ex + a.n * (ey + a.n * ez);
+          ids[e] = ex + a.n * (ey + a.n * ez);
+          packed = ex | (ey << 10) | (ez << 20);
         }
-        ent[i] = v;
+        crd[e] = packed;
+      }
+      __syncthreads();
+      for (int i = tid; i < NE * 27; i += NT) {
+        const int e = i / 27, k = i - e * 27;
+        const int c = crd[e];
+        ent[i] = c < 0 ? 0 : entity_base(a.n, Op::M - 1, c & 1023, (c >> 10) & 1023, c >> 20, k);
       }
     } else if (MT::CONTIG) {
       for (int e = tid; e < NE; e += NT) ids[e] = (e < r) ? (int)(w0 + e) : -1;
