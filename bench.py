@@ -5,8 +5,9 @@ One step = one assembled matrix-free Helmholtz apply y = A^T H A x on the
 64^3 periodic deformed hex mesh (x' = x + 0.03 sin 2πy sin 2πz), P=4, Q=6
 GLL, lambda = 1, per-point geometric factors stored (6 metric terms + |J|):
 fused gather -> BwdTrans -> PhysDeriv -> metric -> IProductWRTDerivBase +
-lambda IProductWRTBase -> colour-ordered C0 scatter-add.  `value` is local
-DoF/s (E (P+1)^3 / step time); global DoF/s is reported too.
+lambda IProductWRTBase -> local block, then the deterministic owner-computes
+C0 sum.  `value` is local DoF/s (E (P+1)^3 / step time,
+SURVEY §8(d)); global DoF/s is reported too.
 
 Arms:
   default            the CUDA path (libspechp_b200.so) through the public API
@@ -50,6 +51,7 @@ def parse():
     ap.add_argument("--n", type=int, default=64)
     ap.add_argument("--sweep", action="store_true", help="also time P=2..8 (extra JSON key)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extras", action="store_true", help="skip the other BASELINE configs")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -324,6 +326,13 @@ def run_ours(args, rank, world, local_rank):
             del b2, c2, a2, op2, x2, y2, cc, yy
             torch.cuda.empty_cache()
 
+    extras = None
+    if not args.no_extras:
+        try:
+            extras = config_extras(sp, dev, timed, peak)
+        except Exception as exc:  # extras must never sink the headline line
+            extras = {"error": repr(exc)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         n_s = 12 if P <= 4 else 8
@@ -360,7 +369,76 @@ def run_ours(args, rank, world, local_rank):
     }
     if sweep is not None:
         line["sweep"] = sweep
+    if extras is not None:
+        line["configs"] = extras
     print(json.dumps(line), flush=True)
+
+
+def config_extras(sp, dev, timed, peak):
+    """The other BASELINE.json configs, timed on the device (parity cases,
+    reported for the roofline picture, not bench lines)."""
+    import torch
+
+    out = {}
+    rng = np.random.default_rng(SEED)
+
+    def op_entry(name, coll, x):
+        y = torch.empty(coll.output_shape, dtype=torch.float64, device=dev)
+        ms = timed(lambda: coll.apply(x, y), 20, 3)
+        b = coll.hbm_bytes()
+        out[name] = {"ms": ms, "elements": coll.num_elements, "hbm_bytes": b,
+                     "hbm_gbs": b / (ms * 1e-3) / 1e9, "frac": b / (ms * 1e-3) / 1e9 / peak,
+                     "dof_s": coll.num_elements * (x.shape[1] if coll.operator.value == "bwdtrans"
+                                                   else coll.output_shape[-1]) / (ms * 1e-3)}
+
+    # cfg1: 32x32 affine quads, P=4, Q=6: BwdTrans + IProductWRTBase
+    q = sp.make_quad(4, 6)
+    b1 = sp.ElementBatch.structured(q, 32, kind=sp.GEOM_AFFINE, device=dev)
+    for op, size in (("bwdtrans", 25), ("iproductwrtbase", 36)):
+        c = sp.Collection(b1, sp.OperatorKind(op), sp.Strategy.CUDA_SUMFAC)
+        op_entry(f"cfg1_quad_{op}", c, torch.as_tensor(rng.uniform(-1, 1, (1024, size)), device=dev))
+    # cfg2: 256x256 curved quads, P=6, Q=8: PhysDeriv + Helmholtz
+    q6 = sp.make_quad(6, 8)
+    bp = sp.ElementBatch.structured(q6, 256, kind=sp.GEOM_POINT, mapping=sp.MAP_QUAD_SINE, amp=0.05,
+                                    device=dev)
+    c = sp.Collection(bp, sp.OperatorKind.PHYS_DERIV, sp.Strategy.CUDA_SUMFAC)
+    op_entry("cfg2_quad_physderiv", c, torch.as_tensor(rng.uniform(-1, 1, (65536, 64)), device=dev))
+    bm = sp.ElementBatch.structured(q6, 256, kind=sp.GEOM_METRIC, mapping=sp.MAP_QUAD_SINE, amp=0.05,
+                                    device=dev)
+    c = sp.Collection(bm, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC, lam=1.0)
+    op_entry("cfg2_quad_helmholtz", c, torch.as_tensor(rng.uniform(-1, 1, (65536, 49)), device=dev))
+    del bp, bm
+    # cfg3: 64^3 affine hexes, P=4, Q=6: BwdTrans, IProductWRTBase, PhysDeriv
+    h = sp.make_hex(4, 6)
+    ba = sp.ElementBatch.structured(h, 64, kind=sp.GEOM_AFFINE, device=dev)
+    for op, size in (("bwdtrans", 125), ("iproductwrtbase", 216), ("physderiv", 216)):
+        c = sp.Collection(ba, sp.OperatorKind(op), sp.Strategy.CUDA_SUMFAC)
+        op_entry(f"cfg3_hex_{op}", c, torch.as_tensor(rng.standard_normal((262144, size)), device=dev))
+        torch.cuda.empty_cache()
+    # cfg5: 48^3 deformed hexes, variable P in {3..7}, assembled Helmholtz
+    n5 = 48
+    orders = np.random.default_rng(SEED + 5).integers(3, 8, n5 ** 3)
+    ng, maps = sp.hex_variable_maps(n5, orders)
+    batches = []
+    choice = {}
+    for P, (ids, amap) in maps.items():
+        e = sp.make_hex(P, P + 2)
+        bb = sp.ElementBatch.structured(e, n5, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE, amp=AMP,
+                                        elem_ids=ids, device=dev)
+        strat, rep = sp.autotune(bb, sp.OperatorKind.HELMHOLTZ, trials=3, warmups=1)
+        choice[str(P)] = {k: (v.get("median_s") if "median_s" in v else v.get("error", "")[:60])
+                          for k, v in rep.items()}
+        choice[str(P)]["pick"] = strat.value
+        batches.append((sp.Collection(bb, sp.OperatorKind.HELMHOLTZ, strat), amap))
+    g = sp.GlobalHelmholtz(batches, ng)
+    x = torch.as_tensor(rng.uniform(-1, 1, ng), device=dev)
+    y = torch.empty_like(x)
+    ms = timed(lambda: g.apply(x, y), 10, 3)
+    ldofs = int(np.sum((orders + 1) ** 3))
+    out["cfg5_hex_variable_assembled"] = {"ms": ms, "elements": n5 ** 3, "global_dofs": ng,
+                                          "local_dof_s": ldofs / (ms * 1e-3),
+                                          "global_dof_s": ng / (ms * 1e-3), "selector": choice}
+    return out
 
 
 def main():

@@ -118,11 +118,15 @@ const double* fast_table_pool() {
   });
   return pool.data();
 }
-cudaError_t upload_tables_hex_helm();
+cudaError_t upload_tables_hex_helm0();
+cudaError_t upload_tables_hex_helm1();
+cudaError_t upload_tables_hex_helm2();
 cudaError_t upload_tables_hex_misc();
 cudaError_t upload_tables_quad();
 cudaError_t upload_all_tables() {
-  cudaError_t e = upload_tables_hex_helm();
+  cudaError_t e = upload_tables_hex_helm0();
+  if (e == cudaSuccess) e = upload_tables_hex_helm1();
+  if (e == cudaSuccess) e = upload_tables_hex_helm2();
   if (e == cudaSuccess) e = upload_tables_hex_misc();
   if (e == cudaSuccess) e = upload_tables_quad();
   return e;
@@ -307,8 +311,8 @@ int stdmat_prepare(sphp_coll* c, cudaStream_t s) {
     if (!t->fast)
       return fail(SPHP_ERR_UNSUPPORTED, "stdmat Helmholtz needs a sum-factorisation key to build H_e");
     const double bytes = 8.0 * c->E * nm * nm;
-    if (bytes > 48e9)
-      return fail(SPHP_ERR_UNSUPPORTED, "stdmat Helmholtz element matrices exceed the 48 GB budget");
+    if (bytes > 16e9)
+      return fail(SPHP_ERR_UNSUPPORTED, "stdmat Helmholtz element matrices exceed the 16 GB budget");
     CK(c->helm_H.ensure((size_t)bytes));
     CK(c->loc_x.ensure(sizeof(double) * c->E * nm));
     CK(c->loc_y.ensure(sizeof(double) * c->E * nm));

@@ -1,18 +1,59 @@
 // Fused hex Helmholtz (K4) instantiations: local, periodic-assembled and
 // explicit-map-assembled modes for the METRIC and AFFINE geometry encodings.
 #include "common.cuh"
-SPHP_DECLARE_TABLE_BANK(hex_helm)
+#ifndef HELM_PART
+#define HELM_PART 0
+#endif
+#if HELM_PART == 0
+SPHP_DECLARE_TABLE_BANK(hex_helm0)
+#elif HELM_PART == 1
+SPHP_DECLARE_TABLE_BANK(hex_helm1)
+#else
+SPHP_DECLARE_TABLE_BANK(hex_helm2)
+#endif
+#include <cstdlib>
+
 #include "launch.cuh"
 
 namespace sphp {
 
+// tile-shape variants: (input stages, shared-memory budget per CTA)
+template <int M, int Q, int GK, int NSTP, int BUDGET>
+static cudaError_t helm_variant(const OpArgs& oa, cudaStream_t s) {
+  using Probe = HexHelm<M, Q, GK, 1, 32, NSTP>;
+  constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(NSTP), Q * Q, BUDGET);
+  constexpr int NT = choose_nt(NE, Q * Q);
+  using Op = HexHelm<M, Q, GK, NE, NT, NSTP>;
+  return launch_mode<Op>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
+}
+
+static int helm_variant_env() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("SPHP_HELM_VARIANT");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+// default tile shapes (tools/time_helm.py sweep on B200, profiles/r01_tune.log):
+// one input stage and ~74 KB (local) / ~55 KB (gathering modes) per CTA
+// beat double buffering at every order: more resident CTAs hide more latency
+// than a second stage does.  SPHP_HELM_VARIANT=0..4 overrides for tuning.
 template <int M, int Q, int GK>
 static cudaError_t helm_go(const OpArgs& oa, cudaStream_t s) {
-  using Probe = HexHelm<M, Q, GK, 1, 32>;
-  constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(), Q * Q);
-  constexpr int NT = choose_nt(NE, Q * Q);
-  using Op = HexHelm<M, Q, GK, NE, NT>;
-  return launch_mode<Op>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
+  if (oa.mode == AsmMode::LOCAL || oa.mode == AsmMode::PERIODIC_GATHER) {
+    switch (helm_variant_env()) {
+      case 0: return helm_variant<M, Q, GK, 2, 110 * 1024>(oa, s);
+      case 1: return helm_variant<M, Q, GK, 1, 74 * 1024>(oa, s);
+      case 2: return helm_variant<M, Q, GK, 1, 55 * 1024>(oa, s);
+      case 3: return helm_variant<M, Q, GK, 2, 74 * 1024>(oa, s);
+      case 4: return helm_variant<M, Q, GK, 1, 110 * 1024>(oa, s);
+      default: break;
+    }
+    if (oa.mode == AsmMode::LOCAL) return helm_variant<M, Q, GK, 1, 74 * 1024>(oa, s);
+  }
+  return helm_variant<M, Q, GK, 1, 55 * 1024>(oa, s);
 }
 
 template <int M, int Q>
@@ -22,16 +63,31 @@ static cudaError_t helm_key(const OpArgs& oa, cudaStream_t s) {
   return cudaErrorNotSupported;
 }
 
-cudaError_t hex_helmholtz(const OpArgs& oa, cudaStream_t s) {
+#if HELM_PART == 0
+#define HELM_KEYS(X) X(2, 3) X(2, 4) X(3, 4) X(3, 5) X(4, 5) X(4, 6)
+cudaError_t hex_helmholtz_part0(const OpArgs& oa, cudaStream_t s) {
+#elif HELM_PART == 1
+#define HELM_KEYS(X) X(5, 6) X(5, 7) X(6, 7) X(6, 8)
+cudaError_t hex_helmholtz_part1(const OpArgs& oa, cudaStream_t s) {
+#else
+#define HELM_KEYS(X) X(7, 8) X(7, 9) X(8, 9) X(8, 10) X(9, 10) X(9, 11)
+cudaError_t hex_helmholtz_part2(const OpArgs& oa, cudaStream_t s) {
+#endif
 #define X(m, q) \
   if (oa.M == m && oa.Q == q) return helm_key<m, q>(oa, s);
-#ifdef SPHP_ONE_KEY
-  X(5, 6)
-#else
-  SPHP_HEX_KEYS(X)
-#endif
+  HELM_KEYS(X)
 #undef X
   return cudaErrorNotSupported;
 }
+
+#if HELM_PART == 0
+cudaError_t hex_helmholtz_part1(const OpArgs& oa, cudaStream_t s);
+cudaError_t hex_helmholtz_part2(const OpArgs& oa, cudaStream_t s);
+cudaError_t hex_helmholtz(const OpArgs& oa, cudaStream_t s) {
+  if (oa.M <= 4) return hex_helmholtz_part0(oa, s);
+  if (oa.M <= 6) return hex_helmholtz_part1(oa, s);
+  return hex_helmholtz_part2(oa, s);
+}
+#endif
 
 }  // namespace sphp

@@ -24,9 +24,10 @@ __host__ __device__ constexpr int pt_stride(int npts) { return even_up(npts); }
 // stages S1..S9; no quadrature data leaves shared memory.
 // GK: SPHP_GEOM_METRIC (7 per-point comps) or SPHP_GEOM_AFFINE (det, inv).
 // ===========================================================================
-template <int M_, int Q_, int GK, int NE_, int NT_>
+template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
 struct HexHelm {
   static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int NSTP = NSTP_;  // preferred input stages (1 or 2)
   static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
   static constexpr int IN = M3, OUT = M3;
   static constexpr int CS = pt_stride(Q3);

@@ -4,7 +4,7 @@
 #include "quad_ops.cuh"
 
 #ifndef SPHP_SMEM_BUDGET
-#define SPHP_SMEM_BUDGET (110 * 1024)  // per CTA: two resident CTAs per SM
+#define SPHP_SMEM_BUDGET (74 * 1024)  // per CTA: three resident CTAs per SM
 #endif
 #ifndef SPHP_MAX_ITEMS
 #define SPHP_MAX_ITEMS 256  // work items per stage per CTA
@@ -14,11 +14,11 @@ namespace sphp {
 
 // per-element shared-memory footprint of an Op (doubles)
 template <class Op1>
-constexpr int per_elem_doubles() {
-  return 2 * (Op1::IN + Op1::GEO) + Op1::OUT + Op1::WORK;
+constexpr int per_elem_doubles(int nst = 1) {
+  return nst * (Op1::IN + Op1::GEO) + Op1::OUT + Op1::WORK;
 }
-constexpr int choose_ne(int per_el_bytes, int items_per_el) {
-  int ne = SPHP_SMEM_BUDGET / per_el_bytes;
+constexpr int choose_ne(int per_el_bytes, int items_per_el, int budget = SPHP_SMEM_BUDGET) {
+  int ne = budget / per_el_bytes;
   int cap = SPHP_MAX_ITEMS / items_per_el;
   if (cap < 1) cap = 1;
   if (ne > cap) ne = cap;

@@ -133,6 +133,15 @@ struct ModeTraits {
   static constexpr bool CONTIG = MODE == 0 || MODE >= 3;
 };
 // ---------------------------------------------------------------------------
+// preferred number of input stages: Op::NSTP when the Op declares it, else 1
+// (measured: more resident CTAs beat a second stage, profiles/r01_tune.log)
+template <class Op>
+constexpr auto nst_pref_impl(int) -> decltype(Op::NSTP, int()) { return Op::NSTP; }
+template <class Op>
+constexpr int nst_pref_impl(...) { return 1; }
+template <class Op>
+constexpr int nst_pref() { return nst_pref_impl<Op>(0); }
+
 template <class Op, int MODE>
 struct Scaffold {
   static constexpr int NE = Op::NE, NT = Op::NT;
@@ -151,7 +160,7 @@ struct Scaffold {
   }
   // two input stages when they fit in 227 KB, else one (the next tile's copy
   // then overlaps only the part of the compute after the release point)
-  static constexpr int NST = fixed_bytes(2) <= 227 * 1024 ? 2 : 1;
+  static constexpr int NST = (nst_pref<Op>() == 2 && fixed_bytes(2) <= 227 * 1024) ? 2 : 1;
   static constexpr size_t SMEM_BYTES = fixed_bytes(NST);
   static_assert(SMEM_BYTES <= 227 * 1024, "one pipeline stage does not fit in shared memory");
 };
