@@ -217,7 +217,7 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_1906_03489_b200 as sp
-    from paper_1906_03489_b200 import _lib
+    from paper_1906_03489_b200 import _lib, parallel
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -261,11 +261,7 @@ def run_ours(args, rank, world, local_rank):
         e1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+        ms = parallel.max_over_ranks(e0.elapsed_time(e1), device=dev)
         return ms / steps
 
     # ---- headline: assembled apply, inputs resident ------------------------
@@ -277,6 +273,14 @@ def run_ours(args, rank, world, local_rank):
     ms = timed(lambda: op.apply(x, y), args.steps, 0)
     clk = clocks.stop()
     value = world * E * m ** 3 / (ms * 1e-3)
+    # replicas were fed rank-seeded inputs; the same input on every rank must
+    # give bitwise-identical outputs (deterministic kernels)
+    if world > 1:
+        x_same = torch.as_tensor(np.random.default_rng(SEED).uniform(-1, 1, ng), device=dev)
+        lo, hi = parallel.replica_checksum(op.apply(x_same, y))
+        replicas_identical = lo == hi
+    else:
+        replicas_identical = None
 
     # ---- e2e: the C-ABI host-buffer call (H2D x, apply, D2H y, sync) -------
     def e2e_step():
@@ -365,7 +369,8 @@ def run_ours(args, rank, world, local_rank):
                      "assembled_bytes_per_step": ab},
         "cpu_baseline": cpu,
         "clocks": clk,
-        "gpu_launches": args.steps * amap.num_colours,
+        "gpu_launches": args.steps * 2,  # gather+fused Helmholtz, owner-computes sum
+        "replicas_identical": replicas_identical,
     }
     if sweep is not None:
         line["sweep"] = sweep
@@ -452,11 +457,9 @@ def main():
         run_reference(args, rank, world)
         return
     if world > 1:
-        import torch
-        import torch.distributed as dist
+        from paper_1906_03489_b200 import parallel
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        parallel.init("nccl")
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

@@ -816,13 +816,13 @@ static int amap_device(const sphp_amap* ac) {
 
 // local (E, nm) -> global with the map's algorithm; accumulate adds to g
 static int amap_assemble_any(const sphp_amap* a, const double* loc, double* g, int accumulate,
-                             cudaStream_t s) {
+                             cudaStream_t s, int mode_major = 0) {
   if (a->alg == SPHP_ASSEMBLY_OWNER) {
     if (a->periodic) {
-      CK(owner_assemble_periodic(a->n, a->P, loc, g, accumulate, s));
+      CK(owner_assemble_periodic(a->n, a->P, loc, g, accumulate, mode_major, s));
     } else {
       CK(owner_assemble_csr(a->num_global, a->d_rowp.as<int64_t>(), a->d_ent.as<int>(), loc, g,
-                            accumulate, s));
+                            accumulate, a->nm, a->E, mode_major, s));
     }
     return SPHP_OK;
   }
@@ -1042,7 +1042,7 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
     cudaError_t e = sumfac_launch(c, o, s);
     if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no assembled kernel for this key");
     if (e != cudaSuccess) return cuda_fail(e, "sphp_helmholtz_assembled");
-    return amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s);
+    return amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s, /*mode_major=*/1);
   }
   if (!accumulate) CK(cudaMemsetAsync(y, 0, sizeof(double) * a->num_global, s));
   for (int col = 0; col < a->ncolours; ++col) {

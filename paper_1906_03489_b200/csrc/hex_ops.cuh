@@ -9,9 +9,19 @@
 // Tables (B, Bd = dB/dxi, D, w) are read from __constant__ memory with
 // compile-time indices (c_tab must be declared by the including TU).
 #pragma once
+#include <type_traits>
+
 #include "pipeline.cuh"
 
 namespace sphp {
+
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+// smallest v >= lo with v = Q (mod 16)
+__host__ __device__ constexpr int pitch_mod16(int lo, int Q) {
+  int v = lo;
+  while (v % 16 != Q % 16) ++v;
+  return v;
+}
 
 // per-element geometry record sizes (see sphp_geom_stride)
 __host__ __device__ constexpr int pt_stride(int npts) { return even_up(npts); }
@@ -19,13 +29,265 @@ __host__ __device__ constexpr int pt_stride(int npts) { return even_up(npts); }
 // work-item loop: items are distributed over the CTA's NT threads
 #define SPHP_FOR_ITEMS(NITEMS, w) for (int w = threadIdx.x; w < (NITEMS); w += NT)
 
+// ---------------------------------------------------------------------------
+// contiguous row helpers: Q doubles at a 16-byte aligned address move as
+// LDS.128 / STS.128 when Q is even (row stride Q then makes 8-lane phases
+// bank-conflict free), as scalar accesses otherwise (odd stride: also free)
+// ---------------------------------------------------------------------------
+template <int Q>
+__device__ __forceinline__ void load_row(const double* __restrict__ p, double* x) {
+  if constexpr (Q % 2 == 0) {
+    const double2* v = reinterpret_cast<const double2*>(p);
+#pragma unroll
+    for (int h = 0; h < Q / 2; ++h) {
+      const double2 t = v[h];
+      x[2 * h] = t.x;
+      x[2 * h + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < Q; ++k) x[k] = p[k];
+  }
+}
+template <int Q>
+__device__ __forceinline__ void store_row(double* __restrict__ p, const double* x) {
+  if constexpr (Q % 2 == 0) {
+    double2* v = reinterpret_cast<double2*>(p);
+#pragma unroll
+    for (int h = 0; h < Q / 2; ++h) v[h] = make_double2(x[2 * h], x[2 * h + 1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < Q; ++k) p[k] = x[k];
+  }
+}
+
 // ===========================================================================
 // Fused matrix-free Helmholtz (K4): y = sum_ab B_a^T G_ab B_b uhat + lam B^T wJ B uhat
-// stages S1..S9; no quadrature data leaves shared memory.
+// (geometry.py:171-184 as one sum-factorised pass; no quadrature data
+// leaves shared memory).  GK: SPHP_GEOM_METRIC (7 per-point comps, point
+// order (i,j,k)) or SPHP_GEOM_AFFINE (det, inv per element).
+//
+// Stages (m = M modes, Q points per direction; e = element of the tile):
+//   S1 r->k   c[p,q,r]  -> T1[p,q,k]            pencils (p,q)
+//   S2 q->j   T1        -> T2[p,j,k]            pencils (p,k)
+//   S3 p->i   T2        -> u, d0 = d/dxi0 u     pencils (j,k)   (dense Q^3)
+//   S4 j      u         -> d1                   pencils (i,k)
+//   S5 k      row (i,j): d2 = D u in registers, f = G grad u, mass term,
+//             t = lam wJ u + D2^T f2; writes t, f0, f1 (contiguous rows,
+//             128-bit accesses, geometry rows read straight from the stage)
+//   S6 j      t += D1^T f1                      pencils (i,k)
+//   S7 i->p   T2'[p,j,k] = B t + dB f0          pencils (j,k)
+//   S8 j->q, S9 k->r    -> y[p,q,r]
+// ===========================================================================
+template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
+struct HexHelmK {
+  static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int NSTP = NSTP_;  // preferred input stages (1 or 2)
+  static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
+  static constexpr int IN = M3, OUT = M3;
+  static constexpr int CS = pt_stride(Q3);
+  static constexpr int GEO = (GK == SPHP_GEOM_METRIC) ? 7 * CS : 10;
+  static constexpr int QK = odd_up(Q);  // T1 row pitch (odd: row stores conflict free)
+  // plane pitches congruent to Q mod 16: lanes (p, k) then address
+  // consecutive banks in the q/j-pencil stages
+  static constexpr int PP1 = pitch_mod16(M * QK, Q);  // T1[p][q][k]
+  static constexpr int PP2 = pitch_mod16(Q * Q, Q);   // T2[p][j][k], rows of Q
+  static constexpr int SE = even_up(cmax(Q3, cmax(M * PP1, M * PP2)));  // element stride
+  static constexpr int WORK = 3 * SE;
+  using T = Tab<M, Q>;
+
+  template <class R, class W>
+  __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
+                                 double* __restrict__ work, double* __restrict__ out, double lam,
+                                 R release, W pre_out, const double* tab) {
+    double* W0 = work;                // T1 | u, t | T1'
+    double* W1 = work + NE * SE;      // T2 | d1, f1 | T2'
+    double* W2 = work + 2 * NE * SE;  // d0, f0
+
+    // S1: r-contraction  c[p,q,r] -> T1[p,q,k]
+    SPHP_FOR_ITEMS(NE * M * M, w) {
+      int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
+      pencil<M, Q, T::B, 1, Q, 1, 1, false>(tab, cin + e * M3 + pq * M,
+                                            W0 + e * SE + p * PP1 + q * QK);
+    }
+    __syncthreads();
+    // S2: q-contraction  T1[p,q,k] -> T2[p,j,k]
+    SPHP_FOR_ITEMS(NE * M * Q, w) {
+      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
+      pencil<M, Q, T::B, 1, Q, QK, Q, false>(tab, W0 + e * SE + p * PP1 + k,
+                                             W1 + e * SE + p * PP2 + k);
+    }
+    __syncthreads();
+    // S3: p-contraction  T2 -> u (W0) and d0 (W2), dense (i,j,k)
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
+      const double* src = W1 + e * SE + jk;
+      double x[M];
+#pragma unroll
+      for (int p = 0; p < M; ++p) x[p] = src[p * PP2];
+      double* du = W0 + e * SE + jk;
+      double* d0 = W2 + e * SE + jk;
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int p = 0; p < M; ++p) {
+          a = fma(tab[T::B + p * Q + i], x[p], a);
+          b = fma(tab[T::BD + p * Q + i], x[p], b);
+        }
+        du[i * Q * Q] = a;
+        d0[i * Q * Q] = b;
+      }
+    }
+    __syncthreads();
+    // S4: d1 = D along j of u
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
+      pencil<Q, Q, T::D, Q, 1, Q, Q, false>(tab, W0 + e * SE + i * Q * Q + k,
+                                            W1 + e * SE + i * Q * Q + k);
+    }
+    __syncthreads();
+    // S5: rows along k: d2, fluxes, mass, t = lam wJ u + D2^T f2
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), ij = w - e * (Q * Q), i = ij / Q, j = ij - i * Q;
+      const int row = e * SE + ij * Q;
+      double u[Q], d[Q], f0[Q], f1[Q], f2[Q], g[Q];
+      load_row<Q>(W0 + row, u);
+      // d2 = D u (registers)
+      double d2[Q];
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < Q; ++l) acc = fma(tab[T::D + k * Q + l], u[l], acc);
+        d2[k] = acc;
+      }
+      if constexpr (GK == SPHP_GEOM_METRIC) {
+        const double* gr = geo + e * GEO + ij * Q;
+        load_row<Q>(W2 + row, d);  // d0
+        load_row<Q>(gr + 0 * CS, g);  // G00
+#pragma unroll
+        for (int k = 0; k < Q; ++k) f0[k] = g[k] * d[k];
+        load_row<Q>(gr + 1 * CS, g);  // G01
+#pragma unroll
+        for (int k = 0; k < Q; ++k) f1[k] = g[k] * d[k];
+        double h[Q];
+        load_row<Q>(W1 + row, h);  // d1
+#pragma unroll
+        for (int k = 0; k < Q; ++k) f0[k] = fma(g[k], h[k], f0[k]);
+        load_row<Q>(gr + 2 * CS, g);  // G02
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          f2[k] = g[k] * d[k];
+          f0[k] = fma(g[k], d2[k], f0[k]);
+        }
+        load_row<Q>(gr + 3 * CS, g);  // G11
+#pragma unroll
+        for (int k = 0; k < Q; ++k) f1[k] = fma(g[k], h[k], f1[k]);
+        load_row<Q>(gr + 4 * CS, g);  // G12
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          f1[k] = fma(g[k], d2[k], f1[k]);
+          f2[k] = fma(g[k], h[k], f2[k]);
+        }
+        load_row<Q>(gr + 5 * CS, g);  // G22
+#pragma unroll
+        for (int k = 0; k < Q; ++k) f2[k] = fma(g[k], d2[k], f2[k]);
+        load_row<Q>(gr + 6 * CS, g);  // wJ
+#pragma unroll
+        for (int k = 0; k < Q; ++k) u[k] = lam * g[k] * u[k];
+      } else {
+        // affine: G_ab = w_i w_j w_k det sum_c inv[a,c] inv[b,c]
+        const double* gg = geo + e * GEO;
+        const double det = gg[0];
+        const double* iv = gg + 1;
+        const double a00 = det * (iv[0] * iv[0] + iv[1] * iv[1] + iv[2] * iv[2]);
+        const double a01 = det * (iv[0] * iv[3] + iv[1] * iv[4] + iv[2] * iv[5]);
+        const double a02 = det * (iv[0] * iv[6] + iv[1] * iv[7] + iv[2] * iv[8]);
+        const double a11 = det * (iv[3] * iv[3] + iv[4] * iv[4] + iv[5] * iv[5]);
+        const double a12 = det * (iv[3] * iv[6] + iv[4] * iv[7] + iv[5] * iv[8]);
+        const double a22 = det * (iv[6] * iv[6] + iv[7] * iv[7] + iv[8] * iv[8]);
+        const double wij = tab[T::W + i] * tab[T::W + j];
+        load_row<Q>(W2 + row, d);
+        double h[Q];
+        load_row<Q>(W1 + row, h);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          const double wq = wij * tab[T::W + k];
+          f0[k] = wq * (a00 * d[k] + a01 * h[k] + a02 * d2[k]);
+          f1[k] = wq * (a01 * d[k] + a11 * h[k] + a12 * d2[k]);
+          f2[k] = wq * (a02 * d[k] + a12 * h[k] + a22 * d2[k]);
+          u[k] = lam * (wq * det) * u[k];
+        }
+      }
+      // t = mass + D2^T f2
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        double t = u[k];
+#pragma unroll
+        for (int l = 0; l < Q; ++l) t = fma(tab[T::D + l * Q + k], f2[l], t);
+        g[k] = t;
+      }
+      store_row<Q>(W0 + row, g);
+      store_row<Q>(W2 + row, f0);
+      store_row<Q>(W1 + row, f1);
+    }
+    __syncthreads();
+    release();
+    // S6: t += D1^T f1 along j
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
+      pencil<Q, Q, T::D, 1, Q, Q, Q, true>(tab, W1 + e * SE + i * Q * Q + k,
+                                           W0 + e * SE + i * Q * Q + k);
+    }
+    __syncthreads();
+    // S7: i -> p: T2'[p,j,k] = sum_i B[p,i] t + Bd[p,i] f0   (into W1)
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
+      const int base = e * SE + jk;
+      double t[Q], f0[Q];
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        t[i] = W0[base + i * Q * Q];
+        f0[i] = W2[base + i * Q * Q];
+      }
+#pragma unroll
+      for (int p = 0; p < M; ++p) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          acc = fma(tab[T::B + p * Q + i], t[i], acc);
+          acc = fma(tab[T::BD + p * Q + i], f0[i], acc);
+        }
+        W1[e * SE + p * PP2 + jk] = acc;
+      }
+    }
+    __syncthreads();
+    // S8: j -> q  (W1 -> W0)
+    SPHP_FOR_ITEMS(NE * M * Q, w) {
+      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
+      pencil<Q, M, T::B, Q, 1, Q, QK, false>(tab, W1 + e * SE + p * PP2 + k,
+                                             W0 + e * SE + p * PP1 + k);
+    }
+    pre_out();
+    __syncthreads();
+    // S9: k -> r  (W0 -> out, dense)
+    SPHP_FOR_ITEMS(NE * M * M, w) {
+      int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
+      pencil<Q, M, T::B, Q, 1, 1, 1, false>(tab, W0 + e * SE + p * PP1 + q * QK,
+                                            out + e * M3 + pq * M);
+    }
+  }
+};
+
+// ===========================================================================
+// Fused Helmholtz, variant J: the pointwise stage runs on pencils along j
+// (used when Q % 4 == 0, where contiguous k-rows of Q doubles map every
+// 128-bit access of an 8-lane phase to two bank groups).
 // GK: SPHP_GEOM_METRIC (7 per-point comps) or SPHP_GEOM_AFFINE (det, inv).
 // ===========================================================================
 template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
-struct HexHelm {
+struct HexHelmJ {
   static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
   static constexpr int NSTP = NSTP_;  // preferred input stages (1 or 2)
   static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
@@ -200,6 +462,11 @@ struct HexHelm {
     }
   }
 };
+
+// variant selection: k-row pointwise stage unless Q % 4 == 0
+template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
+using HexHelm = typename std::conditional<(Q_ % 4 == 0), HexHelmJ<M_, Q_, GK, NE_, NT_, NSTP_>,
+                                          HexHelmK<M_, Q_, GK, NE_, NT_, NSTP_>>::type;
 
 // ===========================================================================
 // BwdTrans (K1): u = (B x B x B)^T c   (collections.py:133-150)

@@ -488,7 +488,8 @@ cudaError_t symmetrise(int64_t E, int nm, double* H, cudaStream_t s) {
 // blocks they read stay in L2.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) owner_periodic_kernel(int n, int P, const double* __restrict__ loc,
-                                                             double* __restrict__ y, int accumulate) {
+                                                             double* __restrict__ y, int accumulate,
+                                                             int mode_major) {
   // block = 32 consecutive elements along x (lanes) for one (ey, ez) row
   // segment; warp w walks owned dofs o = w, w+8, ...: every warp-level branch
   // below is uniform, and the neighbour blocks a CTA reads stay in L1/L2
@@ -503,6 +504,11 @@ __global__ void __launch_bounds__(256) owner_periodic_kernel(int n, int P, const
   auto wrapm = [n](int i) { return i < 0 ? i + n : i; };
   auto eid = [&](int i, int j, int k) { return wrapm(i) + n * (wrapm(j) + n * wrapm(k)); };
   auto flat = [m](int p, int q, int r) { return (p * m + q) * m + r; };
+  // local entry (element, mode): element-major e*nm + nl, or mode-major
+  // nl*N3 + e (written by the gathering fused kernel; coalesced here)
+  auto at = [&](int el, int nl) -> double {
+    return mode_major ? loc[(size_t)nl * N3 + el] : loc[(size_t)el * nm + nl];
+  };
   const int base[3] = {ex, ey, ez};
   for (int o = threadIdx.x >> 5; o < per; o += blockDim.x >> 5) {
     double acc = 0.0;
@@ -516,7 +522,7 @@ __global__ void __launch_bounds__(256) owner_periodic_kernel(int n, int P, const
         for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
           for (int c = 0; c < 2; ++c)
-            acc += loc[(size_t)eid(ex - a, ey - bb, ez - c) * nm + flat(a, bb, c)];
+            acc += at(eid(ex - a, ey - bb, ez - c), flat(a, bb, c));
     } else if ((oo -= 1) < 3 * b) {  // edge leaving the vertex along d, degree k
       const int d = oo / b, k = oo - d * b + 2;
       gid = N3 + (d * N3 + e) * b + (k - 2);
@@ -537,7 +543,7 @@ __global__ void __launch_bounds__(256) owner_periodic_kernel(int n, int P, const
               idx[a] = st[w++];
             }
           }
-          acc += loc[(size_t)eid(c[0], c[1], c[2]) * nm + flat(idx[0], idx[1], idx[2])];
+          acc += at(eid(c[0], c[1], c[2]), flat(idx[0], idx[1], idx[2]));
         }
     } else if ((oo -= 3 * b) < 3 * b * b) {  // face normal d at the vertex
       const int d = oo / (b * b), r2 = oo - d * b * b;
@@ -558,13 +564,13 @@ __global__ void __launch_bounds__(256) owner_periodic_kernel(int n, int P, const
             idx[a] = kk[w++];
           }
         }
-        acc += loc[(size_t)eid(c[0], c[1], c[2]) * nm + flat(idx[0], idx[1], idx[2])];
+        acc += at(eid(c[0], c[1], c[2]), flat(idx[0], idx[1], idx[2]));
       }
     } else {  // interior, owned by the element alone
       oo -= 3 * b * b;
       const int p = oo / (b * b) + 2, q = (oo / b) % b + 2, r = oo % b + 2;
       gid = N3 * (1 + 3 * b + 3 * b * b) + e * b * b * b + oo;
-      acc = loc[(size_t)e * nm + flat(p, q, r)];
+      acc = at(e, flat(p, q, r));
     }
     y[gid] = accumulate ? y[gid] + acc : acc;
   }
@@ -574,29 +580,34 @@ __global__ void __launch_bounds__(256) owner_periodic_kernel(int n, int P, const
 // (-(idx+1)) for sign -1; rows sorted by local index (element order)
 __global__ void owner_csr_kernel(int64_t ng, const int64_t* __restrict__ rowp,
                                  const int* __restrict__ ent, const double* __restrict__ loc,
-                                 double* __restrict__ y, int accumulate) {
+                                 double* __restrict__ y, int accumulate, int nm, int64_t E,
+                                 int mode_major) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= ng) return;
   double acc = 0.0;
   for (int64_t k = rowp[g]; k < rowp[g + 1]; ++k) {
     const int c = ent[k];
-    acc += c >= 0 ? loc[c] : -loc[-(int64_t)c - 1];
+    const int64_t i = c >= 0 ? c : -(int64_t)c - 1;  // element-major local index
+    const int64_t j = mode_major ? (i % nm) * E + i / nm : i;
+    acc += c >= 0 ? loc[j] : -loc[j];
   }
   y[g] = accumulate ? y[g] + acc : acc;
 }
 
 cudaError_t owner_assemble_periodic(int n, int P, const double* loc, double* y, int accumulate,
-                                    cudaStream_t s) {
+                                    int mode_major, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const int64_t blocks = (int64_t)((n + 31) / 32) * n * n;
-  owner_periodic_kernel<<<(unsigned)blocks, 256, 0, s>>>(n, P, loc, y, accumulate);
+  owner_periodic_kernel<<<(unsigned)blocks, 256, 0, s>>>(n, P, loc, y, accumulate, mode_major);
   return cudaGetLastError();
 }
 
 cudaError_t owner_assemble_csr(int64_t ng, const int64_t* rowp, const int* ent, const double* loc,
-                               double* y, int accumulate, cudaStream_t s) {
+                               double* y, int accumulate, int nm, int64_t E, int mode_major,
+                               cudaStream_t s) {
   if (ng == 0) return cudaSuccess;
-  owner_csr_kernel<<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(ng, rowp, ent, loc, y, accumulate);
+  owner_csr_kernel<<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(ng, rowp, ent, loc, y, accumulate, nm,
+                                                                E, mode_major);
   return cudaGetLastError();
 }
 

@@ -49,9 +49,11 @@ cudaError_t elem_matvec(int64_t E, int nm, const double* H, const double* x, dou
 cudaError_t unit_block(int64_t E, int nm, int n, double* x, cudaStream_t s);
 cudaError_t store_column(int64_t E, int nm, int n, const double* y, double* H, cudaStream_t s);
 cudaError_t symmetrise(int64_t E, int nm, double* H, cudaStream_t s);
+// loc is element-major (E, nm), or mode-major (nm, E) when mode_major != 0
 cudaError_t owner_assemble_periodic(int n, int P, const double* loc, double* y, int accumulate,
-                                    cudaStream_t s);
+                                    int mode_major, cudaStream_t s);
 cudaError_t owner_assemble_csr(int64_t ng, const int64_t* rowp, const int* ent, const double* loc,
-                               double* y, int accumulate, cudaStream_t s);
+                               double* y, int accumulate, int nm, int64_t E, int mode_major,
+                               cudaStream_t s);
 
 }  // namespace sphp

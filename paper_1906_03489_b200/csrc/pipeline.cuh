@@ -385,8 +385,15 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     __syncthreads();
 
     // ---- write back ------------------------------------------------------
-    if (!MT::SCATTER) {
+    if (MODE == 0) {
       for (int i = tid; i < r * OUT; i += NT) a.out[w0 * OUT + i] = out_s[i];
+    } else if (!MT::SCATTER) {
+      // gathering modes feed the owner-computes sum: mode-major local block
+      // loc[nl * E + e], so that sum reads it coalesced across elements
+      for (int i = tid; i < r * OUT; i += NT) {
+        const int nl = i / r, e = i - nl * r;
+        a.out[(int64_t)nl * a.E + w0 + e] = out_s[e * OUT + nl];
+      }
     } else {
       // signed scatter-add of one colour class: every global dof touched by
       // this launch belongs to exactly one element, so plain read-add-write
