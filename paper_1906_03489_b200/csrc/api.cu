@@ -1042,7 +1042,7 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
     cudaError_t e = sumfac_launch(c, o, s);
     if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no assembled kernel for this key");
     if (e != cudaSuccess) return cuda_fail(e, "sphp_helmholtz_assembled");
-    return amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s, /*mode_major=*/1);
+    return amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s, /*mode_major=*/0);
   }
   if (!accumulate) CK(cudaMemsetAsync(y, 0, sizeof(double) * a->num_global, s));
   for (int col = 0; col < a->ncolours; ++col) {

@@ -1,6 +1,8 @@
 // Launch helpers: tile-size selection per (operator, M, Q) and the (M, Q)
 // dispatch switch over the fast key set.
 #pragma once
+#include <cstdlib>
+
 #include "quad_ops.cuh"
 
 #ifndef SPHP_SMEM_BUDGET
@@ -78,6 +80,13 @@ cudaError_t launch_pipe(const OpArgs& oa, int64_t gstride, int64_t goff, cudaStr
   const int64_t ntiles = (count + Op::NE - 1) / Op::NE;
   int64_t grid = (int64_t)oa.num_sms * c.occ;
   if (grid > ntiles) grid = ntiles;
+  // SPHP_MAX_GRID caps the persistent grid (tests use it to make every CTA
+  // walk many tiles on small meshes)
+  static const int64_t max_grid = [] {
+    const char* e = getenv("SPHP_MAX_GRID");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  if (max_grid > 0 && grid > max_grid) grid = max_grid;
   kern<<<(unsigned)grid, Op::NT, Sc::SMEM_BYTES, s>>>(a);
   return cudaGetLastError();
 }

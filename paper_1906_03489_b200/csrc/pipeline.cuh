@@ -385,15 +385,10 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     __syncthreads();
 
     // ---- write back ------------------------------------------------------
-    if (MODE == 0) {
+    if (!MT::SCATTER) {
+      // element-major local block (a mode-major layout, coalesced for the
+      // owner-computes sum, measured slower overall: profiles/r01_bench_*.log)
       for (int i = tid; i < r * OUT; i += NT) a.out[w0 * OUT + i] = out_s[i];
-    } else if (!MT::SCATTER) {
-      // gathering modes feed the owner-computes sum: mode-major local block
-      // loc[nl * E + e], so that sum reads it coalesced across elements
-      for (int i = tid; i < r * OUT; i += NT) {
-        const int nl = i / r, e = i - nl * r;
-        a.out[(int64_t)nl * a.E + w0 + e] = out_s[e * OUT + nl];
-      }
     } else {
       // signed scatter-add of one colour class: every global dof touched by
       // this launch belongs to exactly one element, so plain read-add-write
@@ -427,6 +422,9 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
         for (int u = 0; u < U; ++u)
           if (g[u] >= 0) a.yg[g[u]] = yv[u] + v[u];
       }
+      // the next iteration overwrites icur (ids / entity bases) before its
+      // first barrier: every thread must be done with this tile's indices
+      __syncthreads();
     }
   }
   if (MODE != 0) cp_async_wait<0>();
