@@ -81,6 +81,18 @@ def helm_flops(P, E):
     return 2 * E * (2 * staged + 6 * Q ** 4 + 11 * Q ** 3)
 
 
+def ncu_traffic(kernel, P, n):
+    """DRAM bytes per launch of `kernel` at (P, n) from the committed ncu
+    capture (profiles/r01_ncu_traffic.json), or None."""
+    p = ROOT / "profiles" / "r01_ncu_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text()).get(kernel)
+    if d and d.get("P") == P and d.get("n") == n:
+        return d["bytes_per_launch"]
+    return None
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -296,6 +308,7 @@ def run_ours(args, rank, world, local_rank):
     yl = torch.empty_like(c)
     k_ms = timed(lambda: coll.apply(c, yl), args.steps, args.warmup)
     peak, peak_kind = measured_peaks()
+    traffic = ncu_traffic("helmholtz_local", P, n)
     kb = local_bytes(P, E)
     achieved = kb / (k_ms * 1e-3) / 1e9
     # assembled apply as a whole against the same roofline
@@ -361,7 +374,9 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": 8 * ng,
                 "d2h_bytes_per_step": 8 * ng, "ms_per_step": e2e_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, same kernel/config)"
+                     if traffic else None,
                      "kernel": "pipe_kernel<HexHelm> (fused local Helmholtz, one launch)",
                      "bytes_per_launch": kb, "launch_ms": k_ms,
                      "fp64_tflops": helm_flops(P, E) / (k_ms * 1e-3) / 1e12,
