@@ -192,6 +192,35 @@ int sphp_helmholtz_assembled_host(sphp_coll* c, const sphp_amap* a,
                                   const double* x, double* y,
                                   sphp_stream stream);
 
+/* ---- solver support: GlobalSystem.diag / solve_pcg (assembly.py:185-266) -- */
+/* diagonal of every elemental Helmholtz matrix (E, nmodes) — assemble it
+ * with sphp_assemble for the Jacobi preconditioner                          */
+int sphp_helmholtz_diagonal(sphp_coll* c, double* out, sphp_stream stream);
+/* deterministic vector reductions for CG.  ws: device workspace of
+ * sphp_reduction_workspace() doubles; results land in ws[0], ws[1].        */
+int64_t sphp_reduction_workspace(void);
+/* ws[0] = a.b, ws[1] = c.d (c, d may both be NULL)                          */
+int sphp_vec_dot2(int64_t n, const double* a, const double* b, const double* c,
+                  const double* d, double* ws, sphp_stream stream);
+/* x = 0, r = rhs, z = p = dinv*r; ws = [r.z, r.r]                           */
+int sphp_cg_init(int64_t n, const double* rhs, const double* dinv, double* x,
+                 double* r, double* z, double* p, double* ws, sphp_stream stream);
+/* x += alpha p, r -= alpha Ap, z = dinv*r; ws = [r.z, r.r]                  */
+int sphp_cg_update(int64_t n, double alpha, const double* p, const double* ap,
+                   double* x, double* r, const double* dinv, double* z,
+                   double* ws, sphp_stream stream);
+/* p = z + beta p                                                            */
+int sphp_cg_direction(int64_t n, double beta, const double* z, double* p,
+                      sphp_stream stream);
+/* build_assembly_map (assembly.py:72-138) for meshio.structured_quad_mesh
+ * (meshio.py:377-413) with per-element orders; dirichlet_mask bits:
+ * 1 south, 2 east, 4 north, 8 west.  Codes packed per element (m_e^2 each,
+ * element e at offsets[e], offsets has nx*ny+1 entries); NULL arrays only
+ * return the counts.                                                         */
+int sphp_quadmap_structured(int nx, int ny, const int* orders, int dirichlet_mask,
+                            int64_t* num_global, int64_t* num_dirichlet,
+                            int64_t* offsets, int64_t* codes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,8 @@ from .geometry import (GEOM_AFFINE, GEOM_METRIC, GEOM_NONE, GEOM_POINT, MAP_AFFI
                        MAP_HEX_SINE, MAP_QUAD_SINE, ElementBatch, GeometryError, GeomFactors,
                        from_factors, structured_geometry)
 from .quadrature import PointsKey, PointsType, QuadratureError, diff_matrix, make_rule
+from .solvers import (ConvergenceError, HelmholtzSolver, assembled_diagonal,
+                      quad_structured_maps, solve_pcg)
 from .stdregions import (ExpansionError, Shape, StdExpansion, make_expansion, make_hex,
                          make_quad, make_seg)
 

@@ -86,6 +86,13 @@ _SIGS = {
     "sphp_assemble": (_i, [_p, _p, _p, _p]),
     "sphp_helmholtz_assembled": (_i, [_p, _p, _p, _p, _i, _p]),
     "sphp_helmholtz_assembled_host": (_i, [_p, _p, _p, _p, _p]),
+    "sphp_helmholtz_diagonal": (_i, [_p, _p, _p]),
+    "sphp_reduction_workspace": (_i64, []),
+    "sphp_vec_dot2": (_i, [_i64, _p, _p, _p, _p, _p, _p]),
+    "sphp_cg_init": (_i, [_i64, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "sphp_cg_update": (_i, [_i64, _d, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "sphp_cg_direction": (_i, [_i64, _d, _p, _p, _p]),
+    "sphp_quadmap_structured": (_i, [_i, _i, _p, _i, _i64p, _i64p, _p, _p]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "misc.h"
+#include "solver.h"
 #include "tables.h"
 
 using namespace sphp;
@@ -144,7 +145,7 @@ struct sphp_tables {
   bool fast = false;  // sum-factorisation kernels available for this key
   // lazily built device copies
   std::mutex mu;
-  DevBuf d_z, d_w, d_wstd;
+  DevBuf d_z, d_w, d_wstd, d_B, d_Bd;
   std::vector<double> wstd;  // tensor weights, point order
 };
 
@@ -203,6 +204,10 @@ int tables_device(sphp_tables* t) {
   CK(cudaMemcpy(t->d_w.p, t->w[0].data(), sizeof(double) * t->q[0], cudaMemcpyHostToDevice));
   CK(t->d_wstd.ensure(sizeof(double) * t->np));
   CK(cudaMemcpy(t->d_wstd.p, t->wstd.data(), sizeof(double) * t->np, cudaMemcpyHostToDevice));
+  CK(t->d_B.ensure(sizeof(double) * t->B[0].size()));
+  CK(cudaMemcpy(t->d_B.p, t->B[0].data(), sizeof(double) * t->B[0].size(), cudaMemcpyHostToDevice));
+  CK(t->d_Bd.ensure(sizeof(double) * t->Bd[0].size()));
+  CK(cudaMemcpy(t->d_Bd.p, t->Bd[0].data(), sizeof(double) * t->Bd[0].size(), cudaMemcpyHostToDevice));
   return SPHP_OK;
 }
 
@@ -1078,6 +1083,150 @@ int sphp_helmholtz_assembled_host(sphp_coll* c, const sphp_amap* a, const double
   if (rc) return rc;
   CK(cudaMemcpyAsync(y, c->host_out.p, b, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return SPHP_OK;
+}
+
+// ---- solver support (assembly.py:185-266) ------------------------------------
+int sphp_helmholtz_diagonal(sphp_coll* c, double* out, sphp_stream stream) {
+  if (!c || !out) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  if (c->op != SPHP_OP_HELMHOLTZ) return fail(SPHP_ERR_BAD_ARG, "collection is not a Helmholtz operator");
+  sphp_tables* t = c->t;
+  for (int a = 1; a < t->dim; ++a)
+    if (t->m[a] != t->m[0] || t->q[a] != t->q[0])
+      return fail(SPHP_ERR_UNSUPPORTED, "diagonal needs equal modes/points per direction");
+  int rc = tables_device(t);
+  if (rc) return rc;
+  DiagJob j;
+  j.dim = t->dim;
+  j.m = t->m[0];
+  j.Q = t->q[0];
+  j.kind = c->geom_kind;
+  j.E = c->E;
+  j.stride = c->gstride;
+  j.cs = c->cs;
+  j.lam = c->lam;
+  j.B = t->d_B.as<double>();
+  j.Bd = t->d_Bd.as<double>();
+  j.w = t->d_w.as<double>();
+  j.geom = c->geom;
+  j.out = out;
+  CK(helmholtz_diagonal(j, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int64_t sphp_reduction_workspace(void) { return 2 + reduction_partials(); }
+
+int sphp_vec_dot2(int64_t n, const double* a, const double* b, const double* c, const double* d,
+                  double* ws, sphp_stream stream) {
+  if (!a || !b || !ws || ((c == nullptr) != (d == nullptr))) return fail(SPHP_ERR_BAD_ARG, "bad dot arguments");
+  CK(vec_dot2(n, a, b, c, d, ws + 2, ws, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int sphp_cg_init(int64_t n, const double* rhs, const double* dinv, double* x, double* r, double* z,
+                 double* p, double* ws, sphp_stream stream) {
+  if (!rhs || !dinv || !x || !r || !z || !p || !ws) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  CK(cg_init(n, rhs, dinv, x, r, z, p, ws + 2, ws, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int sphp_cg_update(int64_t n, double alpha, const double* p, const double* ap, double* x, double* r,
+                   const double* dinv, double* z, double* ws, sphp_stream stream) {
+  if (!p || !ap || !x || !r || !dinv || !z || !ws) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  CK(cg_update(n, alpha, p, ap, x, r, dinv, z, ws + 2, ws, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int sphp_cg_direction(int64_t n, double beta, const double* z, double* p, sphp_stream stream) {
+  if (!z || !p) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  CK(cg_direction(n, beta, z, p, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+// build_assembly_map (assembly.py:72-138) for meshio.structured_quad_mesh
+// (meshio.py:377-413): vertex j*(nx+1)+i, horizontal segments j*nx+i, then
+// vertical (ny+1)*nx + j*(nx+1) + i, element j*nx+i with loop
+// (v(i,j), v(i+1,j), v(i+1,j+1), v(i,j+1)); every edge is traversed
+// forward, so all signs are +1.  dirichlet_mask: 1 south, 2 east, 4 north,
+// 8 west.  codes packed per element (m_e^2 each) at offsets[e].
+int sphp_quadmap_structured(int nx, int ny, const int* orders, int dmask, int64_t* num_global,
+                            int64_t* num_dirichlet, int64_t* offsets, int64_t* codes) {
+  if (nx < 1 || ny < 1 || !orders || !num_global) return fail(SPHP_ERR_BAD_ARG, "bad arguments");
+  const int64_t E = (int64_t)nx * ny;
+  const int64_t NV = (int64_t)(nx + 1) * (ny + 1);
+  const int64_t NS = (int64_t)(ny + 1) * nx + (int64_t)ny * (nx + 1);
+  auto vid = [nx](int i, int j) -> int64_t { return (int64_t)j * (nx + 1) + i; };
+  auto hseg = [nx](int i, int j) -> int64_t { return (int64_t)j * nx + i; };
+  auto vseg = [nx, ny](int i, int j) -> int64_t { return (int64_t)(ny + 1) * nx + (int64_t)j * (nx + 1) + i; };
+  for (int64_t e = 0; e < E; ++e)
+    if (orders[e] < 1) return fail(SPHP_ERR_BAD_ARG, "orders must be >= 1");
+  std::vector<int> eord(NS, 1 << 30);
+  for (int j = 0; j < ny; ++j)
+    for (int i = 0; i < nx; ++i) {
+      const int P = orders[(int64_t)j * nx + i];
+      const int64_t segs[4] = {hseg(i, j), vseg(i + 1, j), hseg(i, j + 1), vseg(i, j)};
+      for (int k = 0; k < 4; ++k) eord[segs[k]] = std::min(eord[segs[k]], P);
+    }
+  std::vector<char> dseg(NS, 0), dvert(NV, 0);
+  auto mark_h = [&](int j) {
+    for (int i = 0; i < nx; ++i) {
+      dseg[hseg(i, j)] = 1;
+      dvert[vid(i, j)] = dvert[vid(i + 1, j)] = 1;
+    }
+  };
+  auto mark_v = [&](int i) {
+    for (int j = 0; j < ny; ++j) {
+      dseg[vseg(i, j)] = 1;
+      dvert[vid(i, j)] = dvert[vid(i, j + 1)] = 1;
+    }
+  };
+  if (dmask & 1) mark_h(0);
+  if (dmask & 2) mark_v(nx);
+  if (dmask & 4) mark_h(ny);
+  if (dmask & 8) mark_v(0);
+  std::vector<int64_t> vg(NV), eg(NS);  // vertex gid; first gid of each segment's bubbles
+  int64_t gid = 0;
+  for (int64_t v = 0; v < NV; ++v)
+    if (dvert[v]) vg[v] = gid++;
+  for (int64_t sdx = 0; sdx < NS; ++sdx)
+    if (dseg[sdx]) {
+      eg[sdx] = gid;
+      gid += std::max(0, eord[sdx] - 1);
+    }
+  const int64_t nd = gid;
+  for (int64_t v = 0; v < NV; ++v)
+    if (!dvert[v]) vg[v] = gid++;
+  for (int64_t sdx = 0; sdx < NS; ++sdx)
+    if (!dseg[sdx]) {
+      eg[sdx] = gid;
+      gid += std::max(0, eord[sdx] - 1);
+    }
+  int64_t off = 0;
+  for (int j = 0; j < ny; ++j)
+    for (int i = 0; i < nx; ++i) {
+      const int64_t e = (int64_t)j * nx + i;
+      const int m = orders[e] + 1;
+      if (offsets) offsets[e] = off;
+      std::vector<int64_t> l2g((size_t)m * m, -2);
+      auto flat = [m](int p, int q) { return p * m + q; };
+      const int64_t loop[4] = {vid(i, j), vid(i + 1, j), vid(i + 1, j + 1), vid(i, j + 1)};
+      const int vmodes[4] = {0, m, m + 1, 1};
+      for (int k = 0; k < 4; ++k) l2g[vmodes[k]] = vg[loop[k]];
+      const int64_t segs[4] = {hseg(i, j), vseg(i + 1, j), hseg(i, j + 1), vseg(i, j)};
+      for (int le = 0; le < 4; ++le)
+        for (int k = 2; k < m; ++k) {
+          const int mode = le == 0 ? flat(k, 0) : le == 1 ? flat(1, k) : le == 2 ? flat(k, 1) : flat(0, k);
+          l2g[mode] = (k <= eord[segs[le]]) ? eg[segs[le]] + (k - 2) : -1;
+        }
+      for (int n = 0; n < m * m; ++n)
+        if (l2g[n] == -2) l2g[n] = gid++;  // interiors, ascending local order
+      if (codes)
+        for (int n = 0; n < m * m; ++n) codes[off + n] = l2g[n];
+      off += (int64_t)m * m;
+    }
+  if (offsets) offsets[E] = off;
+  *num_global = gid;
+  if (num_dirichlet) *num_dirichlet = nd;
   return SPHP_OK;
 }
 

@@ -27,6 +27,7 @@ static cudaError_t helm_variant(const OpArgs& oa, cudaStream_t s) {
   return launch_mode<Op>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
 }
 
+#ifdef SPHP_TUNING
 static int helm_variant_env() {
   static int v = -2;
   if (v == -2) {
@@ -35,6 +36,7 @@ static int helm_variant_env() {
   }
   return v;
 }
+#endif
 
 // default tile shapes (tools/time_helm.py sweep on B200, profiles/r01_tune.log):
 // one input stage and ~74 KB (local) / ~55 KB (gathering modes) per CTA
@@ -43,6 +45,7 @@ static int helm_variant_env() {
 template <int M, int Q, int GK>
 static cudaError_t helm_go(const OpArgs& oa, cudaStream_t s) {
   if (oa.mode == AsmMode::LOCAL || oa.mode == AsmMode::PERIODIC_GATHER) {
+#ifdef SPHP_TUNING  // tile-shape sweep build (make EXTRA_NVFLAGS=-DSPHP_TUNING)
     switch (helm_variant_env()) {
       case 0: return helm_variant<M, Q, GK, 2, 110 * 1024>(oa, s);
       case 1: return helm_variant<M, Q, GK, 1, 74 * 1024>(oa, s);
@@ -51,6 +54,7 @@ static cudaError_t helm_go(const OpArgs& oa, cudaStream_t s) {
       case 4: return helm_variant<M, Q, GK, 1, 110 * 1024>(oa, s);
       default: break;
     }
+#endif
     if (oa.mode == AsmMode::LOCAL) return helm_variant<M, Q, GK, 1, 74 * 1024>(oa, s);
   }
   return helm_variant<M, Q, GK, 1, 55 * 1024>(oa, s);

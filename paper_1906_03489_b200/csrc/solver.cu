@@ -1,0 +1,232 @@
+// Solver support on the device (solve_pcg /
+// helmholtz_solve, assembly.py:218-354):
+//   * the diagonal of the elemental Helmholtz operators (the Jacobi
+//     preconditioner of GlobalSystem.diag, assembly.py:208-214), evaluated
+//     exactly from the basis tables and the stored geometry;
+//   * deterministic CG vector kernels: fixed grid, fixed-order block trees
+//     and a fixed-order final sum, so repeated solves are bitwise equal.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/spechp_b200.h"
+#include "solver.h"
+
+namespace sphp {
+
+// diag_n = sum_pts sum_ab G_ab d_a phi_n d_b phi_n + lam wJ phi_n^2 with
+// d_a phi_n from the exact derivative tables (hex: n = (p,q,r); quad: (p,q))
+__global__ void helm_diag_kernel(DiagJob j) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int m = j.m, Q = j.Q, d = j.dim;
+  const int nm = d == 3 ? m * m * m : m * m;
+  if (tid >= j.E * nm) return;
+  const int64_t e = tid / nm;
+  const int n = (int)(tid - e * nm);
+  const double* B = j.B;
+  const double* Bd = j.Bd;
+  const double* w = j.w;
+  const double* g = j.geom + e * j.stride;
+  double acc = 0.0;
+  if (d == 3) {
+    const int p = n / (m * m), q = (n / m) % m, r = n % m;
+    double G[6], wj;
+    if (j.kind == SPHP_GEOM_AFFINE) {
+      const double det = g[0];
+      const double* iv = g + 1;
+      int c = 0;
+      for (int a = 0; a < 3; ++a)
+        for (int b = a; b < 3; ++b)
+          G[c++] = det * (iv[a * 3] * iv[b * 3] + iv[a * 3 + 1] * iv[b * 3 + 1] + iv[a * 3 + 2] * iv[b * 3 + 2]);
+      wj = det;
+    }
+    for (int i = 0; i < Q; ++i)
+      for (int jj = 0; jj < Q; ++jj)
+        for (int k = 0; k < Q; ++k) {
+          const int pt = (i * Q + jj) * Q + k;
+          double g00, g01, g02, g11, g12, g22, wq;
+          if (j.kind == SPHP_GEOM_METRIC) {
+            g00 = g[pt];
+            g01 = g[j.cs + pt];
+            g02 = g[2 * j.cs + pt];
+            g11 = g[3 * j.cs + pt];
+            g12 = g[4 * j.cs + pt];
+            g22 = g[5 * j.cs + pt];
+            wq = g[6 * j.cs + pt];
+          } else {
+            const double ww = w[i] * w[jj] * w[k];
+            g00 = ww * G[0];
+            g01 = ww * G[1];
+            g02 = ww * G[2];
+            g11 = ww * G[3];
+            g12 = ww * G[4];
+            g22 = ww * G[5];
+            wq = ww * wj;
+          }
+          const double bp = B[p * Q + i], bq = B[q * Q + jj], br = B[r * Q + k];
+          const double d0 = Bd[p * Q + i] * bq * br, d1 = bp * Bd[q * Q + jj] * br,
+                       d2 = bp * bq * Bd[r * Q + k], ph = bp * bq * br;
+          acc += g00 * d0 * d0 + g11 * d1 * d1 + g22 * d2 * d2 +
+                 2.0 * (g01 * d0 * d1 + g02 * d0 * d2 + g12 * d1 * d2) + j.lam * wq * ph * ph;
+        }
+  } else {
+    const int p = n / m, q = n % m;
+    double G[3], wj;
+    if (j.kind == SPHP_GEOM_AFFINE) {
+      const double det = g[0];
+      G[0] = det * (g[1] * g[1] + g[2] * g[2]);
+      G[1] = det * (g[1] * g[3] + g[2] * g[4]);
+      G[2] = det * (g[3] * g[3] + g[4] * g[4]);
+      wj = det;
+    }
+    for (int i = 0; i < Q; ++i)
+      for (int jj = 0; jj < Q; ++jj) {
+        const int pt = i * Q + jj;
+        double g00, g01, g11, wq;
+        if (j.kind == SPHP_GEOM_METRIC) {
+          g00 = g[pt];
+          g01 = g[j.cs + pt];
+          g11 = g[2 * j.cs + pt];
+          wq = g[3 * j.cs + pt];
+        } else {
+          const double ww = w[i] * w[jj];
+          g00 = ww * G[0];
+          g01 = ww * G[1];
+          g11 = ww * G[2];
+          wq = ww * wj;
+        }
+        const double bp = B[p * Q + i], bq = B[q * Q + jj];
+        const double d0 = Bd[p * Q + i] * bq, d1 = bp * Bd[q * Q + jj], ph = bp * bq;
+        acc += g00 * d0 * d0 + g11 * d1 * d1 + 2.0 * g01 * d0 * d1 + j.lam * wq * ph * ph;
+      }
+  }
+  j.out[tid] = acc;
+}
+
+cudaError_t helmholtz_diagonal(const DiagJob& j, cudaStream_t s) {
+  const int nm = j.dim == 3 ? j.m * j.m * j.m : j.m * j.m;
+  const int64_t total = j.E * nm;
+  if (total == 0) return cudaSuccess;
+  helm_diag_kernel<<<(unsigned)((total + 127) / 128), 128, 0, s>>>(j);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// deterministic reductions: RB blocks x 256 threads, grid-stride in a fixed
+// pattern, fixed tree in shared memory, then one block sums the RB partials
+// in order
+// ---------------------------------------------------------------------------
+constexpr int RB = 592;  // 4 x 148 SMs
+constexpr int RT = 256;
+
+__device__ __forceinline__ void block_sum2(double a, double b, double* partial) {
+  __shared__ double sa[RT], sb[RT];
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  for (int h = RT / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+      sa[threadIdx.x] += sa[threadIdx.x + h];
+      sb[threadIdx.x] += sb[threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = sa[0];
+    partial[2 * blockIdx.x + 1] = sb[0];
+  }
+}
+
+__global__ void __launch_bounds__(RT) dot2_kernel(int64_t n, const double* __restrict__ a,
+                                                  const double* __restrict__ b,
+                                                  const double* __restrict__ c,
+                                                  const double* __restrict__ d, double* partial) {
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x; i < n; i += (int64_t)RB * RT) {
+    s0 = fma(a[i], b[i], s0);
+    if (c) s1 = fma(c[i], d[i], s1);
+  }
+  block_sum2(s0, s1, partial);
+}
+
+// x += alpha p; r -= alpha Ap; z = dinv r; partials of (r.z, r.r)
+__global__ void __launch_bounds__(RT) cg_update_kernel(int64_t n, double alpha,
+                                                       const double* __restrict__ p,
+                                                       const double* __restrict__ ap,
+                                                       double* __restrict__ x, double* __restrict__ r,
+                                                       const double* __restrict__ dinv,
+                                                       double* __restrict__ z, double* partial) {
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x; i < n; i += (int64_t)RB * RT) {
+    const double xi = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, ap[i], r[i]);
+    const double zi = dinv[i] * ri;
+    x[i] = xi;
+    r[i] = ri;
+    z[i] = zi;
+    s0 = fma(ri, zi, s0);
+    s1 = fma(ri, ri, s1);
+  }
+  block_sum2(s0, s1, partial);
+}
+
+__global__ void __launch_bounds__(RT) cg_init_kernel(int64_t n, const double* __restrict__ rhs,
+                                                     const double* __restrict__ dinv, double* x,
+                                                     double* r, double* z, double* p, double* partial) {
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x; i < n; i += (int64_t)RB * RT) {
+    const double ri = rhs[i];
+    const double zi = dinv[i] * ri;
+    x[i] = 0.0;
+    r[i] = ri;
+    z[i] = zi;
+    p[i] = zi;
+    s0 = fma(ri, zi, s0);
+    s1 = fma(ri, ri, s1);
+  }
+  block_sum2(s0, s1, partial);
+}
+
+__global__ void cg_direction_kernel(int64_t n, double beta, const double* __restrict__ z,
+                                    double* __restrict__ p) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+
+__global__ void finish_kernel(const double* partial, double* out) {
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < RB; ++k) {
+      a += partial[2 * k];
+      b += partial[2 * k + 1];
+    }
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+cudaError_t vec_dot2(int64_t n, const double* a, const double* b, const double* c, const double* d,
+                     double* partial, double* out, cudaStream_t s) {
+  dot2_kernel<<<RB, RT, 0, s>>>(n, a, b, c, d, partial);
+  finish_kernel<<<1, 32, 0, s>>>(partial, out);
+  return cudaGetLastError();
+}
+cudaError_t cg_init(int64_t n, const double* rhs, const double* dinv, double* x, double* r, double* z,
+                    double* p, double* partial, double* out, cudaStream_t s) {
+  cg_init_kernel<<<RB, RT, 0, s>>>(n, rhs, dinv, x, r, z, p, partial);
+  finish_kernel<<<1, 32, 0, s>>>(partial, out);
+  return cudaGetLastError();
+}
+cudaError_t cg_update(int64_t n, double alpha, const double* p, const double* ap, double* x, double* r,
+                      const double* dinv, double* z, double* partial, double* out, cudaStream_t s) {
+  cg_update_kernel<<<RB, RT, 0, s>>>(n, alpha, p, ap, x, r, dinv, z, partial);
+  finish_kernel<<<1, 32, 0, s>>>(partial, out);
+  return cudaGetLastError();
+}
+cudaError_t cg_direction(int64_t n, double beta, const double* z, double* p, cudaStream_t s) {
+  cg_direction_kernel<<<RB, RT, 0, s>>>(n, beta, z, p);
+  return cudaGetLastError();
+}
+int reduction_partials() { return 2 * RB; }
+
+}  // namespace sphp

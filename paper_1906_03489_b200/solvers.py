@@ -1,0 +1,153 @@
+"""Device Helmholtz solve: preconditioned CG on the fused assembled operator
+(reference `solve_pcg` / `helmholtz_solve`,
+assembly.py:218-354).
+
+The operator is `GlobalHelmholtz` (gather -> fused elemental Helmholtz ->
+deterministic C0 sum); the Jacobi preconditioner is the assembled diagonal
+of the elemental matrices (`GlobalSystem.diag`, assembly.py:208-214),
+evaluated on the device by `sphp_helmholtz_diagonal`; the CG vector updates
+and dot products are deterministic CUDA kernels (`sphp_cg_*`, fixed
+reduction order), so a solve is bitwise reproducible.  Dirichlet dofs are the
+leading block of the numbering (assembly.py:89-103): they are pinned by
+masking, exactly the reference's restriction to free dofs.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .assembly import AssemblyError, AssemblyMap, GlobalHelmholtz, assemble
+
+
+class ConvergenceError(RuntimeError):
+    """assembly.py:33-36: carries the residual history."""
+
+    def __init__(self, message, residuals):
+        super().__init__(message)
+        self.residuals = residuals
+
+
+def _ws(device):
+    return torch.empty(int(_lib.lib.sphp_reduction_workspace()), dtype=torch.float64, device=device)
+
+
+def assembled_diagonal(batches, num_global, device=None):
+    """Assembled diagonal of A^T H A over per-order batches (signs square away)."""
+    diag = None
+    for coll, amap in batches:
+        loc = torch.empty((coll.num_elements, amap.nmodes), dtype=torch.float64,
+                          device=device or "cuda")
+        _lib.check(_lib.lib.sphp_helmholtz_diagonal(coll._handle, _lib.ptr(loc),
+                                                    _lib.stream_ptr()))
+        part = assemble(amap, loc)
+        diag = part if diag is None else diag + part
+    return diag
+
+
+def solve_pcg(apply, rhs, tol=1e-12, max_iter=2000, diag=None):
+    """Jacobi-preconditioned CG (assembly.py:218-266) on device vectors.
+
+    apply(p, out) writes A p into out.  Returns x; raises ConvergenceError
+    with the residual history when max_iter is reached."""
+    if diag is None:
+        dinv = torch.ones_like(rhs)
+    else:  # inv_diag = 1 / where(diag == 0, 1, diag)   (assembly.py:242)
+        dinv = 1.0 / torch.where(diag == 0, torch.ones_like(diag), diag)
+    return _solve_with_dinv(apply, rhs, dinv, tol, max_iter)
+
+
+class HelmholtzSolver:
+    """-lap(u) + lam u = f with the first `num_dirichlet` global dofs pinned
+    (helmholtz_solve, assembly.py:316-354), on per-order batches
+    [(Collection(HELMHOLTZ), AssemblyMap)]."""
+
+    def __init__(self, batches, num_global, num_dirichlet=0):
+        self.op = GlobalHelmholtz(batches, num_global)
+        self.batches = list(batches)
+        self.num_global = int(num_global)
+        self.nd = int(num_dirichlet)
+        self.diag = assembled_diagonal(self.batches, self.num_global)
+        self._buf = torch.empty(self.num_global, dtype=torch.float64, device=self.diag.device)
+
+    def _apply_free(self, v, out):
+        # A restricted to the free block: Dirichlet entries of the input and
+        # of the result are zero (v's Dirichlet part is zero already)
+        self.op.apply(v, out)
+        out[: self.nd] = 0.0
+        return out
+
+    def solve(self, rhs, u_dirichlet=None, tol=1e-12, max_iter=3000):
+        """rhs: assembled load vector (num_global); u_dirichlet: lifted
+        boundary values (num_global, Dirichlet block used) or None (zero)."""
+        b = rhs.clone()
+        if u_dirichlet is not None and self.nd:
+            ud = torch.zeros_like(b)
+            ud[: self.nd] = u_dirichlet[: self.nd]
+            b -= self.op.apply(ud, self._buf)
+        b[: self.nd] = 0.0
+        diag = self.diag.clone()
+        diag[: self.nd] = 0.0
+        # zero preconditioner on pinned dofs keeps CG in the free subspace
+        dinv = torch.where(diag == 0, torch.zeros_like(diag), 1.0 / torch.where(diag == 0,
+                                                                             torch.ones_like(diag), diag))
+        x = _solve_with_dinv(self._apply_free, b, dinv, tol, max_iter)
+        if u_dirichlet is not None and self.nd:
+            x[: self.nd] = u_dirichlet[: self.nd]
+        return x
+
+
+def _solve_with_dinv(apply, rhs, dinv, tol, max_iter):
+    """solve_pcg with an explicit inverse diagonal (zeros allowed)."""
+    n = rhs.numel()
+    dev = rhs.device
+    x, r, z, p, ap = (torch.empty_like(rhs) for _ in range(5))
+    ws = _ws(dev)
+    s = _lib.stream_ptr()
+    _lib.check(_lib.lib.sphp_cg_init(n, _lib.ptr(rhs), _lib.ptr(dinv), _lib.ptr(x), _lib.ptr(r),
+                                     _lib.ptr(z), _lib.ptr(p), _lib.ptr(ws), s))
+    rz, rr = ws[:2].tolist()
+    rhs_norm = float(np.sqrt(rr))
+    if rhs_norm == 0.0:
+        return x
+    residuals = [1.0]
+    for _ in range(max_iter):
+        apply(p, ap)
+        _lib.check(_lib.lib.sphp_vec_dot2(n, _lib.ptr(p), _lib.ptr(ap), None, None, _lib.ptr(ws), s))
+        alpha = rz / ws[0].item()
+        _lib.check(_lib.lib.sphp_cg_update(n, alpha, _lib.ptr(p), _lib.ptr(ap), _lib.ptr(x),
+                                           _lib.ptr(r), _lib.ptr(dinv), _lib.ptr(z), _lib.ptr(ws), s))
+        rz_new, rr = ws[:2].tolist()
+        res = float(np.sqrt(max(rr, 0.0))) / rhs_norm
+        residuals.append(res)
+        if res <= tol:
+            return x
+        _lib.check(_lib.lib.sphp_cg_direction(n, rz_new / rz, _lib.ptr(z), _lib.ptr(p), s))
+        rz = rz_new
+    raise ConvergenceError(f"PCG did not reach {tol} in {max_iter} iterations "
+                           f"(final residual {residuals[-1]:.3e})", residuals)
+
+
+def quad_structured_maps(nx, ny, orders, dirichlet=()):
+    """build_assembly_map (assembly.py:72-138) for structured_quad_mesh(nx, ny)
+    on the native library, split into per-order batches.
+    Returns (num_global, num_dirichlet, {P: (elem_ids, AssemblyMap)})."""
+    import ctypes as C
+
+    orders = np.ascontiguousarray(np.broadcast_to(np.asarray(orders, dtype=np.int32), (nx * ny,)))
+    mask = 0
+    for name in dirichlet:
+        mask |= {"south": 1, "east": 2, "north": 4, "west": 8}[name]
+    ng, nd = C.c_int64(), C.c_int64()
+    offsets = np.empty(nx * ny + 1, dtype=np.int64)
+    codes = np.empty(int(np.sum((orders.astype(np.int64) + 1) ** 2)), dtype=np.int64)
+    _lib.check(_lib.lib.sphp_quadmap_structured(nx, ny, _lib.ptr(orders), mask, C.byref(ng),
+                                                C.byref(nd), _lib.ptr(offsets), _lib.ptr(codes)),
+               AssemblyError)
+    out = {}
+    for P in sorted(set(int(v) for v in orders)):
+        ids = np.nonzero(orders == P)[0]
+        nm = (P + 1) ** 2
+        rows = np.stack([codes[offsets[e]:offsets[e] + nm] for e in ids])
+        out[P] = (ids, AssemblyMap.explicit(rows, ng.value))
+    return ng.value, nd.value, out, (offsets, codes)

@@ -129,8 +129,34 @@ for tag, (nx, ny, dn, seed) in {"a": (4, 3, (), 1), "b": (5, 4, ("south", "west"
     x = r2.uniform(-1, 1, am.num_global)
     out[f"amap/{tag}/x"] = x
     out[f"amap/{tag}/y"] = sysm.apply(x)
+    out[f"amap/{tag}/diag"] = sysm.diag
     out[f"amap/{tag}/wts"] = np.concatenate([e.gf.weights_world for e in els3])
     out[f"amap/{tag}/inv"] = np.concatenate([e.gf.inv.reshape(-1) for e in els3])
+
+# --- Helmholtz spectral convergence (test_acceptance.py:93-125), reference solve ---
+from spechp.assembly import helmholtz_solve  # noqa: E402
+from spechp.geometry import integral_world, x_map  # noqa: E402
+from spechp.stdregions import bwd_trans  # noqa: E402
+
+errs, iters = [], []
+for P in range(2, 9):
+    mesh = structured_quad_mesh(4, 4)
+    els4 = build_elements(mesh, orders=P)
+    exact = lambda x, y: np.sin(np.pi * x) * np.sin(np.pi * y)
+    forcing = []
+    for el in els4:
+        xy = x_map(el.geom, el.exp.points)
+        forcing.append((2 * np.pi ** 2 + 1.0) * exact(xy[:, 0], xy[:, 1]))
+    dirichlet = {nm: (lambda x, y: 0.0) for nm in ("south", "east", "north", "west")}
+    coeffs, info = helmholtz_solve(mesh, els4, 1.0, forcing, dirichlet, tol=1e-13, max_iter=6000)
+    num = den = 0.0
+    for el, c in zip(els4, coeffs):
+        xy = x_map(el.geom, el.exp.points)
+        diff = bwd_trans(el.exp, c) - exact(xy[:, 0], xy[:, 1])
+        num += integral_world(el.exp, el.gf, diff ** 2)
+        den += integral_world(el.exp, el.gf, exact(xy[:, 0], xy[:, 1]) ** 2)
+    errs.append(np.sqrt(num / den))
+out["helm_conv/errors"] = np.array(errs)
 
 # --- Listing 1 ---------------------------------------------------------------------------
 q7 = make_quad(7, num_points=9)

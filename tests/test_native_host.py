@@ -163,3 +163,20 @@ def test_mac_count_formula():
     assert mac_count("quad", "iproductwrtbase", "sumfac", 4, 6, 1) == 366
     assert mac_count("quad", "physderiv", "sumfac", 4, 6, 1, geometry=False) == 432
     assert mac_count("hex", "bwdtrans", "sumfac", 4, 6, 1) == 125 * 6 + 25 * 36 + 5 * 216
+
+
+@pytest.mark.parametrize("tag", ["a", "b", "c"])
+def test_native_quad_map_matches_reference(tag):
+    """sphp_quadmap_structured == the reference's build_assembly_map
+    (assembly.py:72-138) on structured_quad_mesh, bit for bit: Dirichlet
+    block, min edge order, pinned modes, numbering."""
+    nx, ny = (int(v) for v in G[f"amap/{tag}/shape"])
+    orders = G[f"amap/{tag}/orders"]
+    dn = tuple(d for d in G[f"amap/{tag}/dirichlet"] if d)
+    ng, nd, batches, (offsets, codes) = sp.quad_structured_maps(nx, ny, orders, dn)
+    assert ng == int(G[f"amap/{tag}/num_global"])
+    assert nd == int(G[f"amap/{tag}/num_dirichlet"])
+    assert np.array_equal(codes, G[f"amap/{tag}/l2g"])          # signs all +1 / pinned -1
+    assert np.array_equal(np.where(codes >= 0, 1.0, 0.0), G[f"amap/{tag}/signs"])
+    for P, (ids, amap) in batches.items():
+        assert np.all(orders[ids] == P) and amap.nmodes == (P + 1) ** 2
