@@ -165,9 +165,12 @@ int sphp_amap_destroy(sphp_amap* a);
  *          owner-computes pass that sums each global dof in a fixed order;
  *   COLOUR colour classes (parity colours on periodic grids, greedy
  *          colouring of explicit maps) fused gather/scatter-add, one launch
- *          per colour in a fixed colour order.                            */
+ *          per colour in a fixed colour order;
+ *   SPLIT  scatter kernel -> fused operator on the local block -> owner
+ *          sum (three launches).                                          */
 #define SPHP_ASSEMBLY_OWNER 0
 #define SPHP_ASSEMBLY_COLOUR 1
+#define SPHP_ASSEMBLY_SPLIT 2
 int sphp_amap_set_algorithm(sphp_amap* a, int alg);
 int sphp_amap_info(const sphp_amap* a, int64_t* num_elements, int* nmodes,
                    int64_t* num_global, int* num_colours);

@@ -92,9 +92,11 @@ class AssemblyMap:
         return cls(h)
 
     def set_algorithm(self, alg):
-        """'owner' (default: gather -> local -> owner-computes sum) or
+        """'owner' (default: gather -> local -> owner-computes sum),
+        'split' (scatter kernel -> local operator -> owner sum) or
         'colour' (fused colour-ordered scatter-add)."""
-        code = {"owner": _lib.ASSEMBLY_OWNER, "colour": _lib.ASSEMBLY_COLOUR}[alg]
+        code = {"owner": _lib.ASSEMBLY_OWNER, "colour": _lib.ASSEMBLY_COLOUR,
+                "split": _lib.ASSEMBLY_SPLIT}[alg]
         _lib.check(_lib.lib.sphp_amap_set_algorithm(self._h, code), AssemblyError)
         self.algorithm = alg
         return self

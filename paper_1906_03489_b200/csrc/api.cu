@@ -174,6 +174,7 @@ struct sphp_amap {
   int alg = SPHP_ASSEMBLY_OWNER;
   std::mutex mu;
   DevBuf d_codes, d_elist, d_rowp, d_ent;  // explicit: codes, colour lists, CSR
+  DevBuf d_entity;                          // periodic: (E, 27) entity bases
   AmapDev dev() const {
     AmapDev a;
     a.periodic = periodic;
@@ -276,6 +277,7 @@ OpArgs base_args(const sphp_coll* c) {
   a.elist = nullptr;
   a.nlist = 0;
   a.codes = nullptr;
+  a.ent_g = nullptr;
   a.n = 0;
   a.colour = 0;
   return a;
@@ -785,7 +787,19 @@ static int amap_colour_and_upload(sphp_amap* a) {
 // device copies of an explicit map, made on first device use
 static int amap_device(const sphp_amap* ac) {
   sphp_amap* a = const_cast<sphp_amap*>(ac);
-  if (a->periodic || a->d_codes.p) return SPHP_OK;
+  if (a->periodic) {
+    if (a->d_entity.p) return SPHP_OK;
+    std::lock_guard<std::mutex> lk(a->mu);
+    if (a->d_entity.p) return SPHP_OK;
+    DevBuf tmp;
+    CK(tmp.ensure(sizeof(int) * a->E * 27));
+    CK(periodic_entity_table(a->n, a->P, tmp.as<int>(), 0));
+    CK(cudaDeviceSynchronize());
+    std::swap(a->d_entity.p, tmp.p);
+    std::swap(a->d_entity.bytes, tmp.bytes);
+    return SPHP_OK;
+  }
+  if (a->d_codes.p) return SPHP_OK;
   std::lock_guard<std::mutex> lk(a->mu);
   if (a->d_codes.p) return SPHP_OK;
   std::vector<int> codes32(a->codes_host.size());
@@ -822,7 +836,7 @@ static int amap_device(const sphp_amap* ac) {
 // local (E, nm) -> global with the map's algorithm; accumulate adds to g
 static int amap_assemble_any(const sphp_amap* a, const double* loc, double* g, int accumulate,
                              cudaStream_t s, int mode_major = 0) {
-  if (a->alg == SPHP_ASSEMBLY_OWNER) {
+  if (a->alg == SPHP_ASSEMBLY_OWNER || a->alg == SPHP_ASSEMBLY_SPLIT) {
     if (a->periodic) {
       CK(owner_assemble_periodic(a->n, a->P, loc, g, accumulate, mode_major, s));
     } else {
@@ -965,7 +979,7 @@ int sphp_hexmap_variable(int n, const int* orders, int64_t* num_global, int64_t*
 
 int sphp_amap_set_algorithm(sphp_amap* a, int alg) {
   if (!a) return fail(SPHP_ERR_BAD_ARG, "null map");
-  if (alg != SPHP_ASSEMBLY_OWNER && alg != SPHP_ASSEMBLY_COLOUR)
+  if (alg != SPHP_ASSEMBLY_OWNER && alg != SPHP_ASSEMBLY_COLOUR && alg != SPHP_ASSEMBLY_SPLIT)
     return fail(SPHP_ERR_BAD_ARG, "unknown assembly algorithm");
   a->alg = alg;
   return SPHP_OK;
@@ -1032,6 +1046,20 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
   OpArgs o = base_args(c);
   o.xg = x;
   o.yg = y;
+  if (a->alg == SPHP_ASSEMBLY_SPLIT) {
+    // scatter -> fused local operator -> owner-computes sum (three launches;
+    // the fused kernel then runs in its block-input form)
+    CK(c->loc_x.ensure(sizeof(double) * c->E * c->t->nm));
+    CK(c->loc_y.ensure(sizeof(double) * c->E * c->t->nm));
+    CK(amap_scatter(a->dev(), x, c->loc_x.as<double>(), s));
+    o.in = c->loc_x.as<double>();
+    o.out = c->loc_y.as<double>();
+    o.mode = AsmMode::LOCAL;
+    cudaError_t e = sumfac_launch(c, o, s);
+    if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no kernel for this key");
+    if (e != cudaSuccess) return cuda_fail(e, "sphp_helmholtz_assembled");
+    return amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s, 0);
+  }
   if (a->alg == SPHP_ASSEMBLY_OWNER) {
     // gather -> fused elemental operator -> local block, then the
     // owner-computes sum (two launches, no colour passes)
@@ -1040,6 +1068,7 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
     if (a->periodic) {
       o.mode = AsmMode::PERIODIC_GATHER;
       o.n = a->n;
+      o.ent_g = a->d_entity.as<int>();
     } else {
       o.mode = AsmMode::EXPLICIT_GATHER;
       o.codes = a->d_codes.as<int>();

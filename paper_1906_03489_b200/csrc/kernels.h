@@ -30,6 +30,7 @@ struct OpArgs {
   const int* elist;   // EXPLICIT: element ids of this colour (device)
   int64_t nlist;      // number of elements in this colour
   const int* codes;   // EXPLICIT: (E, nm) int32 codes
+  const int* ent_g;   // PERIODIC_GATHER: precomputed (E, 27) entity bases (optional)
   int n;              // PERIODIC: grid size
   int colour;         // PERIODIC: colour id 0..7
 };

@@ -73,6 +73,7 @@ cudaError_t launch_pipe(const OpArgs& oa, int64_t gstride, int64_t goff, cudaStr
   a.elist = oa.elist;
   a.nlist = oa.nlist;
   a.codes = oa.codes;
+  a.ent_g = oa.ent_g;
   a.n = oa.n;
   a.colour = oa.colour;
   const int64_t count = (MODE == 0 || MODE >= 3) ? oa.E : oa.nlist;

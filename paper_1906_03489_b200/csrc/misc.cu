@@ -10,6 +10,7 @@
 
 #include "../../include/spechp_b200.h"
 #include "misc.h"
+#include "periodic.cuh"
 
 namespace sphp {
 
@@ -205,6 +206,8 @@ __device__ __forceinline__ void map_entry(const AmapDev& m, int64_t e, int nl, i
   }
 }
 
+cudaError_t periodic_scatter(int n, int P, const double* g, double* loc, cudaStream_t s);
+
 __global__ void scatter_kernel(AmapDev m, const double* __restrict__ g, double* __restrict__ loc) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= m.E * m.nm) return;
@@ -241,6 +244,7 @@ __global__ void assemble_colour_kernel(AmapDev m, const double* __restrict__ loc
 }
 
 cudaError_t amap_scatter(const AmapDev& m, const double* g, double* loc, cudaStream_t s) {
+  if (m.periodic) return periodic_scatter(m.n, m.P, g, loc, s);
   const int64_t total = m.E * m.nm;
   if (total == 0) return cudaSuccess;
   scatter_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(m, g, loc);
@@ -487,7 +491,7 @@ cudaError_t symmetrise(int64_t E, int nm, double* H, cudaStream_t s) {
 // P^3 dofs — and threads walk elements in id order so the neighbour
 // blocks they read stay in L2.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) owner_periodic_kernel(int n, int P, const double* __restrict__ loc,
+__global__ void __launch_bounds__(256, 6) owner_periodic_kernel(int n, int P, const double* __restrict__ loc,
                                                              double* __restrict__ y, int accumulate,
                                                              int mode_major) {
   // block = 32 consecutive elements along x (lanes) for one (ey, ez) row
@@ -608,6 +612,63 @@ cudaError_t owner_assemble_csr(int64_t ng, const int64_t* rowp, const int* ent, 
   if (ng == 0) return cudaSuccess;
   owner_csr_kernel<<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(ng, rowp, ent, loc, y, accumulate, nm,
                                                                 E, mode_major);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// periodic scatter (global -> local block), entity-based int32 indexing:
+// a CTA takes EB consecutive elements, builds their 27 entity bases and the
+// per-mode code table in shared memory, then writes the local block in
+// order (coalesced stores; the x reads hit L2 for neighbouring elements)
+// ---------------------------------------------------------------------------
+constexpr int SC_EB = 8;
+__global__ void __launch_bounds__(256) periodic_scatter_kernel(int n, int P, const double* __restrict__ g,
+                                                               double* __restrict__ loc) {
+  extern __shared__ int sh[];
+  const int m = P + 1, nm = m * m * m;
+  int* ent = sh;                // SC_EB * 27
+  int* mtab = sh + SC_EB * 27;  // nm
+  const int N3 = n * n * n;
+  const int e0 = blockIdx.x * SC_EB;
+  for (int i = threadIdx.x; i < nm; i += blockDim.x) mtab[i] = mode_code(m, i);
+  for (int i = threadIdx.x; i < SC_EB * 27; i += blockDim.x) {
+    const int e = e0 + i / 27, k = i % 27;
+    int v = 0;
+    if (e < N3) v = entity_base(n, P, e % n, (e / n) % n, e / (n * n), k);
+    ent[i] = v;
+  }
+  __syncthreads();
+  const int cnt = (N3 - e0 < SC_EB ? N3 - e0 : SC_EB) * nm;
+  double* out = loc + (size_t)e0 * nm;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const int e = i / nm, nl = i - e * nm;
+    const int c = mtab[nl];
+    out[i] = g[ent[e * 27 + (c & 31)] + (c >> 5)];
+  }
+}
+
+cudaError_t periodic_scatter(int n, int P, const double* g, double* loc, cudaStream_t s) {
+  const int N3 = n * n * n;
+  const int nm = (P + 1) * (P + 1) * (P + 1);
+  const int blocks = (N3 + SC_EB - 1) / SC_EB;
+  if (blocks == 0) return cudaSuccess;
+  periodic_scatter_kernel<<<blocks, 256, sizeof(int) * (SC_EB * 27 + nm), s>>>(n, P, g, loc);
+  return cudaGetLastError();
+}
+
+// (E, 27) entity bases of the periodic map, built once per map
+__global__ void entity_table_kernel(int n, int P, int* ent) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t N3 = (int64_t)n * n * n;
+  if (tid >= N3 * 27) return;
+  const int e = (int)(tid / 27), k = (int)(tid % 27);
+  ent[tid] = entity_base(n, P, e % n, (e / n) % n, e / (n * n), k);
+}
+
+cudaError_t periodic_entity_table(int n, int P, int* ent, cudaStream_t s) {
+  const int64_t total = (int64_t)n * n * n * 27;
+  if (total == 0) return cudaSuccess;
+  entity_table_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(n, P, ent);
   return cudaGetLastError();
 }
 

@@ -35,6 +35,7 @@ struct PointJob {
 cudaError_t geom_analytic(const GeomJob& j, int* bad, cudaStream_t s);
 cudaError_t geom_convert(const GeomJob& j, const double* wj, const double* inv, int* bad,
                          cudaStream_t s);
+cudaError_t periodic_entity_table(int n, int P, int* ent, cudaStream_t s);
 cudaError_t amap_scatter(const AmapDev& m, const double* g, double* loc, cudaStream_t s);
 cudaError_t amap_assemble(const AmapDev& m, const double* loc, double* g, int ncolours,
                           const int* elist_dev, const int64_t* colour_off, int accumulate,

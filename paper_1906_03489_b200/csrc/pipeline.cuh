@@ -19,6 +19,7 @@
 #pragma once
 #include "common.cuh"
 #include "kernels.h"
+#include "periodic.cuh"
 #include "../../include/spechp_b200.h"
 
 namespace sphp {
@@ -41,68 +42,10 @@ struct DevArgs {
   const int* elist;
   int64_t nlist;
   const int* codes;
+  const int* ent_g;  // PERIODIC_GATHER: precomputed (E, 27) entity bases, or null
   int n;
   int colour;
 };
-
-// ---------------------------------------------------------------------------
-// Periodic hex numbering by entity (assembled modes): every local mode maps
-// to one of 27 entities of its element (8 vertices, 12 edges, 6 faces, the
-// interior) plus an offset; the per-mode (entity, offset) table is built
-// once per CTA, the 27 entity bases once per element, so a gather/scatter
-// index costs one shared load and one add.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int mode_code(int M, int nl) {
-  const int b = M - 2;  // bubbles per edge (P - 1)
-  const int p = nl / (M * M), q = (nl / M) % M, r = nl % M;
-  const int idx[3] = {p, q, r};
-  const int nb = (p >= 2) + (q >= 2) + (r >= 2);
-  int cls, off;
-  if (nb == 0) {
-    cls = p * 4 + q * 2 + r;
-    off = 0;
-  } else if (nb == 1) {
-    const int d = (p >= 2) ? 0 : ((q >= 2) ? 1 : 2);
-    int o[2], c = 0;
-    for (int a = 0; a < 3; ++a)
-      if (a != d) o[c++] = idx[a];
-    cls = 8 + d * 4 + o[0] * 2 + o[1];
-    off = idx[d] - 2;
-  } else if (nb == 2) {
-    const int d = (p < 2) ? 0 : ((q < 2) ? 1 : 2);
-    int k[2], c = 0;
-    for (int a = 0; a < 3; ++a)
-      if (a != d) k[c++] = idx[a];
-    cls = 20 + d * 2 + idx[d];
-    off = (k[0] - 2) * b + (k[1] - 2);
-  } else {
-    cls = 26;
-    off = ((p - 2) * b + (q - 2)) * b + (r - 2);
-  }
-  return cls | (off << 5);
-}
-
-__device__ __forceinline__ int entity_base(int n, int P, int ex, int ey, int ez, int k) {
-  const int N3 = n * n * n, b = P - 1;
-  auto wrap = [n](int i) { return i >= n ? i - n : i; };
-  auto vid = [&](int i, int j, int l) { return wrap(i) + n * (wrap(j) + n * wrap(l)); };
-  const int base[3] = {ex, ey, ez};
-  if (k < 8) return vid(ex + (k >> 2), ey + ((k >> 1) & 1), ez + (k & 1));
-  if (k < 20) {
-    const int j = k - 8, d = j >> 2;
-    const int st[2] = {(j >> 1) & 1, j & 1};
-    int c[3], m = 0;
-    for (int a = 0; a < 3; ++a) c[a] = base[a] + (a == d ? 0 : st[m++]);
-    return N3 + (d * N3 + vid(c[0], c[1], c[2])) * b;
-  }
-  if (k < 26) {
-    const int j = k - 20, d = j >> 1, side = j & 1;
-    int c[3] = {ex, ey, ez};
-    c[d] += side;
-    return N3 + 3 * N3 * b + (d * N3 + vid(c[0], c[1], c[2])) * b * b;
-  }
-  return N3 * (1 + 3 * b + 3 * b * b) + (ex + n * (ey + n * ez)) * b * b * b;
-}
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
@@ -243,6 +186,34 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     int* crd = ent + NE * ENT;
     const int64_t w0 = (int64_t)t * NE;
     const int r = (t < ntiles) ? (int)((count - w0) < NE ? (count - w0) : NE) : 0;
+    if (MODE == 3 && a.ent_g != nullptr) {
+      // all elements in order with a precomputed entity table: no index
+      // set-up and no barrier — geometry by TMA (thread 0), x by cp.async
+      if (tid == 0 && GEO > 0 && r > 0) {
+        fence_proxy_async();
+        const uint32_t bytes = (uint32_t)(sizeof(double) * r * GEO);
+        mbar_expect_tx(&bar[s], bytes);
+        if (a.gstride == GEO && a.goff == 0) {
+          bulk_g2s(geo_s, a.geom + w0 * a.gstride, bytes, &bar[s]);
+        } else {
+          for (int e = 0; e < r; ++e)
+            bulk_g2s(geo_s + e * GEO, a.geom + (w0 + e) * a.gstride + a.goff,
+                     (uint32_t)(sizeof(double) * GEO), &bar[s]);
+        }
+      }
+      for (int i = tid; i < NE * IN; i += NT) {
+        const int e = i / IN, nl = i - e * IN;
+        if (e >= r) {
+          in_s[i] = 0.0;
+          continue;
+        }
+        const int c = mtab[nl];
+        const int gid = __ldg(a.ent_g + (w0 + e) * 27 + (c & 31)) + (c >> 5);
+        cp_async8(in_s + i, a.xg + gid);
+      }
+      cp_async_commit();
+      return;
+    }
     if (MT::PERIODIC) {
       // element coordinates once per element (packed 10 bits each, n <= 1024),
       // then the 27 entity bases per element
@@ -361,7 +332,8 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
           if (a.codes[(int64_t)ids[e] * IN + nl] <= -2) in_s[i] = -in_s[i];
         }
       }
-      for (int i = tid; i < NE * (1 + ENT); i += NT) icur[i] = ids[i];
+      if (MT::SCATTER)
+        for (int i = tid; i < NE * (1 + ENT); i += NT) icur[i] = ids[i];
       if (GEO > 0)
         for (int i = r * GEO + tid; i < NE * GEO; i += NT) geo_s[i] = 0.0;
     }

@@ -30,7 +30,7 @@ def oracle_assembled(amap, oe_by_el, coeff_x, lam, G_by_el, wj_by_el):
     return oa.assemble(amap, out)
 
 
-ALGS = ("owner", "colour")
+ALGS = ("owner", "colour", "split")
 
 
 @pytest.mark.parametrize("alg", ALGS)
@@ -190,10 +190,11 @@ def test_colour_vs_owner_large_mesh(sp, P):
     per = sp.AssemblyMap.hex_periodic(n, P)
     x = torch.as_tensor(np.random.default_rng(P).uniform(-1, 1, per.num_global), device="cuda")
     ys = {}
-    for alg in ("owner", "colour", "colour"):
+    for alg in ("owner", "colour", "colour", "split"):
         per.set_algorithm(alg)
         y = sp.GlobalHelmholtz([(coll, per)], per.num_global).apply(x).cpu().numpy()
         if alg in ys:
             assert y.tobytes() == ys[alg].tobytes(), "colour path not reproducible"
         ys[alg] = y
     assert_parity(ys["colour"], ys["owner"], what=f"colour vs owner P{P} n{n}")
+    assert_parity(ys["split"], ys["owner"], what=f"split vs owner P{P} n{n}")

@@ -33,8 +33,8 @@ for P in (2, 4, 6, 8):
     x = torch.as_tensor(np.random.default_rng(1).uniform(-1, 1, per.num_global), device="cuda")
     ys = {}
     res = {}
-    for name, amap, alg in (("periodic-owner", per, "owner"), ("explicit-owner", expl, "owner"),
-                            ("periodic-colour", per, "colour"), ("explicit-colour", expl, "colour")):
+    for name, amap, alg in (("periodic-owner", per, "owner"), ("periodic-split", per, "split"),
+                            ("explicit-owner", expl, "owner"), ("periodic-colour", per, "colour")):
         amap.set_algorithm(alg)
         op = sp.GlobalHelmholtz([(coll, amap)], per.num_global)
         y = torch.empty_like(x)
