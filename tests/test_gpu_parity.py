@@ -136,3 +136,55 @@ def test_zero_input_zero_output(sp):
                              sp.Strategy.CUDA_SUMFAC)
         out = coll.apply(np.zeros((7, coll.input_size)))
         assert np.all(out == 0)
+
+
+@pytest.mark.parametrize("op", OPS)
+def test_unaligned_and_tiny_inputs(sp, op):
+    """Inputs not 16-byte aligned take the synchronous (non-TMA) load path;
+    E = 1 and E = 2 exercise single partial tiles."""
+    shape, P, Q = "hex", 4, 6
+    n = 4
+    for E in (1, 2, 37):
+        ids = np.arange(E)
+        geom = "metric" if op == "helmholtz" else ("point" if op != "bwdtrans" else "none")
+        coll, oe, inv, wj = _build(sp, shape, P, Q, n, ids, op, geom, "cuda_sumfac")
+        isz = input_size(op, oe)
+        x = np.random.default_rng(E).uniform(-1, 1, (E, isz))
+        buf = torch.zeros(E * isz + 1, dtype=torch.float64, device="cuda")
+        view = buf[1:].view(E, isz)          # 8-byte offset: misaligned for TMA
+        view.copy_(torch.as_tensor(x, device="cuda"))
+        assert view.data_ptr() % 16 == 8
+        got = coll.apply(view).cpu().numpy()
+        ref = oracle_apply(op, oe, x, inv, wj, geom)
+        assert_parity(got.reshape(ref.shape), ref, what=f"unaligned {op} E{E}")
+
+
+def test_multi_tile_walk_small_grid(sp):
+    """Cap the persistent grid (SPHP_MAX_GRID is read once per process, so
+    run in a subprocess) and check every operator still matches."""
+    import subprocess
+    import sys
+    code = r"""
+import sys; sys.path.insert(0, 'tests'); sys.path.insert(0, '.')
+import numpy as np, torch
+import paper_1906_03489_b200 as sp
+from helpers import OPS, assert_parity, input_size, oracle_apply, oracle_geometry
+from test_gpu_parity import _build
+for op in OPS:
+    for shape, P in (("hex", 3), ("hex", 6), ("quad", 5)):
+        n = 4 if shape == "hex" else 8
+        E = n ** (3 if shape == "hex" else 2)
+        geom = "metric" if op == "helmholtz" else ("point" if op != "bwdtrans" else "none")
+        coll, oe, inv, wj = _build(sp, shape, P, P + 2, n, np.arange(E), op, geom, "cuda_sumfac")
+        x = np.random.default_rng(P).uniform(-1, 1, (E, input_size(op, oe)))
+        got = coll.apply(torch.as_tensor(x, device="cuda")).cpu().numpy()
+        ref = oracle_apply(op, oe, x, inv, wj, geom)
+        assert_parity(got.reshape(ref.shape), ref, what=f"grid-capped {shape} P{P} {op}")
+print("ok")
+"""
+    import os
+    env = dict(os.environ, SPHP_MAX_GRID="3")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0 and "ok" in res.stdout, res.stdout + res.stderr

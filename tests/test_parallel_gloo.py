@@ -85,3 +85,75 @@ def test_gloo_world2_plumbing():
         lo, hi = res[r]["diff"]
         assert lo != hi
         assert res[r]["sharded_err"] == 0.0
+
+
+def _dist_worker(rank, world, port, q, n, P):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from oracle import assembly as oa
+    from oracle import geometry as og
+    from oracle import ops as oo
+    from paper_1906_03489_b200.distributed import DistributedHelmholtz, SlabPartition
+
+    try:
+        parallel.init("gloo")
+        part = SlabPartition(n, P, rank, world)
+        oe = oo.Expansion("hex", P, P + 2)
+        ids = np.arange(part.e0, part.e1)
+        _, _, inv, wj = og.factors(oe, n, ids, og.MAP_HEX_SINE, 0.03)
+        G = oo.metric_from_inv(wj, inv)
+
+        def local_apply(x, y):  # oracle stand-in for the GPU slab operator
+            xl = x.numpy()
+            loc = xl[part.local_codes]
+            yl = oo.helmholtz(oe, loc, 1.0, G, wj)
+            out = np.zeros(part.num_local)
+            np.add.at(out, part.local_codes.ravel(), yl.ravel())
+            y.copy_(torch.as_tensor(out))
+            return y
+
+        op = DistributedHelmholtz(part, local_apply, torch.device("cpu"))
+        x_global = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, part.num_global_total))
+        y_local = op.apply(op.to_local(x_global))
+        # reference: full (unsharded) oracle assembled apply
+        om = oa.hex_periodic_map(n, P)
+        Eall = n ** 3
+        _, _, inv_a, wj_a = og.factors(oe, n, np.arange(Eall), og.MAP_HEX_SINE, 0.03)
+        G_a = oo.metric_from_inv(wj_a, inv_a)
+        locs = np.stack(oa.scatter(om, x_global.numpy()))
+        ref = oa.assemble(om, list(oo.helmholtz(oe, locs, 1.0, G_a, wj_a)))
+        err = float(np.max(np.abs(y_local.numpy() - ref[part.gids])) / np.max(np.abs(ref)))
+        d = float(op.dot(y_local, y_local))
+        q.put((rank, {"err": err, "dot": d, "dot_ref": float(ref @ ref),
+                      "shared": {int(k): len(v) for k, v in part.shared.items()}}))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:  # pragma: no cover
+        import traceback
+        q.put((rank, {"error": traceback.format_exc()}))
+
+
+@pytest.mark.timeout(240)
+@pytest.mark.parametrize("world,n,P", [(2, 4, 2), (2, 4, 3)])
+def test_sharded_assembled_operator(world, n, P):
+    """z-slab sharding with the one interface exchange per apply (SURVEY
+    §8(e)): the gathered distributed result equals the unsharded assembled
+    operator, interface planes hold n^2 P^2 dofs per neighbour, and the
+    owner-masked dot product equals the global one."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dist_worker, args=(r, world, port, q, n, P)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=200) for _ in range(world))
+    for p in procs:
+        p.join(timeout=30)
+    for r in range(world):
+        assert "error" not in res[r], res[r]["error"] if "error" in res[r] else ""
+        assert res[r]["err"] < 1e-13
+        assert abs(res[r]["dot"] - res[r]["dot_ref"]) <= 1e-10 * res[r]["dot_ref"]
+        # both planes are shared with the single other rank: 2 n^2 P^2 dofs
+        assert list(res[r]["shared"].values()) == [2 * n * n * P * P]
