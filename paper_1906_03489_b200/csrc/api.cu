@@ -115,6 +115,47 @@ const double* fast_table_pool() {
         std::copy(Bd.begin(), Bd.end(), dst + m * q);
         std::copy(D.begin(), D.end(), dst + 2 * m * q);
         std::copy(w.begin(), w.end(), dst + 2 * m * q + q * q);
+        // even-odd tables (eo.cuh): GLL points are symmetric, Modified_A
+        // rows 0/1 mirror each other and bubble k has parity (-1)^k
+        const int H = eo_h(q), HF = eo_hf(q), ME = eo_me(m), MO = eo_mo(m);
+        double* e = dst + 2 * m * q + q * q + q;
+        double* BE = e;
+        double* BO = BE + ME * H;
+        double* BDE = BO + MO * H;
+        double* BDO = BDE + ME * H;
+        double* DE = BDO + MO * H;
+        double* DO = DE + H * HF;
+        double* DTE = DO + H * H;
+        double* DTO = DTE + H * HF;
+        for (int i = 0; i < H; ++i) {
+          BE[0 * H + i] = 0.5 * (B[0 * q + i] + B[1 * q + i]);
+          BO[0 * H + i] = 0.5 * (B[1 * q + i] - B[0 * q + i]);
+          BDE[0 * H + i] = 0.0;
+          BDO[0 * H + i] = 0.5 * (Bd[1 * q + i] - Bd[0 * q + i]);
+          int ie = 1, io = 1;
+          for (int k = 2; k < m; ++k) {
+            if (k % 2 == 0) {
+              BE[ie * H + i] = B[k * q + i];
+              BDE[ie * H + i] = Bd[k * q + i];
+              ++ie;
+            } else {
+              BO[io * H + i] = B[k * q + i];
+              BDO[io * H + i] = Bd[k * q + i];
+              ++io;
+            }
+          }
+          for (int j = 0; j < HF; ++j) {
+            DE[i * HF + j] = 0.5 * (D[i * q + j] - D[i * q + (q - 1 - j)]);
+            DO[i * H + j] = 0.5 * (D[i * q + j] + D[i * q + (q - 1 - j)]);
+            // transposed operator: (D^T)[i][j] = D[j][i]
+            DTE[i * HF + j] = 0.5 * (D[j * q + i] - D[(q - 1 - j) * q + i]);
+            DTO[i * H + j] = 0.5 * (D[j * q + i] + D[(q - 1 - j) * q + i]);
+          }
+          if (q % 2) {  // middle point
+            DO[i * H + HF] = D[i * q + HF];
+            DTO[i * H + HF] = D[HF * q + i];
+          }
+        }
       }
   });
   return pool.data();

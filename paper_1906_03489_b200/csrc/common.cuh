@@ -17,7 +17,17 @@ namespace sphp {
 constexpr int FAST_M_MIN = 2;
 constexpr int FAST_M_MAX = 10;
 
-__host__ __device__ constexpr int tab_size(int M, int Q) { return 2 * M * Q + Q * Q + Q; }
+// even-odd (parity) sizes: H = ceil(Q/2) point pairs incl. the middle,
+// HF = floor(Q/2); ME / MO = modes in the even set {s = c0+c1, bubbles 2,4,..}
+// and the odd set {d = c1-c0, bubbles 3,5,..}
+__host__ __device__ constexpr int eo_h(int Q) { return (Q + 1) / 2; }
+__host__ __device__ constexpr int eo_hf(int Q) { return Q / 2; }
+__host__ __device__ constexpr int eo_me(int M) { return 1 + (M - 1) / 2; }
+__host__ __device__ constexpr int eo_mo(int M) { return M - eo_me(M); }
+__host__ __device__ constexpr int eo_size(int M, int Q) {
+  return 2 * (eo_me(M) + eo_mo(M)) * eo_h(Q) + 2 * eo_h(Q) * eo_hf(Q) + 2 * eo_h(Q) * eo_h(Q);
+}
+__host__ __device__ constexpr int tab_size(int M, int Q) { return 2 * M * Q + Q * Q + Q + eo_size(M, Q); }
 __host__ __device__ constexpr bool fast_key(int M, int Q) {
   return M >= FAST_M_MIN && M <= FAST_M_MAX && (Q == M + 1 || Q == M + 2);
 }
@@ -32,13 +42,24 @@ __host__ __device__ constexpr int tab_off(int M, int Q) {
 }
 constexpr int TAB_TOTAL = tab_off(FAST_M_MAX, FAST_M_MAX + 2) + tab_size(FAST_M_MAX, FAST_M_MAX + 2);
 
-// layout inside one key: B[M][Q], Bd[M][Q], D[Q][Q], w[Q]
+// layout inside one key: B[M][Q], Bd[M][Q], D[Q][Q], w[Q], then the
+// even-odd tables BE[ME][H], BO[MO][H], BDE[ME][H], BDO[MO][H],
+// DE[H][HF], DO[H][H], DTE[H][HF], DTO[H][H]  (see eo.cuh)
 template <int M, int Q>
 struct Tab {
   static constexpr int B = tab_off(M, Q);
   static constexpr int BD = B + M * Q;
   static constexpr int D = BD + M * Q;
   static constexpr int W = D + Q * Q;
+  static constexpr int H = eo_h(Q), HF = eo_hf(Q), ME = eo_me(M), MO = eo_mo(M);
+  static constexpr int BE = W + Q;
+  static constexpr int BO = BE + ME * H;
+  static constexpr int BDE = BO + MO * H;
+  static constexpr int BDO = BDE + ME * H;
+  static constexpr int DE = BDO + MO * H;
+  static constexpr int DO = DE + H * HF;
+  static constexpr int DTE = DO + H * H;
+  static constexpr int DTO = DTE + H * HF;
 };
 
 // host: the full pool (computed once, uploaded to every TU's bank)

@@ -12,6 +12,7 @@
 #include <type_traits>
 
 #include "pipeline.cuh"
+#include "eo.cuh"
 
 namespace sphp {
 
@@ -463,10 +464,193 @@ struct HexHelmJ {
   }
 };
 
+// ===========================================================================
+// Fused Helmholtz, K-row plan with even-odd contractions (HexHelmEO): the
+// same stages, layouts and memory traffic as HexHelmK, every 1D contraction
+// evaluated through eo.cuh (half the DFMAs and table loads).
+// ===========================================================================
+template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
+struct HexHelmEO {
+  static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int NSTP = NSTP_;
+  static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
+  static constexpr int IN = M3, OUT = M3;
+  static constexpr int CS = pt_stride(Q3);
+  static constexpr int GEO = (GK == SPHP_GEOM_METRIC) ? 7 * CS : 10;
+  static constexpr int QK = odd_up(Q);
+  static constexpr int PP1 = pitch_mod16(M * QK, Q);
+  static constexpr int PP2 = pitch_mod16(Q * Q, Q);
+  static constexpr int SE = even_up(cmax(Q3, cmax(M * PP1, M * PP2)));
+  static constexpr int WORK = 3 * SE;
+  using T = Tab<M, Q>;
+  using X = EO<M, Q>;
+
+  template <class R, class W>
+  __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
+                                 double* __restrict__ work, double* __restrict__ out, double lam,
+                                 R release, W pre_out, const double* tab) {
+    double* W0 = work;
+    double* W1 = work + NE * SE;
+    double* W2 = work + 2 * NE * SE;
+    // S1: r -> k
+    SPHP_FOR_ITEMS(NE * M * M, w) {
+      int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
+      double x[M], u[Q];
+      ld_pencil<M, 1>(cin + e * M3 + pq * M, x);
+      X::interp(tab, x, u);
+      st_pencil<Q, 1>(W0 + e * SE + p * PP1 + q * QK, u);
+    }
+    __syncthreads();
+    // S2: q -> j
+    SPHP_FOR_ITEMS(NE * M * Q, w) {
+      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
+      double x[M], u[Q];
+      ld_pencil<M, QK>(W0 + e * SE + p * PP1 + k, x);
+      X::interp(tab, x, u);
+      st_pencil<Q, Q>(W1 + e * SE + p * PP2 + k, u);
+    }
+    __syncthreads();
+    // S3: p -> i, u and d0
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), jk = w - e * (Q * Q);
+      double x[M], u[Q], d[Q];
+      ld_pencil<M, PP2>(W1 + e * SE + jk, x);
+      X::interp_and_deriv(tab, x, u, d);
+      st_pencil<Q, Q * Q>(W0 + e * SE + jk, u);
+      st_pencil<Q, Q * Q>(W2 + e * SE + jk, d);
+    }
+    __syncthreads();
+    // S4: d1 = D along j
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
+      double v[Q], r[Q];
+      ld_pencil<Q, Q>(W0 + e * SE + i * Q * Q + k, v);
+      X::template deriv<false, false>(tab, v, r);
+      st_pencil<Q, Q>(W1 + e * SE + i * Q * Q + k, r);
+    }
+    __syncthreads();
+    // S5: k rows
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), ij = w - e * (Q * Q), i = ij / Q, j = ij - i * Q;
+      const int row = e * SE + ij * Q;
+      double u[Q], d[Q], f0[Q], f1[Q], f2[Q], g[Q], d2[Q];
+      load_row<Q>(W0 + row, u);
+      X::template deriv<false, false>(tab, u, d2);
+      if constexpr (GK == SPHP_GEOM_METRIC) {
+        const double* gr = geo + e * GEO + ij * Q;
+        load_row<Q>(W2 + row, d);
+        load_row<Q>(gr + 0 * CS, g);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) f0[k] = g[k] * d[k];
+        load_row<Q>(gr + 1 * CS, g);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) f1[k] = g[k] * d[k];
+        double h[Q];
+        load_row<Q>(W1 + row, h);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) f0[k] = fma(g[k], h[k], f0[k]);
+        load_row<Q>(gr + 2 * CS, g);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          f2[k] = g[k] * d[k];
+          f0[k] = fma(g[k], d2[k], f0[k]);
+        }
+        load_row<Q>(gr + 3 * CS, g);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) f1[k] = fma(g[k], h[k], f1[k]);
+        load_row<Q>(gr + 4 * CS, g);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          f1[k] = fma(g[k], d2[k], f1[k]);
+          f2[k] = fma(g[k], h[k], f2[k]);
+        }
+        load_row<Q>(gr + 5 * CS, g);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) f2[k] = fma(g[k], d2[k], f2[k]);
+        load_row<Q>(gr + 6 * CS, g);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) u[k] = lam * g[k] * u[k];
+      } else {
+        const double* gg = geo + e * GEO;
+        const double det = gg[0];
+        const double* iv = gg + 1;
+        const double a00 = det * (iv[0] * iv[0] + iv[1] * iv[1] + iv[2] * iv[2]);
+        const double a01 = det * (iv[0] * iv[3] + iv[1] * iv[4] + iv[2] * iv[5]);
+        const double a02 = det * (iv[0] * iv[6] + iv[1] * iv[7] + iv[2] * iv[8]);
+        const double a11 = det * (iv[3] * iv[3] + iv[4] * iv[4] + iv[5] * iv[5]);
+        const double a12 = det * (iv[3] * iv[6] + iv[4] * iv[7] + iv[5] * iv[8]);
+        const double a22 = det * (iv[6] * iv[6] + iv[7] * iv[7] + iv[8] * iv[8]);
+        const double wij = tab[T::W + i] * tab[T::W + j];
+        load_row<Q>(W2 + row, d);
+        double h[Q];
+        load_row<Q>(W1 + row, h);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          const double wq = wij * tab[T::W + k];
+          f0[k] = wq * (a00 * d[k] + a01 * h[k] + a02 * d2[k]);
+          f1[k] = wq * (a01 * d[k] + a11 * h[k] + a12 * d2[k]);
+          f2[k] = wq * (a02 * d[k] + a12 * h[k] + a22 * d2[k]);
+          u[k] = lam * (wq * det) * u[k];
+        }
+      }
+      X::template deriv<true, true>(tab, f2, u);  // t = mass + D2^T f2
+      store_row<Q>(W0 + row, u);
+      store_row<Q>(W2 + row, f0);
+      store_row<Q>(W1 + row, f1);
+    }
+    __syncthreads();
+    release();
+    // S6: t += D1^T f1 along j
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
+      double f[Q], t[Q];
+      ld_pencil<Q, Q>(W1 + e * SE + i * Q * Q + k, f);
+      ld_pencil<Q, Q>(W0 + e * SE + i * Q * Q + k, t);
+      X::template deriv<true, true>(tab, f, t);
+      st_pencil<Q, Q>(W0 + e * SE + i * Q * Q + k, t);
+    }
+    __syncthreads();
+    // S7: i -> p, B t + dB f0
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e = w / (Q * Q), jk = w - e * (Q * Q);
+      double t[Q], f0[Q], c[M];
+      ld_pencil<Q, Q * Q>(W0 + e * SE + jk, t);
+      ld_pencil<Q, Q * Q>(W2 + e * SE + jk, f0);
+      X::project2(tab, t, f0, c);
+      st_pencil<M, PP2>(W1 + e * SE + jk, c);
+    }
+    __syncthreads();
+    // S8: j -> q
+    SPHP_FOR_ITEMS(NE * M * Q, w) {
+      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
+      double v[Q], c[M];
+      ld_pencil<Q, Q>(W1 + e * SE + p * PP2 + k, v);
+      X::project(tab, v, c);
+      st_pencil<M, QK>(W0 + e * SE + p * PP1 + k, c);
+    }
+    pre_out();
+    __syncthreads();
+    // S9: k -> r
+    SPHP_FOR_ITEMS(NE * M * M, w) {
+      int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
+      double v[Q], c[M];
+      ld_pencil<Q, 1>(W0 + e * SE + p * PP1 + q * QK, v);
+      X::project(tab, v, c);
+      st_pencil<M, 1>(out + e * M3 + pq * M, c);
+    }
+  }
+};
+
 // variant selection: k-row pointwise stage unless Q % 4 == 0
+#ifndef SPHP_HELM_K_PLAIN
+template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
+using HexHelm = typename std::conditional<(Q_ % 4 == 0), HexHelmJ<M_, Q_, GK, NE_, NT_, NSTP_>,
+                                          HexHelmEO<M_, Q_, GK, NE_, NT_, NSTP_>>::type;
+#else
 template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
 using HexHelm = typename std::conditional<(Q_ % 4 == 0), HexHelmJ<M_, Q_, GK, NE_, NT_, NSTP_>,
                                           HexHelmK<M_, Q_, GK, NE_, NT_, NSTP_>>::type;
+#endif
 
 // ===========================================================================
 // BwdTrans (K1): u = (B x B x B)^T c   (collections.py:133-150)
