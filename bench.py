@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--P", type=int, default=4)
     ap.add_argument("--n", type=int, default=64)
-    ap.add_argument("--sweep", action="store_true", help="also time P=2..8 (extra JSON key)")
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false",
+                    help="skip the P=2..8 sweep (extra JSON key, on by default)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extras", action="store_true", help="skip the other BASELINE configs")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -189,4 +189,33 @@ __device__ __forceinline__ void st_pencil(double* __restrict__ p, const double* 
   for (int i = 0; i < N; ++i) p[i * S] = x[i];
 }
 
+
+// pencil-level wrappers (drop-in for common.cuh pencil<> with the B / B^T /
+// D / D^T tables): load a strided pencil, parity contraction, store
+template <int M, int Q, int IS, int OS>
+__device__ __forceinline__ void eo_interp(const double* tab, const double* __restrict__ in,
+                                          double* __restrict__ out) {
+  double x[M], u[Q];
+  ld_pencil<M, IS>(in, x);
+  EO<M, Q>::interp(tab, x, u);
+  st_pencil<Q, OS>(out, u);
+}
+template <int M, int Q, int IS, int OS>
+__device__ __forceinline__ void eo_project(const double* tab, const double* __restrict__ in,
+                                           double* __restrict__ out) {
+  double v[Q], c[M];
+  ld_pencil<Q, IS>(in, v);
+  EO<M, Q>::project(tab, v, c);
+  st_pencil<M, OS>(out, c);
+}
+template <int M, int Q, bool TR, bool ACC, int IS, int OS>
+__device__ __forceinline__ void eo_deriv(const double* tab, const double* __restrict__ in,
+                                         double* __restrict__ out) {
+  double v[Q], r[Q];
+  ld_pencil<Q, IS>(in, v);
+  if constexpr (ACC) ld_pencil<Q, OS>(out, r);
+  EO<M, Q>::template deriv<TR, ACC>(tab, v, r);
+  st_pencil<Q, OS>(out, r);
+}
+
 }  // namespace sphp

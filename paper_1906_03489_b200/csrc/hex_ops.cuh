@@ -641,10 +641,159 @@ struct HexHelmEO {
   }
 };
 
+// ===========================================================================
+// Fused Helmholtz, J-pencil plan with even-odd contractions (Q % 4 == 0):
+// HexHelmJ's stages and layouts, 1D contractions through eo.cuh.
+// ===========================================================================
+template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
+struct HexHelmJEO {
+  static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int NSTP = NSTP_;
+  static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
+  static constexpr int IN = M3, OUT = M3;
+  static constexpr int CS = pt_stride(Q3);
+  static constexpr int GEO = (GK == SPHP_GEOM_METRIC) ? 7 * CS : 10;
+  static constexpr int QK = odd_up(Q);
+  static constexpr int SW = odd_up(Q * Q * QK);
+  static constexpr int WORK = 3 * SW;
+  using T = Tab<M, Q>;
+  using X = EO<M, Q>;
+
+  template <class R, class W>
+  __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
+                                 double* __restrict__ work, double* __restrict__ out, double lam,
+                                 R release, W pre_out, const double* tab) {
+    double* W0 = work;
+    double* W1 = work + NE * SW;
+    double* W2 = work + 2 * NE * SW;
+    SPHP_FOR_ITEMS(NE * M * M, w) {  // S1 r -> k
+      int e = w / (M * M), pq = w - e * (M * M);
+      double x[M], u[Q];
+      ld_pencil<M, 1>(cin + e * M3 + pq * M, x);
+      X::interp(tab, x, u);
+      st_pencil<Q, 1>(W0 + e * SW + pq * QK, u);
+    }
+    __syncthreads();
+    SPHP_FOR_ITEMS(NE * M * Q, w) {  // S2 q -> j
+      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
+      double x[M], u[Q];
+      ld_pencil<M, QK>(W0 + e * SW + p * M * QK + k, x);
+      X::interp(tab, x, u);
+      st_pencil<Q, QK>(W1 + e * SW + p * Q * QK + k, u);
+    }
+    __syncthreads();
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {  // S3 p -> i: u, d0
+      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
+      double x[M], u[Q], d[Q];
+      ld_pencil<M, Q * QK>(W1 + e * SW + j * QK + k, x);
+      X::interp_and_deriv(tab, x, u, d);
+      st_pencil<Q, Q * QK>(W0 + e * SW + j * QK + k, u);
+      st_pencil<Q, Q * QK>(W2 + e * SW + j * QK + k, d);
+    }
+    __syncthreads();
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {  // S4 d2 = D along k
+      int e = w / (Q * Q), ij = w - e * (Q * Q);
+      double v[Q], r[Q];
+      ld_pencil<Q, 1>(W0 + e * SW + ij * QK, v);
+      X::template deriv<false, false>(tab, v, r);
+      st_pencil<Q, 1>(W1 + e * SW + ij * QK, r);
+    }
+    __syncthreads();
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {  // S5 pencil along j: pointwise, t = mass + D1^T f1
+      int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
+      const int base = e * SW + i * Q * QK + k;
+      double u[Q], d1v[Q], f1[Q];
+      ld_pencil<Q, QK>(W0 + base, u);
+      X::template deriv<false, false>(tab, u, d1v);
+      const double* g = geo + e * GEO;
+      double a00, a01, a02, a11, a12, a22, adet;
+      if (GK == SPHP_GEOM_AFFINE) {
+        const double det = g[0];
+        const double* iv = g + 1;
+        a00 = det * (iv[0] * iv[0] + iv[1] * iv[1] + iv[2] * iv[2]);
+        a01 = det * (iv[0] * iv[3] + iv[1] * iv[4] + iv[2] * iv[5]);
+        a02 = det * (iv[0] * iv[6] + iv[1] * iv[7] + iv[2] * iv[8]);
+        a11 = det * (iv[3] * iv[3] + iv[4] * iv[4] + iv[5] * iv[5]);
+        a12 = det * (iv[3] * iv[6] + iv[4] * iv[7] + iv[5] * iv[8]);
+        a22 = det * (iv[6] * iv[6] + iv[7] * iv[7] + iv[8] * iv[8]);
+        adet = det;
+      }
+#pragma unroll
+      for (int j = 0; j < Q; ++j) {
+        const double d1 = d1v[j];
+        const double d0 = W2[base + j * QK];
+        const double d2 = W1[base + j * QK];
+        double G00, G01, G02, G11, G12, G22, wj;
+        if (GK == SPHP_GEOM_METRIC) {
+          const int pt = (i * Q + j) * Q + k;
+          G00 = g[0 * CS + pt];
+          G01 = g[1 * CS + pt];
+          G02 = g[2 * CS + pt];
+          G11 = g[3 * CS + pt];
+          G12 = g[4 * CS + pt];
+          G22 = g[5 * CS + pt];
+          wj = g[6 * CS + pt];
+        } else {
+          const double wq = tab[T::W + i] * tab[T::W + j] * tab[T::W + k];
+          G00 = wq * a00;
+          G01 = wq * a01;
+          G02 = wq * a02;
+          G11 = wq * a11;
+          G12 = wq * a12;
+          G22 = wq * a22;
+          wj = wq * adet;
+        }
+        W2[base + j * QK] = G00 * d0 + G01 * d1 + G02 * d2;
+        f1[j] = G01 * d0 + G11 * d1 + G12 * d2;
+        W1[base + j * QK] = G02 * d0 + G12 * d1 + G22 * d2;
+        u[j] = lam * wj * u[j];
+      }
+      X::template deriv<true, true>(tab, f1, u);
+      st_pencil<Q, QK>(W0 + base, u);
+    }
+    __syncthreads();
+    release();
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {  // S6 t += D2^T f2 along k
+      int e = w / (Q * Q), ij = w - e * (Q * Q);
+      double f[Q], t[Q];
+      ld_pencil<Q, 1>(W1 + e * SW + ij * QK, f);
+      ld_pencil<Q, 1>(W0 + e * SW + ij * QK, t);
+      X::template deriv<true, true>(tab, f, t);
+      st_pencil<Q, 1>(W0 + e * SW + ij * QK, t);
+    }
+    __syncthreads();
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {  // S7 i -> p
+      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
+      double t[Q], f0[Q], c[M];
+      ld_pencil<Q, Q * QK>(W0 + e * SW + j * QK + k, t);
+      ld_pencil<Q, Q * QK>(W2 + e * SW + j * QK + k, f0);
+      X::project2(tab, t, f0, c);
+      st_pencil<M, Q * QK>(W1 + e * SW + j * QK + k, c);
+    }
+    __syncthreads();
+    SPHP_FOR_ITEMS(NE * M * Q, w) {  // S8 j -> q
+      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
+      double v[Q], c[M];
+      ld_pencil<Q, QK>(W1 + e * SW + p * Q * QK + k, v);
+      X::project(tab, v, c);
+      st_pencil<M, QK>(W0 + e * SW + p * M * QK + k, c);
+    }
+    pre_out();
+    __syncthreads();
+    SPHP_FOR_ITEMS(NE * M * M, w) {  // S9 k -> r
+      int e = w / (M * M), pq = w - e * (M * M);
+      double v[Q], c[M];
+      ld_pencil<Q, 1>(W0 + e * SW + pq * QK, v);
+      X::project(tab, v, c);
+      st_pencil<M, 1>(out + e * M3 + pq * M, c);
+    }
+  }
+};
+
 // variant selection: k-row pointwise stage unless Q % 4 == 0
 #ifndef SPHP_HELM_K_PLAIN
 template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
-using HexHelm = typename std::conditional<(Q_ % 4 == 0), HexHelmJ<M_, Q_, GK, NE_, NT_, NSTP_>,
+using HexHelm = typename std::conditional<(Q_ % 4 == 0), HexHelmJEO<M_, Q_, GK, NE_, NT_, NSTP_>,
                                           HexHelmEO<M_, Q_, GK, NE_, NT_, NSTP_>>::type;
 #else
 template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
@@ -673,20 +822,20 @@ struct HexBwd {
     double* Bb = work + NE * SA;
     SPHP_FOR_ITEMS(NE * M * M, w) {
       int e = w / (M * M), pq = w - e * (M * M);
-      pencil<M, Q, T::B, 1, Q, 1, 1, false>(tab, cin + e * M3 + pq * M, A + e * SA + pq * QK);
+      eo_interp<M, Q, 1, 1>(tab, cin + e * M3 + pq * M, A + e * SA + pq * QK);
     }
     __syncthreads();
     release();
     SPHP_FOR_ITEMS(NE * M * Q, w) {
       int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
-      pencil<M, Q, T::B, 1, Q, QK, QK, false>(tab, A + e * SA + p * M * QK + k,
+      eo_interp<M, Q, QK, QK>(tab, A + e * SA + p * M * QK + k,
                                               Bb + e * SB + p * Q * QK + k);
     }
     pre_out();
     __syncthreads();
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
-      pencil<M, Q, T::B, 1, Q, Q * QK, Q * Q, false>(tab, Bb + e * SB + j * QK + k,
+      eo_interp<M, Q, Q * QK, Q * Q>(tab, Bb + e * SB + j * QK + k,
                                                      out + e * Q3 + j * Q + k);
     }
   }
@@ -742,14 +891,14 @@ struct HexIprod {
     release();
     SPHP_FOR_ITEMS(NE * M * Q, w) {
       int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
-      pencil<Q, M, T::B, Q, 1, QK, QK, false>(tab, Bb + e * SB + p * Q * QK + k,
+      eo_project<M, Q, QK, QK>(tab, Bb + e * SB + p * Q * QK + k,
                                               A + e * SA + p * M * QK + k);
     }
     pre_out();
     __syncthreads();
     SPHP_FOR_ITEMS(NE * M * M, w) {
       int e = w / (M * M), pq = w - e * (M * M);
-      pencil<Q, M, T::B, Q, 1, 1, 1, false>(tab, A + e * SA + pq * QK, out + e * M3 + pq * M);
+      eo_project<M, Q, 1, 1>(tab, A + e * SA + pq * QK, out + e * M3 + pq * M);
     }
   }
 };
@@ -783,10 +932,10 @@ struct HexPhysDeriv {
       const int v = half ? w - NE * Q * Q : w;
       int e = v / (Q * Q), ab = v - e * (Q * Q), a = ab / Q, b = ab - a * Q;
       if (!half) {  // pencil along i at (j=a, k=b)
-        pencil<Q, Q, T::D, Q, 1, Q * Q, Q * Q * QK / Q, false>(
+        eo_deriv<M, Q, false, false, Q * Q, Q * Q * QK / Q>(
             tab, uin + e * Q3 + a * Q + b, W0 + e * SW + a * QK + b);
       } else {  // pencil along j at (i=a, k=b)
-        pencil<Q, Q, T::D, Q, 1, Q, QK, false>(tab, uin + e * Q3 + a * Q * Q + b,
+        eo_deriv<M, Q, false, false, Q, QK>(tab, uin + e * Q3 + a * Q * Q + b,
                                                W1 + e * SW + a * Q * QK + b);
       }
     }
@@ -899,7 +1048,7 @@ struct HexIPDeriv {
     // t += D1^T g1 along j
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
-      pencil<Q, Q, T::D, 1, Q, QK, QK, true>(tab, W2 + e * SW + i * Q * QK + k,
+      eo_deriv<M, Q, true, true, QK, QK>(tab, W2 + e * SW + i * Q * QK + k,
                                              W0 + e * SW + i * Q * QK + k);
     }
     __syncthreads();
@@ -927,14 +1076,14 @@ struct HexIPDeriv {
     __syncthreads();
     SPHP_FOR_ITEMS(NE * M * Q, w) {
       int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
-      pencil<Q, M, T::B, Q, 1, QK, QK, false>(tab, W2 + e * SW + p * Q * QK + k,
+      eo_project<M, Q, QK, QK>(tab, W2 + e * SW + p * Q * QK + k,
                                               W0 + e * SW + p * M * QK + k);
     }
     pre_out();
     __syncthreads();
     SPHP_FOR_ITEMS(NE * M * M, w) {
       int e = w / (M * M), pq = w - e * (M * M);
-      pencil<Q, M, T::B, Q, 1, 1, 1, false>(tab, W0 + e * SW + pq * QK, out + e * M3 + pq * M);
+      eo_project<M, Q, 1, 1>(tab, W0 + e * SW + pq * QK, out + e * M3 + pq * M);
     }
   }
 };

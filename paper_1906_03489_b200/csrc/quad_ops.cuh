@@ -30,7 +30,7 @@ struct QuadHelm {
     double* W2 = work + 2 * NE * SW;
     SPHP_FOR_ITEMS(NE * M, w) {  // q -> j
       int e = w / M, p = w - e * M;
-      pencil<M, Q, T::B, 1, Q, 1, 1, false>(tab, cin + e * M2 + p * M, W0 + e * SW + p * QK);
+      eo_interp<M, Q, 1, 1>(tab, cin + e * M2 + p * M, W0 + e * SW + p * QK);
     }
     __syncthreads();
     SPHP_FOR_ITEMS(NE * Q, w) {  // p -> i, u and d0
@@ -129,7 +129,7 @@ struct QuadHelm {
     __syncthreads();
     SPHP_FOR_ITEMS(NE * M, w) {  // j -> q
       int e = w / M, p = w - e * M;
-      pencil<Q, M, T::B, Q, 1, 1, 1, false>(tab, W0 + e * SW + p * QK, out + e * M2 + p * M);
+      eo_project<M, Q, 1, 1>(tab, W0 + e * SW + p * QK, out + e * M2 + p * M);
     }
   }
 };
@@ -150,14 +150,14 @@ struct QuadBwd {
                                  R release, W pre_out, const double* tab) {
     SPHP_FOR_ITEMS(NE * M, w) {
       int e = w / M, p = w - e * M;
-      pencil<M, Q, T::B, 1, Q, 1, 1, false>(tab, cin + e * M2 + p * M, work + e * SW + p * QK);
+      eo_interp<M, Q, 1, 1>(tab, cin + e * M2 + p * M, work + e * SW + p * QK);
     }
     pre_out();
     __syncthreads();
     release();
     SPHP_FOR_ITEMS(NE * Q, w) {
       int e = w / Q, j = w - e * Q;
-      pencil<M, Q, T::B, 1, Q, QK, Q, false>(tab, work + e * SW + j, out + e * Q2 + j);
+      eo_interp<M, Q, QK, Q>(tab, work + e * SW + j, out + e * Q2 + j);
     }
   }
 };
@@ -206,7 +206,7 @@ struct QuadIprod {
     release();
     SPHP_FOR_ITEMS(NE * M, w) {
       int e = w / M, p = w - e * M;
-      pencil<Q, M, T::B, Q, 1, 1, 1, false>(tab, work + e * SW + p * QK, out + e * M2 + p * M);
+      eo_project<M, Q, 1, 1>(tab, work + e * SW + p * QK, out + e * M2 + p * M);
     }
   }
 };
@@ -229,7 +229,7 @@ struct QuadPhysDeriv {
                                  R release, W pre_out, const double* tab) {
     SPHP_FOR_ITEMS(NE * Q, w) {  // d0 along i
       int e = w / Q, j = w - e * Q;
-      pencil<Q, Q, T::D, Q, 1, Q, QK, false>(tab, uin + e * Q2 + j, work + e * SW + j);
+      eo_deriv<M, Q, false, false, Q, QK>(tab, uin + e * Q2 + j, work + e * SW + j);
     }
     pre_out();
     __syncthreads();
@@ -358,7 +358,7 @@ struct QuadIPDeriv {
     __syncthreads();
     SPHP_FOR_ITEMS(NE * M, w) {
       int e = w / M, p = w - e * M;
-      pencil<Q, M, T::B, Q, 1, 1, 1, false>(tab, W2 + e * SW + p * QK, out + e * M2 + p * M);
+      eo_project<M, Q, 1, 1>(tab, W2 + e * SW + p * QK, out + e * M2 + p * M);
     }
   }
 };
