@@ -244,7 +244,10 @@ __global__ void assemble_colour_kernel(AmapDev m, const double* __restrict__ loc
 }
 
 cudaError_t amap_scatter(const AmapDev& m, const double* g, double* loc, cudaStream_t s) {
-  if (m.periodic) return periodic_scatter(m.n, m.P, g, loc, s);
+  if (m.periodic) {
+    cudaError_t e = periodic_scatter_v2(m.n, m.P, g, loc, s);
+    return e == cudaErrorNotSupported ? periodic_scatter(m.n, m.P, g, loc, s) : e;
+  }
   const int64_t total = m.E * m.nm;
   if (total == 0) return cudaSuccess;
   scatter_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(m, g, loc);
@@ -600,6 +603,10 @@ __global__ void owner_csr_kernel(int64_t ng, const int64_t* __restrict__ rowp,
 
 cudaError_t owner_assemble_periodic(int n, int P, const double* loc, double* y, int accumulate,
                                     int mode_major, cudaStream_t s) {
+  if (!mode_major) {
+    cudaError_t e = owner_periodic_v3(n, P, loc, y, accumulate, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (n == 0) return cudaSuccess;
   const int64_t blocks = (int64_t)((n + 31) / 32) * n * n;
   owner_periodic_kernel<<<(unsigned)blocks, 256, 0, s>>>(n, P, loc, y, accumulate, mode_major);

@@ -35,6 +35,9 @@ struct PointJob {
 cudaError_t geom_analytic(const GeomJob& j, int* bad, cudaStream_t s);
 cudaError_t geom_convert(const GeomJob& j, const double* wj, const double* inv, int* bad,
                          cudaStream_t s);
+cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int accumulate,
+                              cudaStream_t s);
+cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cudaStream_t s);
 cudaError_t periodic_entity_table(int n, int P, int* ent, cudaStream_t s);
 cudaError_t amap_scatter(const AmapDev& m, const double* g, double* loc, cudaStream_t s);
 cudaError_t amap_assemble(const AmapDev& m, const double* loc, double* g, int ncolours,

@@ -1,0 +1,462 @@
+// Periodic-grid scatter (global -> local block) and owner-computes sum
+// (local block -> global) by entity class, for the split / owner assembly
+// algorithms on the periodic structured hex map (periodic.cuh).
+//
+// A CTA handles L consecutive elements of one x-row at a time (persistent
+// over such segments).  Consecutive elements own consecutive entities, so
+// each of the 27 entity classes (8 vertices, 12 edges, 6 faces, the
+// interior) maps to one contiguous range of the global vector, and both
+// kernels move data class by class through a shared-memory block.  All the
+// per-slot index arithmetic depends only on (P, L): it is precomputed once
+// per CTA into one packed 32-bit word per slot, so the streaming loops cost
+// a table load, a few bit operations, a global load and a shared store per
+// value (the first versions were issue-bound on index math).  Each thread
+// holds U register slots (U * 256 >= L * nm): the loads of segment i+1 are
+// issued before segment i's block is written out / summed, so global reads
+// stay in flight across the phases.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdlib>
+#include <type_traits>
+
+#include "misc.h"
+#include "periodic.cuh"
+
+namespace sphp {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ int class_size(int k, int b) {
+  return k < 8 ? 1 : (k < 20 ? b : (k < 26 ? b * b : b * b * b));
+}
+// does class k's entity sit at x + 1 (the element's high-x side)?
+__device__ __forceinline__ int class_dx(int k) {
+  return k < 8    ? (k >> 2)
+         : k < 20 ? ((((k - 8) >> 2) != 0) ? ((k - 8) >> 1) & 1 : 0)  // edge off the x axis
+         : k < 26 ? ((((k - 20) >> 1) == 0) ? (k - 20) & 1 : 0)       // x-normal face
+                  : 0;
+}
+// class k's entity of element (x, y, z) is gid = R + size * vid(x + dx,
+// y + dy, z + dz) (periodic wrap): the closed form of entity_base
+// (periodic.cuh) that per-segment code evaluates with a few integer ops
+struct ClassGeom {
+  int R, s, d;  // region base, entity size, dx | dy << 1 | dz << 2
+};
+__device__ __forceinline__ ClassGeom class_geom(int k, int n, int P) {
+  const int N3 = n * n * n, b = P - 1;
+  if (k < 8) return {0, 1, ((k >> 2) & 1) | (((k >> 1) & 1) << 1) | ((k & 1) << 2)};
+  if (k < 20) {
+    const int j = k - 8, dir = j >> 2, s0 = (j >> 1) & 1, s1 = j & 1;
+    // the two shifts go to the axes other than dir, in order
+    const int d = dir == 0 ? (s0 << 1) | (s1 << 2) : (dir == 1 ? s0 | (s1 << 2) : s0 | (s1 << 1));
+    return {N3 + dir * N3 * b, b, d};
+  }
+  if (k < 26) {
+    const int j = k - 20, dir = j >> 1, side = j & 1;
+    return {N3 + 3 * N3 * b + dir * N3 * b * b, b * b, side << dir};
+  }
+  return {N3 * (1 + 3 * b + 3 * b * b), b * b * b, 0};
+}
+__device__ __forceinline__ int class_gid(const ClassGeom& g, int n, int x, int y, int z) {
+  x += g.d & 1;
+  y += (g.d >> 1) & 1;
+  z += (g.d >> 2) & 1;
+  x -= x >= n ? n : 0;
+  y -= y >= n ? n : 0;
+  z -= z >= n ? n : 0;
+  return g.R + g.s * (x + n * (y + n * z));
+}
+// owned classes of an element: vertex 0, edges 8/12/16, faces 20/22/24, interior 26
+__device__ __forceinline__ int owned_class(int c) {
+  return c == 0 ? 0 : (c < 4 ? 8 + 4 * (c - 1) : (c < 7 ? 20 + 2 * (c - 4) : 26));
+}
+__device__ __forceinline__ int owned_size(int c, int b) {
+  return c == 0 ? 1 : (c < 4 ? b : (c < 7 ? b * b : b * b * b));
+}
+// log2 of the number of elements contributing to a dof of owned class c
+__device__ __forceinline__ int owned_log(int c) { return c == 0 ? 3 : (c < 4 ? 2 : (c < 7 ? 1 : 0)); }
+
+// L: largest of 32/16/8/4 dividing n with L * nm < 2^13 (packed slot
+// indices) and block + tables within 48 KB (4+ CTAs per SM)
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+int segment_length(int n, int P) {
+  const int nm = (P + 1) * (P + 1) * (P + 1);
+  static const int force = env_int("SPHP_PERIODIC_L", 0);  // tuning override
+  if (force >= 4 && n % force == 0 && force * nm < 8192 && force <= 32) return force;
+  for (int L = 32; L >= 4; L /= 2)
+    if (n % L == 0 && L * nm < 8192 && (size_t)L * nm * 12 + (size_t)L * P * P * P * 4 <= 48 * 1024)
+      return L;
+  return 0;
+}
+
+template <typename K>
+unsigned persistent_grid(K kernel, size_t smem, int64_t work) {
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
+  static const int cap = env_int("SPHP_PERIODIC_CTAS", 0);  // tuning: CTAs per SM
+  if (cap > 0 && cap < occ) occ = cap;
+  const int64_t g = (int64_t)sms * (occ > 0 ? occ : 1);
+  return (unsigned)(work < g ? work : g);
+}
+
+// per-launch schedule counter (zeroed on the launch stream); a ring so that
+// launches in flight on different streams do not share one
+int* schedule_counter(cudaStream_t s) {
+  constexpr int kRing = 64, kMaxDev = 16;
+  static int* ring[kMaxDev] = {};
+  static std::atomic<unsigned> next{0};
+  static const int dynamic = env_int("SPHP_PERIODIC_DYNAMIC", 1);
+  if (!dynamic) return nullptr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= kMaxDev) return nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  if (!ring[dev] && cap != cudaStreamCaptureStatusNone) return nullptr;  // no malloc in capture
+  if (!ring[dev] && cudaMalloc(&ring[dev], sizeof(int) * kRing) != cudaSuccess) {
+    ring[dev] = nullptr;
+    return nullptr;
+  }
+  int* c = ring[dev] + (next.fetch_add(1) % kRing);
+  if (cudaMemsetAsync(c, 0, sizeof(int), s) != cudaSuccess) return nullptr;
+  return c;
+}
+
+template <typename K>
+void allow_smem(K kernel, int& configured) {
+  if (!configured) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    configured = 1;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// scatter: loc[e][mode] = x[entity_base(e, class(mode)) + offset(mode)].
+// Slots ordered (class, element, offset) -> coalesced reads per class range.
+// Word: class (5 bits) | rel (13) << 5 | dest (13) << 18 | wrap << 31 with
+// rel = el * size + offset relative to the segment's class range and dest =
+// el * nm + mode in the element-major block.  (A TMA variant — one bulk copy
+// per class range, permute in shared memory, one bulk store — measured
+// 119 us against 90 us for this one at P = 4, n = 64: 27 small copies per
+// segment keep too little in flight.)
+// ---------------------------------------------------------------------------
+template <int U>
+__global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) periodic_scatter_v2_kernel(int n, int P, int L,
+                                                                          const double* __restrict__ x,
+                                                                          double* __restrict__ loc,
+                                                                          int* __restrict__ ctr) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int cb[28], segbase[2][27], segwrap[2][27];
+  const int m = P + 1, nm = m * m * m, b = P - 1, total = L * nm;
+  double* blk = smem;                                          // L * nm
+  uint32_t* word = reinterpret_cast<uint32_t*>(blk + total);  // L * nm
+  int* inv = reinterpret_cast<int*>(word + total);             // nm: class slot -> local mode
+  const int segs = n / L, nseg = segs * n * n;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int k = 0; k < 27; ++k) {
+      cb[k] = acc;
+      acc += class_size(k, b);
+    }
+    cb[27] = acc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nm; i += kThreads) {
+    const int c = mode_code(m, i);
+    inv[cb[c & 31] + (c >> 5)] = i;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < total; t += kThreads) {
+    int k = 0;
+    while (L * cb[k + 1] <= t) ++k;
+    const int s = class_size(k, b);
+    const int r = t - L * cb[k], el = r / s, o = r - el * s;
+    const uint32_t dest = el * nm + inv[cb[k] + o];
+    const uint32_t wrap = (class_dx(k) && el == L - 1) ? 1u : 0u;
+    word[t] = (uint32_t)k | ((uint32_t)r << 5) | (dest << 18) | (wrap << 31);
+  }
+  // gid(el, o) = segbase + el * size + o, minus n * size when the high-x
+  // entity of the row's last element wraps to x = 0
+  auto bases = [&](int sg, int buf) {
+    if (threadIdx.x < 27 && sg < nseg) {
+      const int seg = sg % segs, row = sg / segs, ex0 = seg * L;
+      const int k = threadIdx.x;
+      const ClassGeom cg = class_geom(k, n, P);
+      segbase[buf][k] = class_gid(cg, n, ex0, row % n, row / n);  // ex0 + dx < n
+      segwrap[buf][k] = (ex0 + L == n) ? n * cg.s : 0;
+    }
+  };
+  double v[U];
+  int d[U];
+  auto issue = [&](int sg, int buf) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = u * kThreads + threadIdx.x;
+      d[u] = -1;
+      v[u] = 0.0;
+      if (sg < nseg && t < total) {
+        const uint32_t w = word[t];
+        const int k = w & 31;
+        int g = segbase[buf][k] + (int)((w >> 5) & 8191);
+        if (w >> 31) g -= segwrap[buf][k];
+        v[u] = __ldg(x + g);
+        d[u] = (w >> 18) & 8191;
+      }
+    }
+  };
+  // segment schedule: dynamic (atomic counter, keeps the CTAs' working set
+  // of neighbouring rows tight in L2) or static round robin when ctr is null;
+  // warp 0 grabs the id and computes the segment's bases
+  __shared__ int ids[2];
+  auto grab = [&](int fallback, int buf) {
+    if (threadIdx.x < 32) {
+      int id = fallback;
+      if (ctr) {
+        if (threadIdx.x == 0) id = atomicAdd(ctr, 1);
+        id = __shfl_sync(0xffffffffu, id, 0);
+      }
+      if (threadIdx.x == 0) ids[buf] = id;
+      bases(id, buf);
+    }
+  };
+  grab(blockIdx.x, 0);
+  __syncthreads();  // tables + first bases
+  int cur = ids[0];
+  issue(cur, 0);
+  int buf = 0;
+  for (int k = 1; cur < nseg; ++k, buf ^= 1) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (d[u] >= 0) blk[d[u]] = v[u];
+    grab(blockIdx.x + k * gridDim.x, buf ^ 1);
+    __syncthreads();  // block complete, next bases visible
+    const int nxt = ids[buf ^ 1];
+    issue(nxt, buf ^ 1);  // next segment's loads overlap the write-out
+    // L * nm is even and the block start is 16-byte aligned (L % 4 == 0)
+    double2* out = reinterpret_cast<double2*>(loc + (size_t)cur * total);
+    const double2* src = reinterpret_cast<const double2*>(blk);
+    for (int i = threadIdx.x; i < total / 2; i += kThreads) out[i] = src[i];
+    __syncthreads();  // block consumed
+    cur = nxt;
+  }
+}
+
+// per-thread register batch: U * kThreads >= L * nm
+template <typename F>
+cudaError_t with_unroll(int slots, F&& f) {
+  if (slots <= 4 * kThreads) return f(std::integral_constant<int, 4>());
+  if (slots <= 8 * kThreads) return f(std::integral_constant<int, 8>());
+  if (slots <= 12 * kThreads) return f(std::integral_constant<int, 12>());
+  if (slots <= 16 * kThreads) return f(std::integral_constant<int, 16>());
+  return cudaErrorNotSupported;
+}
+
+cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cudaStream_t s) {
+  const int L = segment_length(n, P);
+  if (L == 0 || P < 2) return cudaErrorNotSupported;
+  if (reinterpret_cast<uintptr_t>(loc) & 15) return cudaErrorNotSupported;
+  if (n == 0) return cudaSuccess;
+  const int nm = (P + 1) * (P + 1) * (P + 1);
+  const size_t smem = (sizeof(double) + sizeof(uint32_t)) * L * nm + sizeof(int) * nm;
+  return with_unroll(L * nm, [&](auto uc) {
+    constexpr int U = decltype(uc)::value;
+    static int configured = 0;
+    allow_smem(periodic_scatter_v2_kernel<U>, configured);
+    const unsigned blocks =
+        persistent_grid(periodic_scatter_v2_kernel<U>, smem, (int64_t)n * n * (n / L));
+    periodic_scatter_v2_kernel<U><<<blocks, kThreads, smem, s>>>(n, P, L, x, loc, schedule_counter(s));
+    return cudaGetLastError();
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Owner-computes sum.  Element e owns its low vertex, the 3 edges and 3 faces
+// leaving it and its interior (P^3 dofs).  Neighbour e - (a,b,c) contributes
+// to them its modes with index 1 in every direction where the offset is 1
+// and index in {0, 2..P} elsewhere: (P+1)^3 values per owner, each used once.
+// Phase 1 stages them (slots ordered offset, element, index: block-
+// contiguous neighbour reads) into a layout where the terms of every owned
+// dof are contiguous and in lexicographic (a, b, c) order; phase 2 sums each
+// run and writes every owned class range contiguously.
+//   phase-1 word: o8 (3) | el - a + 1 (6) << 3 | mode (10) << 9 | dest (13) << 19
+//   phase-2 word: class (3) | el * size + off (13) << 3 | start (13) << 16 | log2 count (2) << 29
+// ---------------------------------------------------------------------------
+template <int U>
+__global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_kernel(int n, int P, int L,
+                                                                     const double* __restrict__ loc,
+                                                                     double* __restrict__ y,
+                                                                     int accumulate,
+                                                                     int* __restrict__ ctr) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int cstart[9], segout[2][8], srow[2][8];
+  const int m = P + 1, nm = m * m * m, b = P - 1, per = P * P * P;
+  const int total1 = L * nm, total2 = L * per;
+  double* S = smem;                                          // L * nm
+  uint32_t* w1 = reinterpret_cast<uint32_t*>(S + total1);  // L * nm
+  uint32_t* w2 = w1 + total1;                                // L * P^3
+  const int segs = n / L, nseg = segs * n * n;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int c = 0; c < 8; ++c) {
+      cstart[c] = acc;  // start of the class's term runs in an element's block
+      acc += owned_size(c, b) << owned_log(c);
+    }
+    cstart[8] = acc;  // == nm
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < total1; t += kThreads) {
+    // offset o8 = (a, b, c) bits; its index set has P or 1 entries per axis
+    int o8 = 0, first = 0, cnt = 0;
+    for (;; ++o8) {
+      cnt = (o8 & 4 ? 1 : P) * (o8 & 2 ? 1 : P) * (o8 & 1 ? 1 : P);
+      if (t < first + L * cnt) break;
+      first += L * cnt;
+    }
+    const int a = o8 >> 2, bb = (o8 >> 1) & 1, c = o8 & 1;
+    const int sb = bb ? 1 : P, sc = c ? 1 : P;
+    const int r0 = t - first, el = r0 / cnt, idx = r0 - el * cnt;
+    const int ia = idx / (sb * sc), ib = (idx / sc) % sb, ic = idx % sc;
+    // neighbour mode and the owner dof (p, q, r) it contributes to
+    const int np = a ? 1 : (ia ? ia + 1 : 0);
+    const int nq = bb ? 1 : (ib ? ib + 1 : 0);
+    const int nr = c ? 1 : (ic ? ic + 1 : 0);
+    const int p = a ? 0 : np, q = bb ? 0 : nq, r = c ? 0 : nr;
+    // owned class / offset of (p, q, r) in mode_code order
+    const int zmask = (p == 0 ? 4 : 0) | (q == 0 ? 2 : 0) | (r == 0 ? 1 : 0);
+    int cc, off;
+    switch (zmask) {
+      case 7: cc = 0; off = 0; break;
+      case 3: cc = 1; off = p - 2; break;
+      case 5: cc = 2; off = q - 2; break;
+      case 6: cc = 3; off = r - 2; break;
+      case 4: cc = 4; off = (q - 2) * b + (r - 2); break;
+      case 2: cc = 5; off = (p - 2) * b + (r - 2); break;
+      case 1: cc = 6; off = (p - 2) * b + (q - 2); break;
+      default: cc = 7; off = ((p - 2) * b + (q - 2)) * b + (r - 2); break;
+    }
+    // position of o8 in the dof's run: o8's bits on the zero axes, in
+    // order of significance (so runs are in increasing o8 order)
+    int pos = 0, nb = 0;
+    for (int d = 0; d < 3; ++d)
+      if (zmask >> d & 1) pos |= ((o8 >> d) & 1) << nb++;
+    const uint32_t dest = el * nm + cstart[cc] + (off << owned_log(cc)) + pos;
+    const uint32_t mode = (np * m + nq) * m + nr;
+    w1[t] = (uint32_t)o8 | ((uint32_t)(el - a + 1) << 3) | (mode << 9) | (dest << 19);
+  }
+  for (int t = threadIdx.x; t < total2; t += kThreads) {
+    int cc = 0, first = 0;
+    while (t >= first + L * owned_size(cc, b)) first += L * owned_size(cc++, b);
+    const int s = owned_size(cc, b), r0 = t - first, el = r0 / s, off = r0 - el * s;
+    const uint32_t start = el * nm + cstart[cc] + (off << owned_log(cc));
+    w2[t] = (uint32_t)cc | ((uint32_t)r0 << 3) | (start << 16) | ((uint32_t)owned_log(cc) << 29);
+  }
+  // per segment: owned-class output bases and the 4 neighbour rows
+  auto bases = [&](int sg, int buf) {
+    if (threadIdx.x < 8 && sg < nseg) {
+      const int seg = sg % segs, row = sg / segs;
+      const int ey = row % n, ez = row / n, ex0 = seg * L;
+      const int c = threadIdx.x;
+      // owned classes sit at the element itself: gid = base + x * size + off
+      segout[buf][c] = class_gid(class_geom(owned_class(c), n, P), n, ex0, ey, ez);
+      // neighbour row for the (b, c) bits of o8 = c; the -1 pairs with the
+      // +1 stored in the phase-1 word
+      int sy = ey - ((c >> 1) & 1), sz = ez - (c & 1);
+      sy += sy < 0 ? n : 0;
+      sz += sz < 0 ? n : 0;
+      srow[buf][c] = n * (sy + n * sz) + ex0 - 1;
+    }
+  };
+  double v[U];
+  int d[U];
+  auto issue = [&](int sg, int buf) {
+    const int ex0 = (sg % segs) * L;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = u * kThreads + threadIdx.x;
+      d[u] = -1;
+      v[u] = 0.0;
+      if (sg < nseg && t < total1) {
+        const uint32_t w = w1[t];
+        const int elx = (w >> 3) & 63;
+        int e = srow[buf][w & 7] + elx;  // row + ex0 + el - a
+        if (ex0 + elx == 0) e += n;      // x wrap of the row's first element
+        v[u] = __ldg(loc + (size_t)e * nm + ((w >> 9) & 1023));
+        d[u] = w >> 19;
+      }
+    }
+  };
+  // segment schedule: dynamic (atomic counter, keeps the CTAs' working set
+  // of neighbouring rows tight in L2) or static round robin when ctr is null;
+  // warp 0 grabs the id and computes the segment's bases
+  __shared__ int ids[2];
+  auto grab = [&](int fallback, int buf) {
+    if (threadIdx.x < 32) {
+      int id = fallback;
+      if (ctr) {
+        if (threadIdx.x == 0) id = atomicAdd(ctr, 1);
+        id = __shfl_sync(0xffffffffu, id, 0);
+      }
+      if (threadIdx.x == 0) ids[buf] = id;
+      bases(id, buf);
+    }
+  };
+  grab(blockIdx.x, 0);
+  __syncthreads();  // tables + first bases
+  int cur = ids[0];
+  issue(cur, 0);
+  int buf = 0;
+  for (int k = 1; cur < nseg; ++k, buf ^= 1) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (d[u] >= 0) S[d[u]] = v[u];
+    grab(blockIdx.x + k * gridDim.x, buf ^ 1);
+    __syncthreads();  // staged block complete, next bases visible
+    const int nxt = ids[buf ^ 1];
+    issue(nxt, buf ^ 1);  // next segment's loads overlap the sums
+    for (int t = threadIdx.x; t < total2; t += kThreads) {
+      const uint32_t w = w2[t];
+      const double* run = S + ((w >> 16) & 8191);
+      const int cnt = 1 << (w >> 29);
+      double acc = run[0];
+      for (int j = 1; j < cnt; ++j) acc += run[j];
+      const int gid = segout[buf][w & 7] + (int)((w >> 3) & 8191);
+      y[gid] = accumulate ? y[gid] + acc : acc;
+    }
+    __syncthreads();  // staged block consumed
+    cur = nxt;
+  }
+}
+
+cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int accumulate,
+                              cudaStream_t s) {
+  const int L = segment_length(n, P);
+  if (L == 0 || P < 2) return cudaErrorNotSupported;
+  if (n == 0) return cudaSuccess;
+  const int nm = (P + 1) * (P + 1) * (P + 1);
+  const size_t smem =
+      (sizeof(double) + sizeof(uint32_t)) * L * nm + sizeof(uint32_t) * L * P * P * P;
+  return with_unroll(L * nm, [&](auto uc) {
+    constexpr int U = decltype(uc)::value;
+    static int configured = 0;
+    allow_smem(owner_periodic_v3_kernel<U>, configured);
+    const unsigned blocks =
+        persistent_grid(owner_periodic_v3_kernel<U>, smem, (int64_t)n * n * (n / L));
+    owner_periodic_v3_kernel<U><<<blocks, kThreads, smem, s>>>(n, P, L, loc, y, accumulate,
+                                                                 schedule_counter(s));
+    return cudaGetLastError();
+  });
+}
+
+}  // namespace sphp
