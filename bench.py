@@ -4,9 +4,10 @@
 One step = one assembled matrix-free Helmholtz apply y = A^T H A x on the
 64^3 periodic deformed hex mesh (x' = x + 0.03 sin 2πy sin 2πz), P=4, Q=6
 GLL, lambda = 1, per-point geometric factors stored (6 metric terms + |J|):
-fused gather -> BwdTrans -> PhysDeriv -> metric -> IProductWRTDerivBase +
-lambda IProductWRTBase -> local block, then the deterministic owner-computes
-C0 sum.  `value` is local DoF/s (E (P+1)^3 / step time,
+the map's default (split) algorithm — class-range scatter kernel, fused
+BwdTrans -> PhysDeriv -> metric -> IProductWRTDerivBase + lambda
+IProductWRTBase on the local block, then the deterministic owner-computes C0
+sum.  `value` is local DoF/s (E (P+1)^3 / step time,
 SURVEY §8(d)); global DoF/s is reported too.
 
 Arms:
@@ -370,6 +371,7 @@ def run_ours(args, rank, world, local_rank):
                                "periodic deformed, lambda=1", "P": P, "Q": P + 2, "n": n,
                    "elements_per_rank": E, "global_dofs_per_rank": ng,
                    "local_dofs_per_rank": E * m ** 3, "parallelism": f"replicas x{world} (weak)",
+                   "assembly": amap.algorithm,
                    "l2": "inputs larger than L2 (geometry 3.2 GB/apply at P=4)"},
         "global_dof_s": world * ng / (ms * 1e-3),
         "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": 8 * ng,
@@ -385,7 +387,8 @@ def run_ours(args, rank, world, local_rank):
                      "assembled_bytes_per_step": ab},
         "cpu_baseline": cpu,
         "clocks": clk,
-        "gpu_launches": args.steps * 2,  # gather+fused Helmholtz, owner-computes sum
+        # split: scatter, fused local Helmholtz, owner sum; owner: gather-fused + owner sum
+        "gpu_launches": args.steps * (3 if amap.algorithm == "split" else 2),
         "replicas_identical": replicas_identical,
     }
     if sweep is not None:

@@ -160,8 +160,10 @@ int sphp_hexmap_variable(int n, const int* orders, int64_t* num_global,
                          int64_t* offsets, int64_t* codes);
 int sphp_amap_destroy(sphp_amap* a);
 /* assembly algorithm of sphp_assemble / sphp_helmholtz_assembled, both
- * deterministic (bitwise reproducible) and atomic-free:
- *   OWNER  (default) gather -> elemental operator -> local block, then one
+ * deterministic (bitwise reproducible) and atomic-free.  Default: SPLIT for
+ * periodic maps with P >= 2 and n % 4 == 0 (class-range scatter and owner
+ * kernels, the fastest measured), OWNER otherwise.
+ *   OWNER  gather -> elemental operator -> local block, then one
  *          owner-computes pass that sums each global dof in a fixed order;
  *   COLOUR colour classes (parity colours on periodic grids, greedy
  *          colouring of explicit maps) fused gather/scatter-add, one launch
@@ -172,6 +174,7 @@ int sphp_amap_destroy(sphp_amap* a);
 #define SPHP_ASSEMBLY_COLOUR 1
 #define SPHP_ASSEMBLY_SPLIT 2
 int sphp_amap_set_algorithm(sphp_amap* a, int alg);
+int sphp_amap_algorithm(const sphp_amap* a, int* alg);
 int sphp_amap_info(const sphp_amap* a, int64_t* num_elements, int* nmodes,
                    int64_t* num_global, int* num_colours);
 /* materialise the map codes (E*nmodes int64, host) — for bit-exact tests   */

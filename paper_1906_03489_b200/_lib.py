@@ -80,6 +80,7 @@ _SIGS = {
     "sphp_hexmap_variable": (_i, [_i, _p, _i64p, _p, _p]),
     "sphp_amap_destroy": (_i, [_p]),
     "sphp_amap_set_algorithm": (_i, [_p, _i]),
+    "sphp_amap_algorithm": (_i, [_p, _p]),
     "sphp_amap_info": (_i, [_p, _i64p, _ip, _i64p, _ip]),
     "sphp_amap_codes": (_i, [_p, _p]),
     "sphp_scatter": (_i, [_p, _p, _p, _p]),

@@ -62,7 +62,15 @@ class AssemblyMap:
                                            C.byref(nc)))
         self.num_elements, self.nmodes = ne.value, nm.value
         self.num_global, self.num_colours = ng.value, nc.value
-        self.algorithm = "owner"
+
+    @property
+    def algorithm(self):
+        """'owner', 'colour' or 'split' (the library default: split for
+        periodic maps the class-range kernels support, owner otherwise)."""
+        a = C.c_int()
+        _lib.check(_lib.lib.sphp_amap_algorithm(self._h, C.byref(a)), AssemblyError)
+        return {_lib.ASSEMBLY_OWNER: "owner", _lib.ASSEMBLY_COLOUR: "colour",
+                _lib.ASSEMBLY_SPLIT: "split"}[a.value]
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -92,13 +100,12 @@ class AssemblyMap:
         return cls(h)
 
     def set_algorithm(self, alg):
-        """'owner' (default: gather -> local -> owner-computes sum),
-        'split' (scatter kernel -> local operator -> owner sum) or
-        'colour' (fused colour-ordered scatter-add)."""
+        """'owner' (gather -> local -> owner-computes sum), 'split' (scatter
+        kernel -> local operator -> owner sum) or 'colour' (fused
+        colour-ordered scatter-add)."""
         code = {"owner": _lib.ASSEMBLY_OWNER, "colour": _lib.ASSEMBLY_COLOUR,
                 "split": _lib.ASSEMBLY_SPLIT}[alg]
         _lib.check(_lib.lib.sphp_amap_set_algorithm(self._h, code), AssemblyError)
-        self.algorithm = alg
         return self
 
     def codes(self):

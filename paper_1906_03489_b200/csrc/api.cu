@@ -925,6 +925,8 @@ int sphp_amap_create_hex_periodic(int n, int P, sphp_amap** out) {
   a->E = (int64_t)n * n * n;
   a->num_global = ipow((int64_t)n * P, 3);
   a->ncolours = 8;
+  // the class-range scatter / owner kernels (periodic_ops.cu) need n % 4 == 0
+  a->alg = (P >= 2 && n % 4 == 0) ? SPHP_ASSEMBLY_SPLIT : SPHP_ASSEMBLY_OWNER;
   if (a->num_global > 2147483645LL) {
     delete a;
     return fail(SPHP_ERR_UNSUPPORTED, "periodic map with more than 2^31-3 global dofs");
@@ -1023,6 +1025,12 @@ int sphp_amap_set_algorithm(sphp_amap* a, int alg) {
   if (alg != SPHP_ASSEMBLY_OWNER && alg != SPHP_ASSEMBLY_COLOUR && alg != SPHP_ASSEMBLY_SPLIT)
     return fail(SPHP_ERR_BAD_ARG, "unknown assembly algorithm");
   a->alg = alg;
+  return SPHP_OK;
+}
+
+int sphp_amap_algorithm(const sphp_amap* a, int* alg) {
+  if (!a || !alg) return fail(SPHP_ERR_BAD_ARG, "null map / output");
+  *alg = a->alg;
   return SPHP_OK;
 }
 

@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include "common.cuh"
 #include "misc.h"
 #include "periodic.cuh"
 
