@@ -81,20 +81,28 @@ __device__ __forceinline__ int owned_size(int c, int b) {
 // log2 of the number of elements contributing to a dof of owned class c
 __device__ __forceinline__ int owned_log(int c) { return c == 0 ? 3 : (c < 4 ? 2 : (c < 7 ? 1 : 0)); }
 
-// L: largest of 32/16/8/4 dividing n with L * nm < 2^13 (packed slot
-// indices) and block + tables within 48 KB (4+ CTAs per SM)
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v && *v ? atoi(v) : dflt;
 }
 
-int segment_length(int n, int P) {
+// L: largest of 32/16/8/4 dividing n with L * nm < 2^13 (packed slot
+// indices) and block + tables within 48 KB (4+ CTAs per SM).  The owner sum
+// prefers segments of at most ~1800 slots (fewer registers per thread, more
+// resident CTAs): measured P=4 108 us at L=8 vs 113 us at L=16.
+int segment_length(int n, int P, bool owner) {
   const int nm = (P + 1) * (P + 1) * (P + 1);
   static const int force = env_int("SPHP_PERIODIC_L", 0);  // tuning override
   if (force >= 4 && n % force == 0 && force * nm < 8192 && force <= 32) return force;
+  auto fits = [&](int L) {
+    return n % L == 0 && L * nm < 8192 &&
+           (size_t)L * nm * 12 + (size_t)L * P * P * P * 4 <= 48 * 1024;
+  };
+  if (owner)
+    for (int L = 32; L >= 4; L /= 2)
+      if (fits(L) && L * nm <= 1800) return L;
   for (int L = 32; L >= 4; L /= 2)
-    if (n % L == 0 && L * nm < 8192 && (size_t)L * nm * 12 + (size_t)L * P * P * P * 4 <= 48 * 1024)
-      return L;
+    if (fits(L)) return L;
   return 0;
 }
 
@@ -159,11 +167,12 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) periodic_scatter_v2_
                                                                           double* __restrict__ loc,
                                                                           int* __restrict__ ctr) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ int cb[28], segbase[2][27], segwrap[2][27];
+  __shared__ int cb[28];
+  __shared__ int2 cseg[2][27];  // per class: (base, wrap correction)
   const int m = P + 1, nm = m * m * m, b = P - 1, total = L * nm;
-  double* blk = smem;                                          // L * nm
-  uint32_t* word = reinterpret_cast<uint32_t*>(blk + total);  // L * nm
-  int* inv = reinterpret_cast<int*>(word + total);             // nm: class slot -> local mode
+  double* blk = smem;                                              // L * nm + 2 (scratch)
+  uint32_t* word = reinterpret_cast<uint32_t*>(blk + total + 2);  // U * kThreads
+  int* inv = reinterpret_cast<int*>(word + U * kThreads);          // nm: class slot -> local mode
   const int segs = n / L, nseg = segs * n * n;
   if (threadIdx.x == 0) {
     int acc = 0;
@@ -179,7 +188,13 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) periodic_scatter_v2_
     inv[cb[c & 31] + (c >> 5)] = i;
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < total; t += kThreads) {
+  // padded to U * kThreads slots: the tail slots load x[segbase[0]] into
+  // the scratch double after the block, so the streaming loop is branch-free
+  for (int t = threadIdx.x; t < U * kThreads; t += kThreads) {
+    if (t >= total) {
+      word[t] = (uint32_t)total << 18;
+      continue;
+    }
     int k = 0;
     while (L * cb[k + 1] <= t) ++k;
     const int s = class_size(k, b);
@@ -195,38 +210,39 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) periodic_scatter_v2_
       const int seg = sg % segs, row = sg / segs, ex0 = seg * L;
       const int k = threadIdx.x;
       const ClassGeom cg = class_geom(k, n, P);
-      segbase[buf][k] = class_gid(cg, n, ex0, row % n, row / n);  // ex0 + dx < n
-      segwrap[buf][k] = (ex0 + L == n) ? n * cg.s : 0;
+      cseg[buf][k] = make_int2(class_gid(cg, n, ex0, row % n, row / n),  // ex0 + dx < n
+                              (ex0 + L == n) ? n * cg.s : 0);
     }
   };
   double v[U];
   int d[U];
   auto issue = [&](int sg, int buf) {
+    if (sg >= nseg) return;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int t = u * kThreads + threadIdx.x;
-      d[u] = -1;
-      v[u] = 0.0;
-      if (sg < nseg && t < total) {
-        const uint32_t w = word[t];
-        const int k = w & 31;
-        int g = segbase[buf][k] + (int)((w >> 5) & 8191);
-        if (w >> 31) g -= segwrap[buf][k];
-        v[u] = __ldg(x + g);
-        d[u] = (w >> 18) & 8191;
-      }
+      const uint32_t w = word[u * kThreads + threadIdx.x];
+      const int2 sb = cseg[buf][w & 31];
+      const int g = sb.x + (int)((w >> 5) & 8191) - ((w >> 31) ? sb.y : 0);
+      v[u] = __ldg(x + g);
+      d[u] = (w >> 18) & 8191;
     }
   };
   // segment schedule: dynamic (atomic counter, keeps the CTAs' working set
   // of neighbouring rows tight in L2) or static round robin when ctr is null;
   // warp 0 grabs the id and computes the segment's bases
   __shared__ int ids[2];
+  // lane 0 of warp 0 keeps one id in flight: the atomic for the segment
+  // after next is issued when this one is consumed, so its latency never
+  // sits in front of a barrier (ids are increasing per CTA, so every id
+  // still in flight when the loop ends is past nseg)
+  int ahead = 0;
+  if (ctr && threadIdx.x == 0) ahead = atomicAdd(ctr, 1);
   auto grab = [&](int fallback, int buf) {
     if (threadIdx.x < 32) {
       int id = fallback;
       if (ctr) {
-        if (threadIdx.x == 0) id = atomicAdd(ctr, 1);
-        id = __shfl_sync(0xffffffffu, id, 0);
+        id = __shfl_sync(0xffffffffu, ahead, 0);
+        if (threadIdx.x == 0) ahead = atomicAdd(ctr, 1);
       }
       if (threadIdx.x == 0) ids[buf] = id;
       bases(id, buf);
@@ -239,8 +255,7 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) periodic_scatter_v2_
   int buf = 0;
   for (int k = 1; cur < nseg; ++k, buf ^= 1) {
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (d[u] >= 0) blk[d[u]] = v[u];
+    for (int u = 0; u < U; ++u) blk[d[u]] = v[u];
     grab(blockIdx.x + k * gridDim.x, buf ^ 1);
     __syncthreads();  // block complete, next bases visible
     const int nxt = ids[buf ^ 1];
@@ -265,14 +280,14 @@ cudaError_t with_unroll(int slots, F&& f) {
 }
 
 cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cudaStream_t s) {
-  const int L = segment_length(n, P);
+  const int L = segment_length(n, P, false);
   if (L == 0 || P < 2) return cudaErrorNotSupported;
   if (reinterpret_cast<uintptr_t>(loc) & 15) return cudaErrorNotSupported;
   if (n == 0) return cudaSuccess;
   const int nm = (P + 1) * (P + 1) * (P + 1);
-  const size_t smem = (sizeof(double) + sizeof(uint32_t)) * L * nm + sizeof(int) * nm;
   return with_unroll(L * nm, [&](auto uc) {
     constexpr int U = decltype(uc)::value;
+    const size_t smem = sizeof(double) * (L * nm + 2) + sizeof(uint32_t) * U * kThreads + sizeof(int) * nm;
     static int configured = 0;
     allow_smem(periodic_scatter_v2_kernel<U>, configured);
     const unsigned blocks =
@@ -291,7 +306,8 @@ cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cuda
 // contiguous neighbour reads) into a layout where the terms of every owned
 // dof are contiguous and in lexicographic (a, b, c) order; phase 2 sums each
 // run and writes every owned class range contiguously.
-//   phase-1 word: o8 (3) | el - a + 1 (6) << 3 | mode (10) << 9 | dest (13) << 19
+//   phase-1 word: row (2) | (el - a + 1) * nm + mode (15) << 2 | dest (13) << 17
+//                 | x-wrap << 31, row = the (b, c) bits of the offset
 //   phase-2 word: class (3) | el * size + off (13) << 3 | start (13) << 16 | log2 count (2) << 29
 // ---------------------------------------------------------------------------
 template <int U>
@@ -301,12 +317,13 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
                                                                      int accumulate,
                                                                      int* __restrict__ ctr) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ int cstart[9], segout[2][8], srow[2][8];
+  __shared__ int cstart[9], segout[2][8], wrapadd[2];
+  __shared__ long long rowoff[2][4];  // per neighbour row: (row element + ex0 - 1) * nm
   const int m = P + 1, nm = m * m * m, b = P - 1, per = P * P * P;
   const int total1 = L * nm, total2 = L * per;
-  double* S = smem;                                          // L * nm
-  uint32_t* w1 = reinterpret_cast<uint32_t*>(S + total1);  // L * nm
-  uint32_t* w2 = w1 + total1;                                // L * P^3
+  double* S = smem;                                              // L * nm + 2 (scratch)
+  uint32_t* w1 = reinterpret_cast<uint32_t*>(S + total1 + 2);  // U * kThreads
+  uint32_t* w2 = w1 + U * kThreads;                              // L * P^3
   const int segs = n / L, nseg = segs * n * n;
   if (threadIdx.x == 0) {
     int acc = 0;
@@ -317,7 +334,11 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
     cstart[8] = acc;  // == nm
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < total1; t += kThreads) {
+  for (int t = threadIdx.x; t < U * kThreads; t += kThreads) {
+    if (t >= total1) {  // padding: a valid load into the scratch double
+      w1[t] = ((uint32_t)nm << 2) | ((uint32_t)total1 << 17);
+      continue;
+    }
     // offset o8 = (a, b, c) bits; its index set has P or 1 entries per axis
     int o8 = 0, first = 0, cnt = 0;
     for (;; ++o8) {
@@ -354,7 +375,8 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
       if (zmask >> d & 1) pos |= ((o8 >> d) & 1) << nb++;
     const uint32_t dest = el * nm + cstart[cc] + (off << owned_log(cc)) + pos;
     const uint32_t mode = (np * m + nq) * m + nr;
-    w1[t] = (uint32_t)o8 | ((uint32_t)(el - a + 1) << 3) | (mode << 9) | (dest << 19);
+    const uint32_t elx = el - a + 1, wrap = elx == 0 ? 1u : 0u;
+    w1[t] = (uint32_t)(o8 & 3) | ((elx * nm + mode) << 2) | (dest << 17) | (wrap << 31);
   }
   for (int t = threadIdx.x; t < total2; t += kThreads) {
     int cc = 0, first = 0;
@@ -373,41 +395,45 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
       segout[buf][c] = class_gid(class_geom(owned_class(c), n, P), n, ex0, ey, ez);
       // neighbour row for the (b, c) bits of o8 = c; the -1 pairs with the
       // +1 stored in the phase-1 word
-      int sy = ey - ((c >> 1) & 1), sz = ez - (c & 1);
-      sy += sy < 0 ? n : 0;
-      sz += sz < 0 ? n : 0;
-      srow[buf][c] = n * (sy + n * sz) + ex0 - 1;
+      if (c < 4) {
+        int sy = ey - ((c >> 1) & 1), sz = ez - (c & 1);
+        sy += sy < 0 ? n : 0;
+        sz += sz < 0 ? n : 0;
+        rowoff[buf][c] = ((long long)n * (sy + n * sz) + ex0 - 1) * nm;
+      }
+      // element ex0 - 1 of the row's first segment wraps to x = n - 1
+      if (c == 0) wrapadd[buf] = ex0 == 0 ? n * nm : 0;
     }
   };
   double v[U];
   int d[U];
   auto issue = [&](int sg, int buf) {
-    const int ex0 = (sg % segs) * L;
+    if (sg >= nseg) return;
+    const int wa = wrapadd[buf];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int t = u * kThreads + threadIdx.x;
-      d[u] = -1;
-      v[u] = 0.0;
-      if (sg < nseg && t < total1) {
-        const uint32_t w = w1[t];
-        const int elx = (w >> 3) & 63;
-        int e = srow[buf][w & 7] + elx;  // row + ex0 + el - a
-        if (ex0 + elx == 0) e += n;      // x wrap of the row's first element
-        v[u] = __ldg(loc + (size_t)e * nm + ((w >> 9) & 1023));
-        d[u] = w >> 19;
-      }
+      const uint32_t w = w1[u * kThreads + threadIdx.x];
+      const int rel = (int)((w >> 2) & 32767) + ((w >> 31) ? wa : 0);
+      v[u] = __ldg(loc + rowoff[buf][w & 3] + rel);
+      d[u] = (w >> 17) & 8191;
     }
   };
   // segment schedule: dynamic (atomic counter, keeps the CTAs' working set
   // of neighbouring rows tight in L2) or static round robin when ctr is null;
   // warp 0 grabs the id and computes the segment's bases
   __shared__ int ids[2];
+  // lane 0 of warp 0 keeps one id in flight: the atomic for the segment
+  // after next is issued when this one is consumed, so its latency never
+  // sits in front of a barrier (ids are increasing per CTA, so every id
+  // still in flight when the loop ends is past nseg)
+  int ahead = 0;
+  if (ctr && threadIdx.x == 0) ahead = atomicAdd(ctr, 1);
   auto grab = [&](int fallback, int buf) {
     if (threadIdx.x < 32) {
       int id = fallback;
       if (ctr) {
-        if (threadIdx.x == 0) id = atomicAdd(ctr, 1);
-        id = __shfl_sync(0xffffffffu, id, 0);
+        id = __shfl_sync(0xffffffffu, ahead, 0);
+        if (threadIdx.x == 0) ahead = atomicAdd(ctr, 1);
       }
       if (threadIdx.x == 0) ids[buf] = id;
       bases(id, buf);
@@ -420,8 +446,7 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
   int buf = 0;
   for (int k = 1; cur < nseg; ++k, buf ^= 1) {
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (d[u] >= 0) S[d[u]] = v[u];
+    for (int u = 0; u < U; ++u) S[d[u]] = v[u];
     grab(blockIdx.x + k * gridDim.x, buf ^ 1);
     __syncthreads();  // staged block complete, next bases visible
     const int nxt = ids[buf ^ 1];
@@ -442,14 +467,14 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
 
 cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int accumulate,
                               cudaStream_t s) {
-  const int L = segment_length(n, P);
+  const int L = segment_length(n, P, true);
   if (L == 0 || P < 2) return cudaErrorNotSupported;
   if (n == 0) return cudaSuccess;
   const int nm = (P + 1) * (P + 1) * (P + 1);
-  const size_t smem =
-      (sizeof(double) + sizeof(uint32_t)) * L * nm + sizeof(uint32_t) * L * P * P * P;
   return with_unroll(L * nm, [&](auto uc) {
     constexpr int U = decltype(uc)::value;
+    const size_t smem =
+        sizeof(double) * (L * nm + 2) + sizeof(uint32_t) * (U * kThreads + L * P * P * P);
     static int configured = 0;
     allow_smem(owner_periodic_v3_kernel<U>, configured);
     const unsigned blocks =
