@@ -125,6 +125,20 @@ def test_explicit_map_from_reference_roundtrip(tag):
         assert 1 <= am.num_colours <= 8
 
 
+def test_default_assembly_algorithm():
+    """Periodic maps the class-range kernels support default to split,
+    everything else to owner; set_algorithm round-trips through the C ABI."""
+    assert sp.AssemblyMap.hex_periodic(8, 4).algorithm == "split"
+    assert sp.AssemblyMap.hex_periodic(6, 4).algorithm == "owner"   # n % 4 != 0
+    assert sp.AssemblyMap.hex_periodic(8, 1).algorithm == "owner"   # no bubbles
+    am = sp.AssemblyMap.explicit(np.array([[0, 1, 2], [2, 3, 0]]), 4)
+    assert am.algorithm == "owner"
+    for alg in ("colour", "split", "owner"):
+        assert am.set_algorithm(alg).algorithm == alg
+    with pytest.raises(KeyError):
+        am.set_algorithm("atomic")
+
+
 def test_explicit_map_rejects_bad_codes():
     with pytest.raises(sp.AssemblyError, match="outside"):
         sp.AssemblyMap.explicit(np.array([[0, 1, 5]]), 5)
