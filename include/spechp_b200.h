@@ -227,6 +227,60 @@ int sphp_quadmap_structured(int nx, int ny, const int* orders, int dirichlet_mas
                             int64_t* num_global, int64_t* num_dirichlet,
                             int64_t* offsets, int64_t* codes);
 
+/* ---- DG primitives: the batched pieces of the
+ * reference's DGSystem (solvers.py:189-392), AdvectionOperator.rhs
+ * (solvers.py:425-457) and ape_rhs (solvers.py:546-642) that are not
+ * Collections operators.  Device pointers, row-major, FP64; deterministic. */
+/* y[e] = alpha * A[e] (s[e] x[e]) (+ y[e] if accumulate); A (E, m, n),
+ * x (E, n), y (E, m); s per-element scale or NULL.  DGSystem.mass_solve
+ * (solvers.py:353-354) with A = minv.                                       */
+int sphp_batched_matvec(int64_t E, int m, int n, const double* A, const double* x,
+                        const double* s, double alpha, int accumulate, double* y,
+                        sphp_stream stream);
+/* out[t, q] = sum_n ex[t, q, n] phys[idx[t], n]: DGSystem.trace_minus /
+ * trace_plus (solvers.py:366-372)                                           */
+int sphp_trace_extract(int64_t T, int nq, int np, const double* ex, const int64_t* idx,
+                       const double* phys, double* out, sphp_stream stream);
+/* deterministic trace lift (np.add.at of solvers.py:374-389, 571-586): for
+ * every rhs r and element e, over the CSR list rowptr[e]..rowptr[e+1] of
+ * codes c = (t << 2) | (plus << 1) | neg, in list order,
+ *   b[r, e, n] (-)= sum_q L[t, n, q] w[t, q] s[r, t, q],  L = plus ? Lp : Lm;
+ * w may be NULL (weights already in s).  Lm, Lp (T, nm, nq), s (nrhs, T, nq),
+ * b (nrhs, E, nm) updated in place.                                         */
+int sphp_trace_lift(int nrhs, int64_t E, int nm, int nq, int64_t T, const int64_t* rowptr,
+                    const int64_t* codes, const double* Lm, const double* Lp, const double* w,
+                    const double* s, double* b, sphp_stream stream);
+#define SPHP_RIEMANN_UPWIND 0
+#define SPHP_RIEMANN_LAXFRIEDRICHS 1
+#define SPHP_BC_INTERIOR 0   /* q_plus given                              */
+#define SPHP_BC_RIGID_WALL 1 /* ghost = mirrored normal velocity           */
+#define SPHP_BC_FARFIELD 2   /* ghost = 0                                  */
+#define SPHP_BC_DIRICHLET 3  /* ghost p = 2 g - p (APE), u = 2 g - u (adv.) */
+/* APE trace flux (riemann_flux, solvers.py:142-181, ghost states of
+ * _ghost_state, solvers.py:498-517): qm, qp planes (3, npts) = (p, ux, uy),
+ * qp NULL unless SPHP_BC_INTERIOR; gv (npts) for DIRICHLET; nrm (npts, 2);
+ * base planes (4, npts) = (ux, uy, rho, c2); w = warc (npts).  out: 3 planes
+ * (w F_p / c2, w F_ux, w F_uy) of npts values, plane r at out + r *
+ * out_stride (out_stride 0 = npts).                                         */
+int sphp_ape_trace_flux(int64_t npts, int riemann, int bc, const double* qm, const double* qp,
+                        const double* gv, const double* nrm, const double* base, const double* w,
+                        double* out, int64_t out_stride, sphp_stream stream);
+/* APE volume fluxes (solvers.py:563-569), negated: q planes (3, E*np),
+ * base planes (4, E*np); G = -(gx, gy), HX = -(h, 0), HY = -(0, h), each
+ * (E, 2, np) as IProductWRTDerivBase takes it.                              */
+int sphp_ape_volume(int64_t E, int np, const double* q, const double* base, double* G,
+                    double* HX, double* HY, sphp_stream stream);
+/* advection: F = (ax u, ay u) as (E, 2, np) (solvers.py:428-430), and the
+ * upwind trace flux an (an >= 0 ? um : up) with boundary ghosts
+ * (solvers.py:433-455; bc INTERIOR needs up, DIRICHLET gv)                  */
+int sphp_advect_volume(int64_t E, int np, const double* ax, const double* ay, const double* u,
+                       double* F, sphp_stream stream);
+int sphp_advect_trace_flux(int64_t npts, int bc, const double* an, const double* um,
+                           const double* up, const double* gv, double* out, sphp_stream stream);
+/* out = c v (+ src): the pointwise-c2 branch of ape_rhs (solvers.py:621-624) */
+int sphp_scale_points(int64_t n, const double* c, const double* v, const double* src,
+                      double* out, sphp_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

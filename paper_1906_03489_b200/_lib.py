@@ -29,6 +29,8 @@ STRATEGY_CUDA_SUMFAC, STRATEGY_CUDA_STDMAT = 0, 1
 GEOM_NONE, GEOM_AFFINE, GEOM_POINT, GEOM_METRIC = 0, 1, 2, 3
 MAP_AFFINE, MAP_QUAD_SINE, MAP_HEX_SINE = 0, 1, 2
 ASSEMBLY_OWNER, ASSEMBLY_COLOUR, ASSEMBLY_SPLIT = 0, 1, 2
+RIEMANN = {"upwind": 0, "laxfriedrichs": 1}
+BC_INTERIOR, BC_RIGID_WALL, BC_FARFIELD, BC_DIRICHLET = 0, 1, 2, 3
 
 
 class LibraryError(RuntimeError):
@@ -94,6 +96,14 @@ _SIGS = {
     "sphp_cg_update": (_i, [_i64, _d, _p, _p, _p, _p, _p, _p, _p, _p]),
     "sphp_cg_direction": (_i, [_i64, _d, _p, _p, _p]),
     "sphp_quadmap_structured": (_i, [_i, _i, _p, _i, _i64p, _i64p, _p, _p]),
+    "sphp_batched_matvec": (_i, [_i64, _i, _i, _p, _p, _p, _d, _i, _p, _p]),
+    "sphp_trace_extract": (_i, [_i64, _i, _i, _p, _p, _p, _p, _p]),
+    "sphp_trace_lift": (_i, [_i, _i64, _i, _i, _i64, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "sphp_ape_trace_flux": (_i, [_i64, _i, _i, _p, _p, _p, _p, _p, _p, _p, _i64, _p]),
+    "sphp_ape_volume": (_i, [_i64, _i, _p, _p, _p, _p, _p, _p]),
+    "sphp_advect_volume": (_i, [_i64, _i, _p, _p, _p, _p, _p]),
+    "sphp_advect_trace_flux": (_i, [_i64, _i, _p, _p, _p, _p, _p, _p]),
+    "sphp_scale_points": (_i, [_i64, _p, _p, _p, _p, _p]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

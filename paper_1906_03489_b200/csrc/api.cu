@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/spechp_b200.h"
+#include "dg.h"
 #include "common.cuh"
 #include "kernels.h"
 #include "misc.h"
@@ -1305,6 +1306,83 @@ int sphp_quadmap_structured(int nx, int ny, const int* orders, int dmask, int64_
   if (offsets) offsets[E] = off;
   *num_global = gid;
   if (num_dirichlet) *num_dirichlet = nd;
+  return SPHP_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// DG primitives (dg.cu)
+// ---------------------------------------------------------------------------
+int sphp_batched_matvec(int64_t E, int m, int n, const double* A, const double* x, const double* s,
+                        double alpha, int accumulate, double* y, sphp_stream stream) {
+  if (E < 0 || m < 0 || n < 0) return fail(SPHP_ERR_BAD_ARG, "negative size");
+  if (E * m > 0 && (!A || !x || !y)) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  CK(sphp::batched_matvec(E, m, n, A, x, s, alpha, accumulate, y, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int sphp_trace_extract(int64_t T, int nq, int np, const double* ex, const int64_t* idx,
+                       const double* phys, double* out, sphp_stream stream) {
+  if (T < 0 || nq < 0 || np < 0) return fail(SPHP_ERR_BAD_ARG, "negative size");
+  if (T * nq > 0 && (!ex || !idx || !phys || !out)) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  CK(sphp::trace_extract(T, nq, np, ex, idx, phys, out, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int sphp_trace_lift(int nrhs, int64_t E, int nm, int nq, int64_t T, const int64_t* rowptr,
+                    const int64_t* codes, const double* Lm, const double* Lp, const double* w,
+                    const double* s, double* b, sphp_stream stream) {
+  if (nrhs < 0 || E < 0 || nm < 0 || nq < 0 || T < 0) return fail(SPHP_ERR_BAD_ARG, "negative size");
+  if ((int64_t)nrhs * E * nm > 0 && (!rowptr || !codes || !Lm || !s || !b))
+    return fail(SPHP_ERR_BAD_ARG, "null argument");
+  CK(sphp::trace_lift(nrhs, E, nm, nq, T, rowptr, codes, Lm, Lp, w, s, b, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int sphp_ape_trace_flux(int64_t npts, int riemann, int bc, const double* qm, const double* qp,
+                        const double* gv, const double* nrm, const double* base, const double* w,
+                        double* out, int64_t out_stride, sphp_stream stream) {
+  if (riemann != SPHP_RIEMANN_UPWIND && riemann != SPHP_RIEMANN_LAXFRIEDRICHS)
+    return fail(SPHP_ERR_BAD_ARG, "unknown Riemann flux kind");
+  if (bc < SPHP_BC_INTERIOR || bc > SPHP_BC_DIRICHLET) return fail(SPHP_ERR_BAD_ARG, "unknown bc kind");
+  if (npts > 0 && (!qm || !nrm || !base || !w || !out || (bc == SPHP_BC_INTERIOR && !qp) ||
+                   (bc == SPHP_BC_DIRICHLET && !gv)))
+    return fail(SPHP_ERR_BAD_ARG, "null argument");
+  if (out_stride != 0 && out_stride < npts) return fail(SPHP_ERR_BAD_ARG, "out_stride < npts");
+  CK(sphp::ape_trace_flux(npts, riemann, bc, qm, qp, gv, nrm, base, w, out,
+                          out_stride ? out_stride : npts, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int sphp_ape_volume(int64_t E, int np, const double* q, const double* base, double* G, double* HX,
+                    double* HY, sphp_stream stream) {
+  if (E * np > 0 && (!q || !base || !G || !HX || !HY)) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  CK(sphp::ape_volume(E, np, q, base, G, HX, HY, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int sphp_advect_volume(int64_t E, int np, const double* ax, const double* ay, const double* u,
+                       double* F, sphp_stream stream) {
+  if (E * np > 0 && (!ax || !ay || !u || !F)) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  CK(sphp::advect_volume(E, np, ax, ay, u, F, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int sphp_advect_trace_flux(int64_t npts, int bc, const double* an, const double* um,
+                           const double* up, const double* gv, double* out, sphp_stream stream) {
+  if (bc < SPHP_BC_INTERIOR || bc > SPHP_BC_DIRICHLET || bc == SPHP_BC_RIGID_WALL)
+    return fail(SPHP_ERR_BAD_ARG, "bc kind unsupported for advection");
+  if (npts > 0 && (!an || !um || !out || (bc == SPHP_BC_INTERIOR && !up) ||
+                   (bc == SPHP_BC_DIRICHLET && !gv)))
+    return fail(SPHP_ERR_BAD_ARG, "null argument");
+  CK(sphp::advect_trace_flux(npts, bc, an, um, up, gv, out, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int sphp_scale_points(int64_t n, const double* c, const double* v, const double* src, double* out,
+                      sphp_stream stream) {
+  if (n > 0 && (!c || !v || !out)) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  CK(sphp::scale_points(n, c, v, src, out, (cudaStream_t)stream));
   return SPHP_OK;
 }
 
