@@ -189,4 +189,23 @@ class GlobalHelmholtz:
             _lib.check(rc, AssemblyError)
         return out
 
+    def apply_host(self, x, out=None, stream=None):
+        """y = A^T H A x with HOST vectors (numpy or CPU tensor; pinned for
+        full overlap): the C-ABI call sphp_helmholtz_assembled_host, which on
+        periodic split maps pipelines the copies over z-slabs.  Single batch."""
+        if len(self.batches) != 1:
+            raise AssemblyError("apply_host takes one (collection, map) batch")
+        coll, amap = self.batches[0]
+        if torch.is_tensor(x):
+            if x.is_cuda or x.dtype != torch.float64 or not x.is_contiguous():
+                raise AssemblyError("x must be a contiguous float64 host tensor")
+        else:
+            x = np.ascontiguousarray(x, dtype=np.float64)
+        if out is None:
+            out = np.empty(self.num_global) if not torch.is_tensor(x) else torch.empty_like(x)
+        rc = _lib.lib.sphp_helmholtz_assembled_host(coll._handle, amap._h, _lib.ptr(x), _lib.ptr(out),
+                                                    _lib.stream_ptr(stream))
+        _lib.check(rc, AssemblyError)
+        return out
+
     __call__ = apply

@@ -35,9 +35,13 @@ struct PointJob {
 cudaError_t geom_analytic(const GeomJob& j, int* bad, cudaStream_t s);
 cudaError_t geom_convert(const GeomJob& j, const double* wj, const double* inv, int* bad,
                          cudaStream_t s);
+// class-range kernels (periodic_ops.cu) over the x-rows [row0, row1) of
+// rows ey + n ez (row1 < 0: all); cudaErrorNotSupported if the grid or
+// order is outside their range
 cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int accumulate,
-                              cudaStream_t s);
-cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cudaStream_t s);
+                              cudaStream_t s, int row0 = 0, int row1 = -1);
+cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cudaStream_t s,
+                                int row0 = 0, int row1 = -1);
 cudaError_t periodic_entity_table(int n, int P, int* ent, cudaStream_t s);
 cudaError_t amap_scatter(const AmapDev& m, const double* g, double* loc, cudaStream_t s);
 cudaError_t amap_assemble(const AmapDev& m, const double* loc, double* g, int ncolours,

@@ -165,7 +165,8 @@ template <int U>
 __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) periodic_scatter_v2_kernel(int n, int P, int L,
                                                                           const double* __restrict__ x,
                                                                           double* __restrict__ loc,
-                                                                          int* __restrict__ ctr) {
+                                                                          int* __restrict__ ctr, int sg0,
+                                                                          int sg1) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int cb[28];
   __shared__ int2 cseg[2][27];  // per class: (base, wrap correction)
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) periodic_scatter_v2_
   double* blk = smem;                                              // L * nm + 2 (scratch)
   uint32_t* word = reinterpret_cast<uint32_t*>(blk + total + 2);  // U * kThreads
   int* inv = reinterpret_cast<int*>(word + U * kThreads);          // nm: class slot -> local mode
-  const int segs = n / L, nseg = segs * n * n;
+  const int segs = n / L, nseg = sg1;  // segments [sg0, sg1) (x-rows of L elements)
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int k = 0; k < 27; ++k) {
@@ -244,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) periodic_scatter_v2_
         id = __shfl_sync(0xffffffffu, ahead, 0);
         if (threadIdx.x == 0) ahead = atomicAdd(ctr, 1);
       }
+      id += sg0;
       if (threadIdx.x == 0) ids[buf] = id;
       bases(id, buf);
     }
@@ -279,7 +281,8 @@ cudaError_t with_unroll(int slots, F&& f) {
   return cudaErrorNotSupported;
 }
 
-cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cudaStream_t s) {
+cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cudaStream_t s, int row0,
+                                int row1) {
   const int L = segment_length(n, P, false);
   if (L == 0 || P < 2) return cudaErrorNotSupported;
   if (reinterpret_cast<uintptr_t>(loc) & 15) return cudaErrorNotSupported;
@@ -290,9 +293,13 @@ cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cuda
     const size_t smem = sizeof(double) * (L * nm + 2) + sizeof(uint32_t) * U * kThreads + sizeof(int) * nm;
     static int configured = 0;
     allow_smem(periodic_scatter_v2_kernel<U>, configured);
+    if (row1 < 0) row1 = n * n;  // rows ey + n ez
+    const int segs = n / L;
+    if (row1 <= row0) return cudaSuccess;
     const unsigned blocks =
-        persistent_grid(periodic_scatter_v2_kernel<U>, smem, (int64_t)n * n * (n / L));
-    periodic_scatter_v2_kernel<U><<<blocks, kThreads, smem, s>>>(n, P, L, x, loc, schedule_counter(s));
+        persistent_grid(periodic_scatter_v2_kernel<U>, smem, (int64_t)(row1 - row0) * segs);
+    periodic_scatter_v2_kernel<U><<<blocks, kThreads, smem, s>>>(n, P, L, x, loc, schedule_counter(s),
+                                                                 row0 * segs, row1 * segs);
     return cudaGetLastError();
   });
 }
@@ -315,7 +322,8 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
                                                                      const double* __restrict__ loc,
                                                                      double* __restrict__ y,
                                                                      int accumulate,
-                                                                     int* __restrict__ ctr) {
+                                                                     int* __restrict__ ctr, int sg0,
+                                                                     int sg1) {
   extern __shared__ __align__(16) double smem[];
   __shared__ int cstart[9], segout[2][8], wrapadd[2];
   __shared__ long long rowoff[2][4];  // per neighbour row: (row element + ex0 - 1) * nm
@@ -324,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
   double* S = smem;                                              // L * nm + 2 (scratch)
   uint32_t* w1 = reinterpret_cast<uint32_t*>(S + total1 + 2);  // U * kThreads
   uint32_t* w2 = w1 + U * kThreads;                              // L * P^3
-  const int segs = n / L, nseg = segs * n * n;
+  const int segs = n / L, nseg = sg1;  // segments [sg0, sg1) (x-rows of L elements)
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int c = 0; c < 8; ++c) {
@@ -435,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
         id = __shfl_sync(0xffffffffu, ahead, 0);
         if (threadIdx.x == 0) ahead = atomicAdd(ctr, 1);
       }
+      id += sg0;
       if (threadIdx.x == 0) ids[buf] = id;
       bases(id, buf);
     }
@@ -466,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
 }
 
 cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int accumulate,
-                              cudaStream_t s) {
+                              cudaStream_t s, int row0, int row1) {
   const int L = segment_length(n, P, true);
   if (L == 0 || P < 2) return cudaErrorNotSupported;
   if (n == 0) return cudaSuccess;
@@ -477,10 +486,14 @@ cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int ac
         sizeof(double) * (L * nm + 2) + sizeof(uint32_t) * (U * kThreads + L * P * P * P);
     static int configured = 0;
     allow_smem(owner_periodic_v3_kernel<U>, configured);
+    if (row1 < 0) row1 = n * n;
+    const int segs = n / L;
+    if (row1 <= row0) return cudaSuccess;
     const unsigned blocks =
-        persistent_grid(owner_periodic_v3_kernel<U>, smem, (int64_t)n * n * (n / L));
+        persistent_grid(owner_periodic_v3_kernel<U>, smem, (int64_t)(row1 - row0) * segs);
     owner_periodic_v3_kernel<U><<<blocks, kThreads, smem, s>>>(n, P, L, loc, y, accumulate,
-                                                                 schedule_counter(s));
+                                                                 schedule_counter(s), row0 * segs,
+                                                                 row1 * segs);
     return cudaGetLastError();
   });
 }
