@@ -15,6 +15,7 @@
 
 #include "../../include/spechp_b200.h"
 #include "dg.h"
+#include "tri.h"
 #include "common.cuh"
 #include "kernels.h"
 #include "misc.h"
@@ -189,6 +190,13 @@ struct sphp_tables {
   std::mutex mu;
   DevBuf d_z, d_w, d_wstd, d_B, d_Bd;
   std::vector<double> wstd;  // tensor weights, point order
+  // triangles: direction-2 table is Modified_B with nm rows; mode blocks,
+  // collapse factors, and the packed device tables of tri.cu
+  bool tri = false;
+  std::vector<int> tri_p, tri_start;
+  std::vector<double> tri_f, tri_g;
+  DevBuf d_tri, d_tri_i;
+  int tri_ntab = 0;
 };
 
 struct sphp_coll {
@@ -267,6 +275,19 @@ int tables_device(sphp_tables* t) {
 // B[n][i] = prod_a B_a[idx_a(n)][idx_a(i)]   (stdregions.py:189-198)
 std::vector<double> dense_bwd(const sphp_tables* t) {
   std::vector<double> M((size_t)t->nm * t->np);
+  if (t->tri) {  // stdregions.py:199-208, collapsed-vertex mode (0,1) gains A1[1] B2[1]
+    const int Q1 = t->q[0], Q2 = t->q[1];
+    for (int64_t n = 0; n < t->nm; ++n) {
+      const int p = t->tri_p[n];
+      for (int i = 0; i < Q1; ++i)
+        for (int j = 0; j < Q2; ++j) {
+          double v = t->B[0][(size_t)p * Q1 + i] * t->B[1][(size_t)n * Q2 + j];
+          if (n == 1) v += t->B[0][(size_t)1 * Q1 + i] * t->B[1][(size_t)n * Q2 + j];
+          M[(size_t)n * t->np + (size_t)i * Q2 + j] = v;
+        }
+    }
+    return M;
+  }
   for (int64_t n = 0; n < t->nm; ++n)
     for (int64_t i = 0; i < t->np; ++i) {
       int64_t rn = n, ri = i;
@@ -284,6 +305,13 @@ std::vector<double> dense_bwd(const sphp_tables* t) {
 // derivative along direction a acting on flattened point vectors:
 // (D_a)[i][j] (stdregions.py:218-235)
 double dense_deriv(const sphp_tables* t, int a, int64_t i, int64_t j) {
+  if (t->tri) {  // collapsed chain rule (stdregions.py:221-235)
+    const int Q2 = t->q[1], Q1 = t->q[0];
+    const int i1 = (int)(i / Q2), i2 = (int)(i % Q2), j1 = (int)(j / Q2), j2 = (int)(j % Q2);
+    const double k1 = (i2 == j2) ? t->D[0][(size_t)i1 * Q1 + j1] : 0.0;
+    const double k2 = (i1 == j1) ? t->D[1][(size_t)i2 * Q2 + j2] : 0.0;
+    return a == 0 ? t->tri_f[i2] * k1 : t->tri_g[i] * k1 + k2;
+  }
   int64_t ri = i, rj = j;
   double v = 1.0;
   for (int b = t->dim - 1; b >= 0; --b) {
@@ -335,6 +363,25 @@ OpArgs base_args(const sphp_coll* c) {
 }
 
 cudaError_t sumfac_launch(const sphp_coll* c, const OpArgs& a, cudaStream_t s) {
+  if (c->t->tri) {
+    TriJob j;
+    j.op = c->op;
+    j.m1 = c->t->m[0];
+    j.nm = (int)c->t->nm;
+    j.Q1 = c->t->q[0];
+    j.Q2 = c->t->q[1];
+    j.ntab = c->t->tri_ntab;
+    j.tab = c->t->d_tri.as<double>();
+    j.itab = c->t->d_tri_i.as<int>();
+    j.geom_kind = a.geom_kind;
+    j.geom = a.geom;
+    j.gstride = a.gstride;
+    j.cs = c->cs;
+    j.E = a.E;
+    j.in = a.in;
+    j.out = a.out;
+    return tri_apply(j, a.num_sms, s);
+  }
   const bool hex = c->t->shape == SPHP_SHAPE_HEX;
   switch (c->op) {
     case SPHP_OP_BWD_TRANS: return hex ? hex_bwd(a, s) : quad_bwd(a, s);
@@ -465,6 +512,17 @@ int64_t mac_count(const sphp_coll* c) {
   const bool geo = c->geom_kind != SPHP_GEOM_NONE;
   const bool sm = c->strategy == SPHP_STRATEGY_CUDA_STDMAT;
   int64_t staged = (d == 2) ? m * m * Q + m * Q * Q : m * m * m * Q + m * m * Q * Q + m * Q * Q * Q;
+  if (t->tri) {  // collections.py:250-273, triangle staged shapes
+    const int64_t q1 = t->q[0], q2 = t->q[1];
+    staged = (nm + 1) * q2 + m * q1 * q2;
+    int64_t per = 0;
+    switch (c->op) {
+      case SPHP_OP_BWD_TRANS: per = sm ? nm * np : staged; break;
+      case SPHP_OP_IPRODUCT_WRT_BASE: per = np + (sm ? nm * np : staged); break;
+      default: per = (sm ? 2 * np * np : q1 * q1 * q2 + q1 * q2 * q2 + 2 * np) + (geo ? 4 * np : 0); break;
+    }
+    return E * per;
+  }
   const int64_t dense = nm * np;
   int64_t per = 0;
   switch (c->op) {
@@ -506,6 +564,77 @@ int64_t hbm_bytes(const sphp_coll* c) {
 
 }  // namespace
 
+// stdregions.make_tri / StdExpansion(Shape.TRI) (stdregions.py:83-240, 402-408):
+// direction 1 Modified_A, direction 2 Modified_B (basis.py:117-157) with the
+// collapse Jacobian (1 - eta2)/2 folded into the direction-2 weights
+int tables_create_tri(const int* nmodes, const int* npoints, const int* points_type,
+                      const int* basis_type, sphp_tables** out) {
+  if (basis_type[1] != SPHP_BASIS_MODIFIED_B)
+    return fail(SPHP_ERR_BAD_ARG, "triangle direction 2 must use the collapsed-direction basis");
+  if (basis_type[0] != SPHP_BASIS_MODIFIED_A)
+    return fail(SPHP_ERR_BAD_ARG, "triangle direction 1 must be modal");
+  if (nmodes[1] < nmodes[0]) return fail(SPHP_ERR_BAD_ARG, "triangle needs P2 >= P1");
+  auto* t = new sphp_tables();
+  t->shape = SPHP_SHAPE_TRI;
+  t->dim = 2;
+  t->tri = true;
+  try {
+    for (int a = 0; a < 2; ++a) {
+      t->m[a] = nmodes[a];
+      t->q[a] = npoints[a];
+      t->ptype[a] = points_type[a];
+      t->btype[a] = basis_type[a];
+      if (nmodes[a] < 2) throw std::invalid_argument("modified basis needs num_modes >= 2");
+      if (npoints[a] < 1) throw std::invalid_argument("num_points must be a positive integer");
+      make_rule(npoints[a], points_type[a], t->z[a], t->w[a]);
+      diff_matrix(t->z[a], t->D[a]);
+    }
+    basis_table(SPHP_BASIS_MODIFIED_A, nmodes[0], t->z[0], t->B[0], t->Bd[0]);
+    modified_b_table(nmodes[0] - 1, nmodes[1] - 1, t->z[1], t->B[1], t->Bd[1], t->tri_p, t->tri_start);
+  } catch (const std::exception& ex) {
+    delete t;
+    return fail(SPHP_ERR_BAD_ARG, ex.what());
+  }
+  const int Q1 = t->q[0], Q2 = t->q[1];
+  t->nm = (int64_t)t->tri_p.size();
+  t->np = (int64_t)Q1 * Q2;
+  t->fast = false;
+  t->wstd.resize(t->np);
+  t->tri_f.resize(Q2);
+  t->tri_g.resize(t->np);
+  for (int j = 0; j < Q2; ++j) t->tri_f[j] = 2.0 / (1.0 - t->z[1][j]);
+  for (int i = 0; i < Q1; ++i)
+    for (int j = 0; j < Q2; ++j) {
+      t->wstd[(size_t)i * Q2 + j] = t->w[0][i] * (t->w[1][j] * 0.5 * (1.0 - t->z[1][j]));
+      t->tri_g[(size_t)i * Q2 + j] = (1.0 + t->z[0][i]) / (1.0 - t->z[1][j]);
+    }
+  *out = t;
+  return SPHP_OK;
+}
+
+// packed device tables for tri.cu (once per tables object)
+int tri_tables_device(sphp_tables* t) {
+  std::lock_guard<std::mutex> lk(t->mu);
+  if (t->d_tri.p) return SPHP_OK;
+  std::vector<double> tab;
+  auto put = [&](const std::vector<double>& v) { tab.insert(tab.end(), v.begin(), v.end()); };
+  put(t->B[0]);
+  put(t->B[1]);
+  put(t->D[0]);
+  put(t->D[1]);
+  put(t->tri_f);
+  put(t->tri_g);
+  put(t->wstd);
+  std::vector<int> it(t->tri_p);
+  it.insert(it.end(), t->tri_start.begin(), t->tri_start.end());
+  CK(t->d_tri.ensure(sizeof(double) * tab.size()));
+  CK(cudaMemcpy(t->d_tri.p, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));
+  CK(t->d_tri_i.ensure(sizeof(int) * it.size()));
+  CK(cudaMemcpy(t->d_tri_i.p, it.data(), sizeof(int) * it.size(), cudaMemcpyHostToDevice));
+  t->tri_ntab = (int)tab.size();
+  return SPHP_OK;
+}
+
 // ===========================================================================
 extern "C" {
 
@@ -523,8 +652,7 @@ int sphp_tables_create(int shape, const int* nmodes, const int* npoints, const i
     case SPHP_SHAPE_SEG: dim = 1; break;
     case SPHP_SHAPE_QUAD: dim = 2; break;
     case SPHP_SHAPE_HEX: dim = 3; break;
-    case SPHP_SHAPE_TRI:
-      return fail(SPHP_ERR_UNSUPPORTED, "triangle (Modified_B) collections are not built yet");
+    case SPHP_SHAPE_TRI: return tables_create_tri(nmodes, npoints, points_type, basis_type, out);
     default: return fail(SPHP_ERR_BAD_ARG, "unknown shape");
   }
   auto* t = new sphp_tables();
@@ -586,7 +714,8 @@ int sphp_tables_destroy(sphp_tables* t) {
 int sphp_tables_query(const sphp_tables* t, int dir, double* z, double* w, double* B, double* Bd,
                       double* D) {
   if (!t || dir < 0 || dir >= t->dim) return fail(SPHP_ERR_BAD_ARG, "bad direction");
-  const size_t q = t->q[dir], m = t->m[dir];
+  // triangle direction 2: the Modified_B table has one row per mode
+  const size_t q = t->q[dir], m = (t->tri && dir == 1) ? (size_t)t->nm : (size_t)t->m[dir];
   if (z) std::memcpy(z, t->z[dir].data(), sizeof(double) * q);
   if (w) std::memcpy(w, t->w[dir].data(), sizeof(double) * q);
   if (B) std::memcpy(B, t->B[dir].data(), sizeof(double) * m * q);
@@ -706,7 +835,17 @@ int sphp_collection_create(const sphp_tables* tc, int op, int strategy, int64_t 
     return fail(SPHP_ERR_BAD_ARG, "METRIC geometry is specific to the Helmholtz operator");
   }
   if (op == SPHP_OP_BWD_TRANS && geom_kind != SPHP_GEOM_NONE) geom_kind = SPHP_GEOM_NONE;
-  if (strategy == SPHP_STRATEGY_CUDA_SUMFAC && !t->fast)
+  if (t->tri) {
+    if (op != SPHP_OP_BWD_TRANS && op != SPHP_OP_IPRODUCT_WRT_BASE && op != SPHP_OP_PHYS_DERIV &&
+        !(op == SPHP_OP_IPRODUCT_WRT_DERIV_BASE && strategy == SPHP_STRATEGY_CUDA_STDMAT))
+      return fail(SPHP_ERR_UNSUPPORTED,
+                  "triangle collections: BwdTrans, IProductWRTBase, PhysDeriv (sumfac or stdmat), "
+                  "IProductWRTDerivBase (stdmat)");
+    if (strategy == SPHP_STRATEGY_CUDA_SUMFAC) {
+      int rc = tri_tables_device(t);
+      if (rc) return rc;
+    }
+  } else if (strategy == SPHP_STRATEGY_CUDA_SUMFAC && !t->fast)
     return fail(SPHP_ERR_UNSUPPORTED,
                 "sumfac kernels cover Modified_A/GLL with Q = P+2 or P+3 (hex P <= 8, quad P <= 9); "
                 "use the stdmat strategy for this key");

@@ -244,4 +244,55 @@ void basis_table(int btype, int m, const std::vector<double>& z, std::vector<dou
   }
 }
 
+
+// Modified_B (basis.py:117-157): rows in storage order, block p = 0..Pa,
+// q = 0..Pb-p within a block (block 0 = the Modified_A table of order Pb).
+// pidx[n] = p of row n; bstart[p] = first row of block p (Pa + 2 entries).
+void modified_b_table(int Pa, int Pb, const std::vector<double>& z, std::vector<double>& B,
+                      std::vector<double>& Bd, std::vector<int>& pidx, std::vector<int>& bstart) {
+  if (Pa < 1 || Pb < 1) throw std::invalid_argument("orders must be >= 1");
+  if (Pb < Pa) throw std::invalid_argument("second-direction order must be >= first (P_b >= P_a)");
+  const int q = (int)z.size();
+  std::vector<double> seg, dseg;
+  basis_table(0, Pb + 1, z, seg, dseg);
+  B.clear();
+  Bd.clear();
+  pidx.clear();
+  bstart.clear();
+  for (int p = 0; p <= Pa; ++p) {
+    bstart.push_back((int)pidx.size());
+    if (p == 0) {
+      for (int r = 0; r <= Pb; ++r) {
+        B.insert(B.end(), seg.begin() + (size_t)r * q, seg.begin() + (size_t)(r + 1) * q);
+        Bd.insert(Bd.end(), dseg.begin() + (size_t)r * q, dseg.begin() + (size_t)(r + 1) * q);
+        pidx.push_back(0);
+      }
+      continue;
+    }
+    std::vector<double> lop(q), dlop(q), hi(q);
+    for (int i = 0; i < q; ++i) {
+      const double lo = 0.5 * (1.0 - z[i]);
+      double pw = 1.0, pw1 = 1.0;
+      for (int k = 0; k < p; ++k) pw *= lo;
+      for (int k = 0; k < p - 1; ++k) pw1 *= lo;
+      lop[i] = pw;
+      dlop[i] = -0.5 * p * pw1;
+      hi[i] = 0.5 * (1.0 + z[i]);
+    }
+    B.insert(B.end(), lop.begin(), lop.end());
+    Bd.insert(Bd.end(), dlop.begin(), dlop.end());
+    pidx.push_back(p);
+    for (int r = 1; r <= Pb - p; ++r) {
+      for (int i = 0; i < q; ++i) {
+        const double j = (double)jacobi(r - 1, 2 * p - 1, 1, (ld)z[i]);
+        const double dj = (double)jacobi_deriv(r - 1, 2 * p - 1, 1, (ld)z[i]);
+        B.push_back(lop[i] * hi[i] * j);
+        Bd.push_back((dlop[i] * hi[i] + 0.5 * lop[i]) * j + lop[i] * hi[i] * dj);
+      }
+      pidx.push_back(p);
+    }
+  }
+  bstart.push_back((int)pidx.size());
+}
+
 }  // namespace sphp
