@@ -46,7 +46,7 @@ extern "C" {
 /* stdregions.py:41-44 Shape (+ HEX, the 3D generalisation)               */
 #define SPHP_SHAPE_SEG 0
 #define SPHP_SHAPE_QUAD 1
-#define SPHP_SHAPE_TRI 2 /* declared for parity; kernels: UNSUPPORTED */
+#define SPHP_SHAPE_TRI 2 /* Modified_A x Modified_B, collapsed (tri.cu) */
 #define SPHP_SHAPE_HEX 3
 /* quadrature.py:19-25 PointsType                                          */
 #define SPHP_POINTS_GAUSS_LEGENDRE 0
@@ -98,7 +98,10 @@ int sphp_tables_create(int shape, const int* nmodes, const int* npoints,
                        sphp_tables** out);
 int sphp_tables_destroy(sphp_tables* t);
 /* copy direction `dir`'s tables to host: z,w (Q); B,Bd (m*Q, B[p*Q+i]);
- * D (Q*Q, D[i*Q+j]).  Any pointer may be NULL.                              */
+ * D (Q*Q, D[i*Q+j]).  Any pointer may be NULL.  Triangles: direction 1 is
+ * the Modified_B table with one row per triangle mode (nmodes rows).
+ * Triangle collections: BwdTrans / IProductWRTBase / PhysDeriv (sumfac and
+ * stdmat), IProductWRTDerivBase (stdmat); geometry NONE, AFFINE or POINT.   */
 int sphp_tables_query(const sphp_tables* t, int dir, double* z, double* w,
                       double* B, double* Bd, double* D);
 /* sizes: num_modes, num_points, dim                                        */

@@ -19,7 +19,7 @@ from .geometry import (GEOM_AFFINE, GEOM_METRIC, GEOM_NONE, GEOM_POINT, MAP_AFFI
 from .quadrature import PointsKey, PointsType, QuadratureError, diff_matrix, make_rule
 from .solvers import (ConvergenceError, HelmholtzSolver, assembled_diagonal,
                       quad_structured_maps, solve_pcg)
-from .stdregions import (ExpansionError, Shape, StdExpansion, make_expansion, make_hex,
+from .stdregions import (ExpansionError, Shape, StdExpansion, make_expansion, make_hex, make_tri,
                          make_quad, make_seg)
 
 __version__ = "0.1.0"

@@ -71,6 +71,10 @@ class NativeTables:
         _lib.check(rc, ExpansionError)
         self.dim = n
         self.modes, self.pts = modes, pts
+        self.tri = shape_code == _lib.SHAPE_TRI
+        nm = C.c_int64()
+        _lib.check(_lib.lib.sphp_tables_sizes(self.handle, C.byref(nm), None, None))
+        self.num_modes = nm.value
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -80,6 +84,8 @@ class NativeTables:
 
     def direction(self, d):
         q, m = self.pts[d], self.modes[d]
+        if self.tri and d == 1:  # Modified_B: one row per triangle mode
+            m = self.num_modes
         z, w = np.empty(q), np.empty(q)
         B, Bd, D = np.empty((m, q)), np.empty((m, q)), np.empty((q, q))
         _lib.check(_lib.lib.sphp_tables_query(self.handle, d, _lib.ptr(z), _lib.ptr(w),
@@ -108,11 +114,17 @@ class StdExpansion:
         if len(basis_keys) != expected:
             raise ExpansionError(
                 f"{shape.value} needs {expected} basis keys, got {len(basis_keys)}")
-        if shape is Shape.TRI:
-            raise ExpansionError("triangle expansions are not built by spechp_b200 yet")
-        for key in basis_keys:
-            if key.basis_type is BasisType.MODIFIED_B:
-                raise ExpansionError("collapsed-direction basis is only valid on triangles")
+        if shape is Shape.TRI:  # stdregions.py:83-91
+            if basis_keys[1].basis_type is not BasisType.MODIFIED_B:
+                raise ExpansionError("triangle direction 2 must use the collapsed-direction basis")
+            if basis_keys[0].basis_type is not BasisType.MODIFIED_A:
+                raise ExpansionError("triangle direction 1 must be modal")
+            if basis_keys[1].num_modes < basis_keys[0].num_modes:
+                raise ExpansionError("triangle needs P2 >= P1")
+        else:
+            for key in basis_keys:
+                if key.basis_type is BasisType.MODIFIED_B:
+                    raise ExpansionError("collapsed-direction basis is only valid on triangles")
         self.shape = shape
         self.basis_keys = basis_keys
 
@@ -138,6 +150,8 @@ class StdExpansion:
 
     @cached_property
     def num_modes(self):
+        if self.shape is Shape.TRI:
+            return self.native.num_modes
         return int(np.prod([k.num_modes for k in self.basis_keys]))
 
     @cached_property
@@ -148,6 +162,9 @@ class StdExpansion:
     @cached_property
     def weights(self):
         ws = [self.native.direction(d)[1] for d in range(self.dim)]
+        if self.shape is Shape.TRI:  # collapse Jacobian in direction 2 (stdregions.py:113-121)
+            z2 = self.native.direction(1)[0]
+            ws[1] = ws[1] * 0.5 * (1.0 - z2)
         out = ws[0]
         for w in ws[1:]:
             out = np.multiply.outer(out, w)
@@ -157,16 +174,39 @@ class StdExpansion:
     def points(self):
         zs = [self.native.direction(d)[0] for d in range(self.dim)]
         grids = np.meshgrid(*zs, indexing="ij")
-        return np.stack([g.ravel() for g in grids], axis=1)
+        pts = np.stack([g.ravel() for g in grids], axis=1)
+        if self.shape is Shape.TRI:  # duffy_collapse (basis.py:187-195)
+            xi = pts.copy()
+            xi[:, 0] = 0.5 * (1.0 + pts[:, 0]) * (1.0 - pts[:, 1]) - 1.0
+            return xi
+        return pts
 
     @cached_property
     def mode_index(self):
+        if self.shape is Shape.TRI:  # blocks p, q = 0..P2-p (basis.py:117-157)
+            P1, P2 = self.basis_keys[0].num_modes - 1, self.basis_keys[1].num_modes - 1
+            return tuple((p, q) for p in range(P1 + 1) for q in range(P2 + 1 - p if p else P2 + 1))
         ms = [k.num_modes for k in self.basis_keys]
         return tuple(np.unravel_index(n, ms) for n in range(self.num_modes))
 
     @cached_property
+    def _collapse_factors(self):
+        """Chain-rule factors f = 2/(1-eta2), g = (1+eta1)/(1-eta2) (stdregions.py:210-217)."""
+        eta1, eta2 = self.native.direction(0)[0], self.native.direction(1)[0]
+        return 2.0 / (1.0 - eta2)[None, :], (1.0 + eta1)[:, None] / (1.0 - eta2)[None, :]
+
+    @cached_property
     def bwd_matrix(self):
-        """Dense B[n, i] = phi_n(xi_i) (stdregions.py:189-198)."""
+        """Dense B[n, i] = phi_n(xi_i) (stdregions.py:189-208)."""
+        if self.shape is Shape.TRI:
+            a1, b2 = self.tables[0][0], self.tables[1][0]
+            rows = []
+            for n, (p, q) in enumerate(self.mode_index):
+                m = np.outer(a1[p], b2[n])
+                if (p, q) == (0, 1):
+                    m = m + np.outer(a1[1], b2[n])
+                rows.append(m.ravel())
+            return np.array(rows)
         out = self.tables[0][0]
         for d in range(1, self.dim):
             out = np.einsum("ni,pj->npij", out, self.tables[d][0]).reshape(
@@ -183,6 +223,11 @@ class StdExpansion:
             for d in range(self.dim):
                 k = np.kron(k, Ds[d] if d == a else np.eye(len(Ds[d])))
             out.append(k)
+        if self.shape is Shape.TRI:  # collapsed chain rule (stdregions.py:221-235)
+            f, g = self._collapse_factors
+            q1, q2 = self.num_points_dir
+            fr = np.broadcast_to(f, (q1, q2)).ravel()
+            return (fr[:, None] * out[0], g.ravel()[:, None] * out[0] + out[1])
         return tuple(out)
 
     @cached_property
@@ -207,6 +252,15 @@ def make_quad(P, num_points=None, basis=BasisType.MODIFIED_A, P2=None):
     return StdExpansion(Shape.QUAD, (BasisKey(basis, m1, pk1), BasisKey(basis, m2, pk2)))
 
 
+def make_tri(P, num_points=None, P2=None):
+    """stdregions.py:402-408: Modified_A on GLL x Modified_B on Gauss-Radau."""
+    m1, m2 = P + 1, (P2 if P2 is not None else P) + 1
+    pk1 = PointsKey(num_points or m1 + 1, PointsType.GAUSS_LOBATTO_LEGENDRE)
+    pk2 = PointsKey(num_points or m2 + 1, PointsType.GAUSS_RADAU_M_LEGENDRE)
+    return StdExpansion(Shape.TRI, (BasisKey(BasisType.MODIFIED_A, m1, pk1),
+                                    BasisKey(BasisType.MODIFIED_B, m2, pk2)))
+
+
 def make_hex(P, num_points=None, basis=BasisType.MODIFIED_A):
     """The hexahedral generalisation: three identical Modified_A keys."""
     pk = _gll(num_points or P + 2)
@@ -220,4 +274,6 @@ def make_expansion(shape, P, num_points=None, basis=BasisType.MODIFIED_A):
         return make_quad(P, num_points, basis)
     if shape is Shape.HEX:
         return make_hex(P, num_points, basis)
+    if shape is Shape.TRI:
+        return make_tri(P, num_points)
     raise ExpansionError(f"unsupported shape {shape}")
