@@ -124,6 +124,14 @@ int sphp_geom_from_factors(const sphp_tables* t, int geom_kind, int64_t E,
                            const double* wj, const double* inv, double* geom,
                            sphp_stream stream);
 
+/* geometry.geom_factors (geometry.py:125-142) on the device for 2D
+ * elements: dx, dy (E, 2, np) = reference-direction derivatives (d/dxi1,
+ * d/dxi2) of the x and y coordinate maps at the expansion's points (e.g.
+ * PhysDeriv of the interpolated map); writes POINT or METRIC records.
+ * Non-positive Jacobians fail naming the first element (*first_bad).      */
+int sphp_geom_from_jacobian(const sphp_tables* t, int kind, int64_t E, const double* dx,
+                            const double* dy, double* geom, int64_t* first_bad,
+                            sphp_stream stream);
 /* ---- collections: replaces collections.Collection (collections.py:76-246)
  * geom: device pointer in `geom_kind` layout, borrowed (must outlive the
  * handle); NULL with SPHP_GEOM_NONE.  lambda only used by HELMHOLTZ.        */

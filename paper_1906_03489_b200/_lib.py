@@ -96,6 +96,7 @@ _SIGS = {
     "sphp_cg_update": (_i, [_i64, _d, _p, _p, _p, _p, _p, _p, _p, _p]),
     "sphp_cg_direction": (_i, [_i64, _d, _p, _p, _p]),
     "sphp_quadmap_structured": (_i, [_i, _i, _p, _i, _i64p, _i64p, _p, _p]),
+    "sphp_geom_from_jacobian": (_i, [_p, _i, _i64, _p, _p, _p, _i64p, _p]),
     "sphp_batched_matvec": (_i, [_i64, _i, _i, _p, _p, _p, _d, _i, _p, _p]),
     "sphp_trace_extract": (_i, [_i64, _i, _i, _p, _p, _p, _p, _p]),
     "sphp_trace_lift": (_i, [_i, _i64, _i, _i, _i64, _p, _p, _p, _p, _p, _p, _p, _p]),

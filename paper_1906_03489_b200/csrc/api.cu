@@ -815,6 +815,52 @@ int sphp_geom_from_factors(const sphp_tables* tc, int kind, int64_t E, const dou
   return SPHP_OK;
 }
 
+// geometry.geom_factors (geometry.py:125-142) on the device, from the
+// reference-direction derivatives of the coordinate map at the points
+int sphp_geom_from_jacobian(const sphp_tables* tc, int kind, int64_t E, const double* dx,
+                            const double* dy, double* geom, int64_t* first_bad, sphp_stream stream) {
+  sphp_tables* t = const_cast<sphp_tables*>(tc);
+  if (!t || !dx || !dy || !geom) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  if (t->dim != 2) return fail(SPHP_ERR_UNSUPPORTED, "coordinate-map geometry is 2D (quad, tri)");
+  if (kind != SPHP_GEOM_POINT && kind != SPHP_GEOM_METRIC)
+    return fail(SPHP_ERR_BAD_ARG, "geometry from a map produces POINT or METRIC encodings");
+  if (first_bad) *first_bad = -1;
+  if (E == 0) return SPHP_OK;
+  if (int rc = tables_device(t)) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t np = t->np;
+  DevBuf scratch;
+  CK(scratch.ensure(sizeof(double) * E * np * 5 + 2 * sizeof(unsigned long long)));
+  double* wj = scratch.as<double>();
+  double* inv = wj + E * np;
+  auto* bad = reinterpret_cast<unsigned long long*>(inv + E * np * 4);
+  const unsigned long long init[2] = {0ull, ~0ull};
+  CK(cudaMemcpyAsync(bad, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  CK(jacobian_factors(E, np, dx, dy, t->d_wstd.as<double>(), wj, inv, bad, s));
+  unsigned long long hb[2];
+  CK(cudaMemcpyAsync(hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (hb[0]) {
+    if (first_bad) *first_bad = (int64_t)hb[1];
+    return fail(SPHP_ERR_BAD_ARG, "element " + std::to_string(hb[1]) + ": non-positive Jacobian at " +
+                                      std::to_string(hb[0]) + " quadrature point(s); invalid element");
+  }
+  GeomJob j;
+  std::memset(&j, 0, sizeof(j));
+  j.dim = 2;
+  j.kind = kind;
+  j.E = E;
+  j.npts = np;
+  j.cs = (np + 1) & ~1LL;
+  j.stride = geom_record(t, kind);
+  j.out = geom;
+  int* cbad = reinterpret_cast<int*>(bad);
+  CK(cudaMemsetAsync(cbad, 0, sizeof(int), s));
+  CK(geom_convert(j, wj, inv, cbad, s));
+  CK(cudaStreamSynchronize(s));
+  return SPHP_OK;
+}
+
 // collections.Collection.__init__ (collections.py:79-129)
 int sphp_collection_create(const sphp_tables* tc, int op, int strategy, int64_t E, int geom_kind,
                            const double* geom, double lambda, sphp_coll** out) {

@@ -155,6 +155,41 @@ cudaError_t geom_convert(const GeomJob& j, const double* wj, const double* inv, 
   return cudaGetLastError();
 }
 
+// geometry.geom_factors (geometry.py:125-142) from the reference-direction
+// derivatives of the coordinate map at the quadrature points: jac[k][a] =
+// dx_k / dxi_a, det, inv[a][k] = dxi_a / dx_k, wj = w det.  bad[0] counts
+// points with det <= 0, bad[1] keeps the first such element.
+__global__ void jacobian_factors_kernel(int64_t E, int64_t np, const double* __restrict__ dx,
+                                        const double* __restrict__ dy, const double* __restrict__ w,
+                                        double* __restrict__ wj, double* __restrict__ inv,
+                                        unsigned long long* bad) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= E * np) return;
+  const int64_t e = tid / np, i = tid - e * np;
+  const double j00 = dx[(e * 2) * np + i], j01 = dx[(e * 2 + 1) * np + i];
+  const double j10 = dy[(e * 2) * np + i], j11 = dy[(e * 2 + 1) * np + i];
+  const double det = j00 * j11 - j01 * j10;
+  if (!(det > 0.0)) {
+    atomicAdd(&bad[0], 1ull);
+    atomicMin(&bad[1], (unsigned long long)e);
+  }
+  double* iv = inv + tid * 4;
+  iv[0] = j11 / det;
+  iv[1] = -j01 / det;
+  iv[2] = -j10 / det;
+  iv[3] = j00 / det;
+  wj[tid] = w[i] * det;
+}
+
+cudaError_t jacobian_factors(int64_t E, int64_t np, const double* dx, const double* dy,
+                             const double* w, double* wj, double* inv, unsigned long long* bad,
+                             cudaStream_t s) {
+  const int64_t total = E * np;
+  if (total == 0) return cudaSuccess;
+  jacobian_factors_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(E, np, dx, dy, w, wj, inv, bad);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // assembly: scatter (global -> local) and colour-ordered assemble
 // ---------------------------------------------------------------------------

@@ -35,6 +35,9 @@ struct PointJob {
 cudaError_t geom_analytic(const GeomJob& j, int* bad, cudaStream_t s);
 cudaError_t geom_convert(const GeomJob& j, const double* wj, const double* inv, int* bad,
                          cudaStream_t s);
+cudaError_t jacobian_factors(int64_t E, int64_t np, const double* dx, const double* dy,
+                             const double* w, double* wj, double* inv, unsigned long long* bad,
+                             cudaStream_t s);
 // class-range kernels (periodic_ops.cu) over the x-rows [row0, row1) of
 // rows ey + n ez (row1 < 0: all); cudaErrorNotSupported if the grid or
 // order is outside their range
