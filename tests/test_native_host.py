@@ -161,9 +161,10 @@ def test_collection_errors_before_device_use():
 def test_c_abi_rejects_bad_keys():
     h = C.c_void_p()
     one = C.c_int * 3
+    # a triangle needs Modified_B in direction 2 (stdregions.py:83-86)
     rc = _lib.lib.sphp_tables_create(_lib.SHAPE_TRI, one(3, 3, 3), one(4, 4, 4), one(1, 1, 1),
                                      one(0, 0, 0), C.byref(h))
-    assert rc == _lib.ERR_UNSUPPORTED
+    assert rc == _lib.ERR_BAD_ARG and "collapsed-direction" in _lib.last_error()
     rc = _lib.lib.sphp_tables_create(_lib.SHAPE_HEX, one(3, 3, 3), one(1, 4, 4), one(1, 1, 1),
                                      one(0, 0, 0), C.byref(h))
     assert rc == _lib.ERR_BAD_ARG and "Lobatto" in _lib.last_error()
