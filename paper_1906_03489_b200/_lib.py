@@ -12,6 +12,9 @@ from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libspechp_b200.so"
+# tuning experiments may point at an alternative in-tree build
+if os.environ.get("SPHP_LIBRARY_VARIANT"):
+    LIB_PATH = _HERE.parent / "build" / "variants" / os.environ["SPHP_LIBRARY_VARIANT"] / "libspechp_b200.so"
 
 # error codes (include/spechp_b200.h)
 OK = 0

@@ -3,13 +3,16 @@
 #include "common.cuh"
 SPHP_DECLARE_TABLE_BANK(hex_misc)
 #include "launch.cuh"
+#ifndef SPHP_HEXOPS_BUDGET
+#define SPHP_HEXOPS_BUDGET (40 * 1024)  // per-CTA smem target: measured (tools/time_hexops.py)
+#endif
 
 namespace sphp {
 
 template <template <int, int, int, int, int> class OpT, int M, int Q, int GK>
 static cudaError_t go_gk(const OpArgs& oa, int64_t goff, cudaStream_t s) {
   using Probe = OpT<M, Q, GK, 1, 32>;
-  constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(), Q * Q);
+  constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(), Q * Q, SPHP_HEXOPS_BUDGET);
   constexpr int NT = choose_nt(NE, Q * Q);
   using Op = OpT<M, Q, GK, NE, NT>;
   return launch_pipe<Op, 0>(oa, geom_record<3, Q * Q * Q>(GK), goff, s);
@@ -18,7 +21,7 @@ static cudaError_t go_gk(const OpArgs& oa, int64_t goff, cudaStream_t s) {
 template <int M, int Q>
 static cudaError_t bwd_key(const OpArgs& oa, cudaStream_t s) {
   using Probe = HexBwd<M, Q, 1, 32>;
-  constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(), Q * Q);
+  constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(), Q * Q, SPHP_HEXOPS_BUDGET);
   constexpr int NT = choose_nt(NE, Q * Q);
   return launch_pipe<HexBwd<M, Q, NE, NT>, 0>(oa, 0, 0, s);
 }

@@ -4,13 +4,16 @@
 #include "common.cuh"
 SPHP_DECLARE_TABLE_BANK(quad)
 #include "launch.cuh"
+#ifndef SPHP_QUAD_BUDGET
+#define SPHP_QUAD_BUDGET (40 * 1024)  // per-CTA smem target: measured best for cfg2 (tools/time_quad.py)
+#endif
 
 namespace sphp {
 
 template <template <int, int, int, int, int> class OpT, int M, int Q, int GK, bool ASM = false>
 static cudaError_t qgo(const OpArgs& oa, int64_t goff, cudaStream_t s) {
   using Probe = OpT<M, Q, GK, 1, 32>;
-  constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(), Q);
+  constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(), Q, SPHP_QUAD_BUDGET);
   constexpr int NT = choose_nt(NE, Q);
   using Op = OpT<M, Q, GK, NE, NT>;
   const int64_t rec = geom_record<2, Q * Q>(GK);
@@ -32,7 +35,7 @@ static cudaError_t qhelm_key(const OpArgs& oa, cudaStream_t s) {
 template <int M, int Q>
 static cudaError_t qbwd_key(const OpArgs& oa, cudaStream_t s) {
   using Probe = QuadBwd<M, Q, 1, 32>;
-  constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(), Q);
+  constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(), Q, SPHP_QUAD_BUDGET);
   constexpr int NT = choose_nt(NE, Q);
   return launch_pipe<QuadBwd<M, Q, NE, NT>, 0>(oa, 0, 0, s);
 }

@@ -3,6 +3,9 @@
 // Helmholtz operator (geometry.py:171-184).
 // Layouts: coefficient c[p*M + q], point u[i*Q + j] (stdregions.py:5-13).
 #pragma once
+#ifndef SPHP_QUAD_NST
+#define SPHP_QUAD_NST 1  // quad tile pipeline input stages (tuning)
+#endif
 #include "hex_ops.cuh"
 
 namespace sphp {
@@ -12,6 +15,7 @@ namespace sphp {
 template <int M_, int Q_, int GK, int NE_, int NT_>
 struct QuadHelm {
   static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int NSTP = SPHP_QUAD_NST;  // preferred input stages
   static constexpr int M2 = M * M, Q2 = Q * Q;
   static constexpr int IN = M2, OUT = M2;
   static constexpr int CS = pt_stride(Q2);
@@ -137,6 +141,7 @@ struct QuadHelm {
 template <int M_, int Q_, int NE_, int NT_>
 struct QuadBwd {
   static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int NSTP = SPHP_QUAD_NST;
   static constexpr int M2 = M * M, Q2 = Q * Q;
   static constexpr int IN = M2, OUT = Q2, GEO = 0;
   static constexpr int QK = odd_up(Q);
@@ -165,6 +170,7 @@ struct QuadBwd {
 template <int M_, int Q_, int GK, int NE_, int NT_>
 struct QuadIprod {
   static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int NSTP = SPHP_QUAD_NST;
   static constexpr int M2 = M * M, Q2 = Q * Q;
   static constexpr int IN = Q2, OUT = M2;
   static constexpr int CS = pt_stride(Q2);
@@ -214,6 +220,7 @@ struct QuadIprod {
 template <int M_, int Q_, int GK, int NE_, int NT_>
 struct QuadPhysDeriv {
   static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int NSTP = SPHP_QUAD_NST;
   static constexpr int Q2 = Q * Q;
   static constexpr int IN = Q2, OUT = 2 * Q2;
   static constexpr int CS = pt_stride(Q2);
@@ -275,6 +282,7 @@ struct QuadPhysDeriv {
 template <int M_, int Q_, int GK, int NE_, int NT_>
 struct QuadIPDeriv {
   static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int NSTP = SPHP_QUAD_NST;
   static constexpr int M2 = M * M, Q2 = Q * Q;
   static constexpr int IN = 2 * Q2, OUT = M2;
   static constexpr int CS = pt_stride(Q2);
