@@ -77,11 +77,19 @@ constexpr int nst_pref_impl(...) { return 1; }
 template <class Op>
 constexpr int nst_pref() { return nst_pref_impl<Op>(0); }
 
+// smem stride of one element's staged geometry: Op::GEO_S when the op pads
+// it (bank spreading across elements), else GEO
+template <class Op>
+constexpr auto geo_s_impl(int) -> decltype(Op::GEO_S, int()) { return Op::GEO_S; }
+template <class Op>
+constexpr int geo_s_impl(...) { return Op::GEO; }
+
 template <class Op, int MODE>
 struct Scaffold {
   static constexpr int NE = Op::NE, NT = Op::NT;
   static constexpr int IN_T = even_up(NE * Op::IN + 2);
-  static constexpr int GEO_T = NE * Op::GEO;  // GEO is even
+  static constexpr int GEO_S = geo_s_impl<Op>(0);  // even, >= GEO
+  static constexpr int GEO_T = NE * GEO_S;
   static constexpr int STAGE = IN_T + GEO_T;
   static constexpr int OUT_T = even_up(NE * Op::OUT);
   static constexpr int WORK_T = even_up(NE * Op::WORK);
@@ -105,6 +113,7 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
   using S = Scaffold<Op, MODE>;
   using MT = ModeTraits<MODE>;
   constexpr int NE = Op::NE, NT = Op::NT, IN = Op::IN, OUT = Op::OUT, GEO = Op::GEO;
+  constexpr int GEO_S = S::GEO_S;
   constexpr int NST = S::NST, ENT = S::ENT;
   extern __shared__ __align__(128) double smem[];
   double* stage_base = smem;
@@ -157,11 +166,11 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     mbar_expect_tx(&bar[s], bytes_in + bytes_g);
     bulk_g2s(in_s, reinterpret_cast<const char*>(a.in) + a0, bytes_in, &bar[s]);
     if (GEO > 0) {
-      if (a.gstride == GEO && a.goff == 0) {
+      if (a.gstride == GEO && a.goff == 0 && GEO_S == GEO) {
         bulk_g2s(geo_s, a.geom + w0 * a.gstride, bytes_g, &bar[s]);
       } else {
         for (int e = 0; e < r; ++e)
-          bulk_g2s(geo_s + e * GEO, a.geom + (w0 + e) * a.gstride + a.goff,
+          bulk_g2s(geo_s + e * GEO_S, a.geom + (w0 + e) * a.gstride + a.goff,
                    (uint32_t)(sizeof(double) * GEO), &bar[s]);
       }
     }
@@ -185,11 +194,11 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
         fence_proxy_async();
         const uint32_t bytes = (uint32_t)(sizeof(double) * r * GEO);
         mbar_expect_tx(&bar[s], bytes);
-        if (a.gstride == GEO && a.goff == 0) {
+        if (a.gstride == GEO && a.goff == 0 && GEO_S == GEO) {
           bulk_g2s(geo_s, a.geom + w0 * a.gstride, bytes, &bar[s]);
         } else {
           for (int e = 0; e < r; ++e)
-            bulk_g2s(geo_s + e * GEO, a.geom + (w0 + e) * a.gstride + a.goff,
+            bulk_g2s(geo_s + e * GEO_S, a.geom + (w0 + e) * a.gstride + a.goff,
                      (uint32_t)(sizeof(double) * GEO), &bar[s]);
         }
       }
@@ -245,7 +254,7 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
       fence_proxy_async();
       mbar_expect_tx(&bar[s], (uint32_t)(sizeof(double) * r * GEO));
       for (int e = 0; e < r; ++e)
-        bulk_g2s(geo_s + e * GEO, a.geom + (int64_t)ids[e] * a.gstride + a.goff,
+        bulk_g2s(geo_s + e * GEO_S, a.geom + (int64_t)ids[e] * a.gstride + a.goff,
                  (uint32_t)(sizeof(double) * GEO), &bar[s]);
     }
     for (int i = tid; i < NE * IN; i += NT) {
@@ -303,14 +312,14 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
         if constexpr (GEO > 0) {
           for (int i = tid; i < r * GEO; i += NT) {
             int e = i / GEO, c = i - e * GEO;
-            geo_s[i] = a.geom[(w0 + e) * a.gstride + a.goff + c];
+            geo_s[e * GEO_S + c] = a.geom[(w0 + e) * a.gstride + a.goff + c];
           }
         }
       }
       // zero the unused tail of a partial tile (its results are discarded)
       for (int i = r * IN + tid; i < NE * IN; i += NT) in_s[(in_p - in_s) + i] = 0.0;
       if (GEO > 0)
-        for (int i = r * GEO + tid; i < NE * GEO; i += NT) geo_s[i] = 0.0;
+        for (int i = r * GEO_S + tid; i < NE * GEO_S; i += NT) geo_s[i] = 0.0;
     } else {
       cp_async_wait<NST - 1>();
       if (GEO > 0) {
@@ -327,7 +336,7 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
       if (MT::SCATTER)
         for (int i = tid; i < NE * (1 + ENT); i += NT) icur[i] = ids[i];
       if (GEO > 0)
-        for (int i = r * GEO + tid; i < NE * GEO; i += NT) geo_s[i] = 0.0;
+        for (int i = r * GEO_S + tid; i < NE * GEO_S; i += NT) geo_s[i] = 0.0;
     }
     __syncthreads();
 

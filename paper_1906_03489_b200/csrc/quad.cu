@@ -25,10 +25,23 @@ static cudaError_t qgo(const OpArgs& oa, int64_t goff, cudaStream_t s) {
   return cudaErrorNotSupported;
 }
 
+// the Helmholtz tile is 8 elements (its bank-spread layout assumes it)
+template <int M, int Q, int GK>
+static cudaError_t qhelm_go(const OpArgs& oa, cudaStream_t s) {
+  constexpr int NE = 8;
+  constexpr int NT = choose_nt(NE, Q);
+  using Op = QuadHelm<M, Q, GK, NE, NT>;
+  const int64_t rec = geom_record<2, Q * Q>(GK);
+  if (oa.mode == AsmMode::LOCAL) return launch_pipe<Op, 0>(oa, rec, 0, s);
+  if (oa.mode == AsmMode::EXPLICIT) return launch_pipe<Op, 2>(oa, rec, 0, s);
+  if (oa.mode == AsmMode::EXPLICIT_GATHER) return launch_pipe<Op, 4>(oa, rec, 0, s);
+  return cudaErrorNotSupported;
+}
+
 template <int M, int Q>
 static cudaError_t qhelm_key(const OpArgs& oa, cudaStream_t s) {
-  if (oa.geom_kind == SPHP_GEOM_METRIC) return qgo<QuadHelm, M, Q, SPHP_GEOM_METRIC, true>(oa, 0, s);
-  if (oa.geom_kind == SPHP_GEOM_AFFINE) return qgo<QuadHelm, M, Q, SPHP_GEOM_AFFINE, true>(oa, 0, s);
+  if (oa.geom_kind == SPHP_GEOM_METRIC) return qhelm_go<M, Q, SPHP_GEOM_METRIC>(oa, s);
+  if (oa.geom_kind == SPHP_GEOM_AFFINE) return qhelm_go<M, Q, SPHP_GEOM_AFFINE>(oa, s);
   return cudaErrorNotSupported;
 }
 

@@ -12,6 +12,19 @@ namespace sphp {
 
 // 2D geometry records: AFFINE [det, inv00, inv01, inv10, inv11, pad];
 // POINT [wJ, inv00, inv01, inv10, inv11] x CS; METRIC [G00, G01, G11, wJ] x CS
+// smallest stride >= x that is = 2 (mod 16) doubles: eight elements at that
+// stride start on eight distinct even bank pairs (and on eight distinct
+// 16-byte slots of a 128-byte line), so a half-warp of 8 elements x 2
+// positions that differ by an odd offset is conflict free
+__host__ __device__ constexpr int spread16(int x) { return x + ((2 - x % 16) + 16) % 16; }
+
+// Fused Helmholtz on quads.  Work items are ordered element-fastest (item w:
+// element w % NE, position w / NE) with NE = 8, and the per-element strides
+// of the work buffers (SW) and of the staged geometry (GEO_S) are = 2 (mod
+// 16): every stage's half-warp (8 elements x 2 positions, odd position
+// offset) and every geometry row read (a quarter-warp of 8 elements, same
+// row: LDS.128) then touch distinct banks.  (The first layout, positions
+// fastest with SW = odd, measured 59 % bank-conflict excess at cfg2.)
 template <int M_, int Q_, int GK, int NE_, int NT_>
 struct QuadHelm {
   static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
@@ -20,8 +33,9 @@ struct QuadHelm {
   static constexpr int IN = M2, OUT = M2;
   static constexpr int CS = pt_stride(Q2);
   static constexpr int GEO = (GK == SPHP_GEOM_METRIC) ? 4 * CS : 6;
+  static constexpr int GEO_S = (GK == SPHP_GEOM_METRIC) ? spread16(GEO) : GEO;
   static constexpr int QK = odd_up(Q);
-  static constexpr int SW = odd_up(Q * QK);
+  static constexpr int SW = spread16(Q * QK);
   static constexpr int WORK = 3 * SW;
   using T = Tab<M, Q>;
 
@@ -33,12 +47,12 @@ struct QuadHelm {
     double* W1 = work + NE * SW;
     double* W2 = work + 2 * NE * SW;
     SPHP_FOR_ITEMS(NE * M, w) {  // q -> j
-      int e = w / M, p = w - e * M;
+      const int e = w % NE, p = w / NE;
       eo_interp<M, Q, 1, 1>(tab, cin + e * M2 + p * M, W0 + e * SW + p * QK);
     }
     __syncthreads();
     SPHP_FOR_ITEMS(NE * Q, w) {  // p -> i, u and d0
-      int e = w / Q, j = w - e * Q;
+      const int e = w % NE, j = w / NE;
       double x[M];
 #pragma unroll
       for (int p = 0; p < M; ++p) x[p] = W0[e * SW + p * QK + j];
@@ -56,12 +70,12 @@ struct QuadHelm {
     }
     __syncthreads();
     SPHP_FOR_ITEMS(NE * Q, w) {  // pencil along j: d1, fluxes, t = mass + D1^T f1
-      int e = w / Q, i = w - e * Q;
+      const int e = w % NE, i = w / NE;
       const int base = e * SW + i * QK;
       double u[Q], f1[Q];
 #pragma unroll
       for (int j = 0; j < Q; ++j) u[j] = W1[base + j];
-      const double* g = geo + e * GEO;
+      const double* g = geo + e * GEO_S;
       double a00, a01, a11, adet;
       if (GK == SPHP_GEOM_AFFINE) {
         const double det = g[0];
@@ -111,7 +125,7 @@ struct QuadHelm {
     __syncthreads();
     release();
     SPHP_FOR_ITEMS(NE * Q, w) {  // i -> p : B t + Bd f0
-      int e = w / Q, j = w - e * Q;
+      const int e = w % NE, j = w / NE;
       double t[Q], f0[Q];
 #pragma unroll
       for (int i = 0; i < Q; ++i) {
@@ -132,7 +146,7 @@ struct QuadHelm {
     pre_out();
     __syncthreads();
     SPHP_FOR_ITEMS(NE * M, w) {  // j -> q
-      int e = w / M, p = w - e * M;
+      const int e = w % NE, p = w / NE;
       eo_project<M, Q, 1, 1>(tab, W0 + e * SW + p * QK, out + e * M2 + p * M);
     }
   }
