@@ -482,6 +482,7 @@ struct HexHelmEO {
   static constexpr int PP2 = pitch_mod16(Q * Q, Q);
   static constexpr int SE = even_up(cmax(Q3, cmax(M * PP1, M * PP2)));
   static constexpr int WORK = 3 * SE;
+  static constexpr int OUT_OFF = NE * SE;  // S9 writes the block into W1 (free after S8)
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
 
@@ -656,6 +657,7 @@ struct HexHelmJEO {
   static constexpr int QK = odd_up(Q);
   static constexpr int SW = odd_up(Q * Q * QK);
   static constexpr int WORK = 3 * SW;
+  static constexpr int OUT_OFF = NE * SW;  // the last stage writes the block into W1 (free)
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
 

@@ -84,6 +84,14 @@ constexpr auto geo_s_impl(int) -> decltype(Op::GEO_S, int()) { return Op::GEO_S;
 template <class Op>
 constexpr int geo_s_impl(...) { return Op::GEO; }
 
+// an Op whose last stage leaves part of its work area free may stage the
+// output block there (Op::OUT_OFF, doubles into the work area): one buffer
+// fewer, which is what lets the P=4 Helmholtz tile fit four CTAs per SM
+template <class Op>
+constexpr auto out_off_impl(int) -> decltype(Op::OUT_OFF, int()) { return Op::OUT_OFF; }
+template <class Op>
+constexpr int out_off_impl(...) { return -1; }
+
 template <class Op, int MODE>
 struct Scaffold {
   static constexpr int NE = Op::NE, NT = Op::NT;
@@ -91,7 +99,8 @@ struct Scaffold {
   static constexpr int GEO_S = geo_s_impl<Op>(0);  // even, >= GEO
   static constexpr int GEO_T = NE * GEO_S;
   static constexpr int STAGE = IN_T + GEO_T;
-  static constexpr int OUT_T = even_up(NE * Op::OUT);
+  static constexpr int OUT_OFF = out_off_impl<Op>(0);
+  static constexpr int OUT_T = OUT_OFF >= 0 ? 0 : even_up(NE * Op::OUT);
   static constexpr int WORK_T = even_up(NE * Op::WORK);
   // assembled-mode integer tables (in doubles): per stage ids + entities,
   // current-tile copies, and the per-mode code table
@@ -117,8 +126,8 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
   constexpr int NST = S::NST, ENT = S::ENT;
   extern __shared__ __align__(128) double smem[];
   double* stage_base = smem;
-  double* out_s = smem + NST * S::STAGE;
-  double* work = out_s + S::OUT_T;
+  double* work = smem + NST * S::STAGE + S::OUT_T;
+  double* out_s = S::OUT_OFF >= 0 ? work + (S::OUT_OFF >= 0 ? S::OUT_OFF : 0) : smem + NST * S::STAGE;
   int* itab = reinterpret_cast<int*>(work + S::WORK_T);      // NST stages of [ids NE | ent NE*27]
   int* icur = itab + NST * 2 * S::ITAB;                       // current tile copy
   int* mtab = icur + 2 * S::ITAB;                             // per-mode codes (MODE 1)
