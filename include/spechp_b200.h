@@ -180,14 +180,10 @@ int sphp_amap_destroy(sphp_amap* a);
  *          colouring of explicit maps) fused gather/scatter-add, one launch
  *          per colour in a fixed colour order;
  *   SPLIT  scatter kernel -> fused operator on the local block -> owner
- *          sum (three launches);
- *   FUSED  scatter kernel -> one launch running the fused operator tiles
- *          and the owner sums from one dependency-ordered work queue
- *          (periodic hex maps, P >= 2, n % 4 == 0; same sums as SPLIT).  */
+ *          sum (three launches).                                          */
 #define SPHP_ASSEMBLY_OWNER 0
 #define SPHP_ASSEMBLY_COLOUR 1
 #define SPHP_ASSEMBLY_SPLIT 2
-#define SPHP_ASSEMBLY_FUSED 3
 int sphp_amap_set_algorithm(sphp_amap* a, int alg);
 int sphp_amap_algorithm(const sphp_amap* a, int* alg);
 int sphp_amap_info(const sphp_amap* a, int64_t* num_elements, int* nmodes,

@@ -31,7 +31,7 @@ OP_BWD_TRANS, OP_IPRODUCT_WRT_BASE, OP_PHYS_DERIV, OP_IPRODUCT_WRT_DERIV_BASE, O
 STRATEGY_CUDA_SUMFAC, STRATEGY_CUDA_STDMAT = 0, 1
 GEOM_NONE, GEOM_AFFINE, GEOM_POINT, GEOM_METRIC = 0, 1, 2, 3
 MAP_AFFINE, MAP_QUAD_SINE, MAP_HEX_SINE = 0, 1, 2
-ASSEMBLY_OWNER, ASSEMBLY_COLOUR, ASSEMBLY_SPLIT, ASSEMBLY_FUSED = 0, 1, 2, 3
+ASSEMBLY_OWNER, ASSEMBLY_COLOUR, ASSEMBLY_SPLIT = 0, 1, 2
 RIEMANN = {"upwind": 0, "laxfriedrichs": 1}
 BC_INTERIOR, BC_RIGID_WALL, BC_FARFIELD, BC_DIRICHLET = 0, 1, 2, 3
 

@@ -65,12 +65,12 @@ class AssemblyMap:
 
     @property
     def algorithm(self):
-        """'owner', 'colour', 'split' or 'fused' (the library default for
+        """'owner', 'colour' or 'split' (the library default: split for
         periodic maps the class-range kernels support, owner otherwise)."""
         a = C.c_int()
         _lib.check(_lib.lib.sphp_amap_algorithm(self._h, C.byref(a)), AssemblyError)
         return {_lib.ASSEMBLY_OWNER: "owner", _lib.ASSEMBLY_COLOUR: "colour",
-                _lib.ASSEMBLY_SPLIT: "split", _lib.ASSEMBLY_FUSED: "fused"}[a.value]
+                _lib.ASSEMBLY_SPLIT: "split"}[a.value]
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -101,12 +101,10 @@ class AssemblyMap:
 
     def set_algorithm(self, alg):
         """'owner' (gather -> local -> owner-computes sum), 'split' (scatter
-        kernel -> local operator -> owner sum), 'fused' (scatter kernel ->
-        one launch running the local operator tiles and the owner sums from
-        a dependency-ordered queue; periodic hex maps) or 'colour' (fused
+        kernel -> local operator -> owner sum) or 'colour' (fused
         colour-ordered scatter-add)."""
         code = {"owner": _lib.ASSEMBLY_OWNER, "colour": _lib.ASSEMBLY_COLOUR,
-                "split": _lib.ASSEMBLY_SPLIT, "fused": _lib.ASSEMBLY_FUSED}[alg]
+                "split": _lib.ASSEMBLY_SPLIT}[alg]
         _lib.check(_lib.lib.sphp_amap_set_algorithm(self._h, code), AssemblyError)
         return self
 

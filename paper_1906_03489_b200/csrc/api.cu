@@ -212,7 +212,6 @@ struct sphp_coll {
   DevBuf mat_a, mat_b;            // StdMat dense operators
   DevBuf helm_H;                  // StdMat Helmholtz element matrices
   DevBuf loc_x, loc_y;            // StdMat assembled path
-  DevBuf fsync;                   // FUSED assembly: claim counter + per-tile flags
   // host-buffer pipeline (sphp_helmholtz_assembled_host): copy streams and
   // per-slab events, created on first use
   cudaStream_t pipe_h2d = nullptr, pipe_d2h = nullptr;
@@ -1073,7 +1072,7 @@ static int amap_device(const sphp_amap* ac) {
 // local (E, nm) -> global with the map's algorithm; accumulate adds to g
 static int amap_assemble_any(const sphp_amap* a, const double* loc, double* g, int accumulate,
                              cudaStream_t s, int mode_major = 0) {
-  if (a->alg == SPHP_ASSEMBLY_OWNER || a->alg == SPHP_ASSEMBLY_SPLIT || a->alg == SPHP_ASSEMBLY_FUSED) {
+  if (a->alg == SPHP_ASSEMBLY_OWNER || a->alg == SPHP_ASSEMBLY_SPLIT) {
     if (a->periodic) {
       CK(owner_assemble_periodic(a->n, a->P, loc, g, accumulate, mode_major, s));
     } else {
@@ -1218,11 +1217,8 @@ int sphp_hexmap_variable(int n, const int* orders, int64_t* num_global, int64_t*
 
 int sphp_amap_set_algorithm(sphp_amap* a, int alg) {
   if (!a) return fail(SPHP_ERR_BAD_ARG, "null map");
-  if (alg != SPHP_ASSEMBLY_OWNER && alg != SPHP_ASSEMBLY_COLOUR && alg != SPHP_ASSEMBLY_SPLIT &&
-      alg != SPHP_ASSEMBLY_FUSED)
+  if (alg != SPHP_ASSEMBLY_OWNER && alg != SPHP_ASSEMBLY_COLOUR && alg != SPHP_ASSEMBLY_SPLIT)
     return fail(SPHP_ERR_BAD_ARG, "unknown assembly algorithm");
-  if (alg == SPHP_ASSEMBLY_FUSED && !(a->periodic && a->P >= 2 && a->n % 4 == 0))
-    return fail(SPHP_ERR_UNSUPPORTED, "FUSED assembly needs a periodic hex map with P >= 2 and n % 4 == 0");
   a->alg = alg;
   return SPHP_OK;
 }
@@ -1294,30 +1290,7 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
   OpArgs o = base_args(c);
   o.xg = x;
   o.yg = y;
-  if (a->alg == SPHP_ASSEMBLY_FUSED && a->periodic && c->t->shape == SPHP_SHAPE_HEX) {
-    // scatter -> one launch: fused local operator tiles + owner-computes
-    // sums from the same work queue (fused_owner.cuh)
-    CK(c->loc_x.ensure(sizeof(double) * c->E * c->t->nm));
-    CK(c->loc_y.ensure(sizeof(double) * c->E * c->t->nm));
-    CK(c->fsync.ensure(sizeof(int) * (c->E + 2)));
-    CK(amap_scatter(a->dev(), x, c->loc_x.as<double>(), s));
-    o.in = c->loc_x.as<double>();
-    o.out = c->loc_y.as<double>();
-    o.mode = AsmMode::PERIODIC_FUSED;
-    o.n = a->n;
-    o.sync = c->fsync.as<int>();
-    o.accumulate = accumulate;
-    cudaError_t e = sumfac_launch(c, o, s);
-    if (e == cudaSuccess) return SPHP_OK;
-    if (e != cudaErrorNotSupported) return cuda_fail(e, "sphp_helmholtz_assembled");
-    // no fused kernel for this key: the split form below
-    o.mode = AsmMode::LOCAL;
-    e = sumfac_launch(c, o, s);
-    if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no kernel for this key");
-    if (e != cudaSuccess) return cuda_fail(e, "sphp_helmholtz_assembled");
-    return amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s, 0);
-  }
-  if (a->alg == SPHP_ASSEMBLY_SPLIT || a->alg == SPHP_ASSEMBLY_FUSED) {
+  if (a->alg == SPHP_ASSEMBLY_SPLIT) {
     // scatter -> fused local operator -> owner-computes sum (three launches;
     // the fused kernel then runs in its block-input form)
     CK(c->loc_x.ensure(sizeof(double) * c->E * c->t->nm));
@@ -1508,8 +1481,7 @@ int sphp_helmholtz_assembled_host(sphp_coll* c, const sphp_amap* a, const double
   if (!c || !a || !x || !y) return fail(SPHP_ERR_BAD_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
   if (c->op == SPHP_OP_HELMHOLTZ && c->strategy == SPHP_STRATEGY_CUDA_SUMFAC && a->periodic &&
-      (a->alg == SPHP_ASSEMBLY_SPLIT || a->alg == SPHP_ASSEMBLY_FUSED) && a->P >= 2 && a->n % 4 == 0 &&
-      a->E == c->E && a->nm == c->t->nm &&
+      a->alg == SPHP_ASSEMBLY_SPLIT && a->P >= 2 && a->n % 4 == 0 && a->E == c->E && a->nm == c->t->nm &&
       c->t->shape == SPHP_SHAPE_HEX) {
     const std::vector<int> zb = host_slabs(a->n);
     if (zb.size() > 2) {

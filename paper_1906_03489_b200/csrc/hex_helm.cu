@@ -14,7 +14,6 @@ SPHP_DECLARE_TABLE_BANK(hex_helm2)
 #include <cstdlib>
 
 #include "launch.cuh"
-#include "fused_owner.cuh"
 
 namespace sphp {
 
@@ -25,11 +24,6 @@ static cudaError_t helm_variant(const OpArgs& oa, cudaStream_t s) {
   constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(NSTP), Q * Q, BUDGET);
   constexpr int NT = choose_nt(NE, Q * Q);
   using Op = HexHelm<M, Q, GK, NE, NT, NSTP>;
-  if (oa.mode == AsmMode::PERIODIC_FUSED) {
-    if constexpr (Scaffold<Op, 0>::NST == 1 && M >= 3)
-      return launch_fused<Op>(oa, geom_record<3, Q * Q * Q>(GK), s);
-    return cudaErrorNotSupported;
-  }
   return launch_mode<Op>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
 }
 
@@ -50,8 +44,7 @@ static int helm_variant_env() {
 // than a second stage does.  SPHP_HELM_VARIANT=0..4 overrides for tuning.
 template <int M, int Q, int GK>
 static cudaError_t helm_go(const OpArgs& oa, cudaStream_t s) {
-  if (oa.mode == AsmMode::LOCAL || oa.mode == AsmMode::PERIODIC_GATHER ||
-      oa.mode == AsmMode::PERIODIC_FUSED) {
+  if (oa.mode == AsmMode::LOCAL || oa.mode == AsmMode::PERIODIC_GATHER) {
 #ifdef SPHP_TUNING  // tile-shape sweep build (make EXTRA_NVFLAGS=-DSPHP_TUNING)
     switch (helm_variant_env()) {
       case 0: return helm_variant<M, Q, GK, 2, 110 * 1024>(oa, s);
@@ -62,7 +55,7 @@ static cudaError_t helm_go(const OpArgs& oa, cudaStream_t s) {
       default: break;
     }
 #endif
-    if (oa.mode != AsmMode::PERIODIC_GATHER) return helm_variant<M, Q, GK, 1, 74 * 1024>(oa, s);
+    if (oa.mode == AsmMode::LOCAL) return helm_variant<M, Q, GK, 1, 74 * 1024>(oa, s);
   }
   return helm_variant<M, Q, GK, 1, 55 * 1024>(oa, s);
 }

@@ -501,7 +501,7 @@ struct HexHelmEO {
       X::interp(tab, x, u);
       st_pencil<Q, 1>(W0 + e * SE + p * PP1 + q * QK, u);
     }
-    cta_bar<NT>();
+    __syncthreads();
     // S2: q -> j
     SPHP_FOR_ITEMS(NE * M * Q, w) {
       int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
@@ -510,7 +510,7 @@ struct HexHelmEO {
       X::interp(tab, x, u);
       st_pencil<Q, Q>(W1 + e * SE + p * PP2 + k, u);
     }
-    cta_bar<NT>();
+    __syncthreads();
     // S3: p -> i, u and d0
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), jk = w - e * (Q * Q);
@@ -520,7 +520,7 @@ struct HexHelmEO {
       st_pencil<Q, Q * Q>(W0 + e * SE + jk, u);
       st_pencil<Q, Q * Q>(W2 + e * SE + jk, d);
     }
-    cta_bar<NT>();
+    __syncthreads();
     // S4: d1 = D along j
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
@@ -529,7 +529,7 @@ struct HexHelmEO {
       X::template deriv<false, false>(tab, v, r);
       st_pencil<Q, Q>(W1 + e * SE + i * Q * Q + k, r);
     }
-    cta_bar<NT>();
+    __syncthreads();
     // S5: k rows
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), ij = w - e * (Q * Q), i = ij / Q, j = ij - i * Q;
@@ -599,7 +599,7 @@ struct HexHelmEO {
       store_row<Q>(W2 + row, f0);
       store_row<Q>(W1 + row, f1);
     }
-    cta_bar<NT>();
+    __syncthreads();
     release();
     // S6: t += D1^T f1 along j
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
@@ -610,7 +610,7 @@ struct HexHelmEO {
       X::template deriv<true, true>(tab, f, t);
       st_pencil<Q, Q>(W0 + e * SE + i * Q * Q + k, t);
     }
-    cta_bar<NT>();
+    __syncthreads();
     // S7: i -> p, B t + dB f0
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), jk = w - e * (Q * Q);
@@ -620,7 +620,7 @@ struct HexHelmEO {
       X::project2(tab, t, f0, c);
       st_pencil<M, PP2>(W1 + e * SE + jk, c);
     }
-    cta_bar<NT>();
+    __syncthreads();
     // S8: j -> q
     SPHP_FOR_ITEMS(NE * M * Q, w) {
       int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
@@ -630,7 +630,7 @@ struct HexHelmEO {
       st_pencil<M, QK>(W0 + e * SE + p * PP1 + k, c);
     }
     pre_out();
-    cta_bar<NT>();
+    __syncthreads();
     // S9: k -> r
     SPHP_FOR_ITEMS(NE * M * M, w) {
       int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
@@ -675,7 +675,7 @@ struct HexHelmJEO {
       X::interp(tab, x, u);
       st_pencil<Q, 1>(W0 + e * SW + pq * QK, u);
     }
-    cta_bar<NT>();
+    __syncthreads();
     SPHP_FOR_ITEMS(NE * M * Q, w) {  // S2 q -> j
       int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
       double x[M], u[Q];
@@ -683,7 +683,7 @@ struct HexHelmJEO {
       X::interp(tab, x, u);
       st_pencil<Q, QK>(W1 + e * SW + p * Q * QK + k, u);
     }
-    cta_bar<NT>();
+    __syncthreads();
     SPHP_FOR_ITEMS(NE * Q * Q, w) {  // S3 p -> i: u, d0
       int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
       double x[M], u[Q], d[Q];
@@ -692,7 +692,7 @@ struct HexHelmJEO {
       st_pencil<Q, Q * QK>(W0 + e * SW + j * QK + k, u);
       st_pencil<Q, Q * QK>(W2 + e * SW + j * QK + k, d);
     }
-    cta_bar<NT>();
+    __syncthreads();
     SPHP_FOR_ITEMS(NE * Q * Q, w) {  // S4 d2 = D along k
       int e = w / (Q * Q), ij = w - e * (Q * Q);
       double v[Q], r[Q];
@@ -700,7 +700,7 @@ struct HexHelmJEO {
       X::template deriv<false, false>(tab, v, r);
       st_pencil<Q, 1>(W1 + e * SW + ij * QK, r);
     }
-    cta_bar<NT>();
+    __syncthreads();
     SPHP_FOR_ITEMS(NE * Q * Q, w) {  // S5 pencil along j: pointwise, t = mass + D1^T f1
       int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
       const int base = e * SW + i * Q * QK + k;
@@ -753,7 +753,7 @@ struct HexHelmJEO {
       X::template deriv<true, true>(tab, f1, u);
       st_pencil<Q, QK>(W0 + base, u);
     }
-    cta_bar<NT>();
+    __syncthreads();
     release();
     SPHP_FOR_ITEMS(NE * Q * Q, w) {  // S6 t += D2^T f2 along k
       int e = w / (Q * Q), ij = w - e * (Q * Q);
@@ -763,7 +763,7 @@ struct HexHelmJEO {
       X::template deriv<true, true>(tab, f, t);
       st_pencil<Q, 1>(W0 + e * SW + ij * QK, t);
     }
-    cta_bar<NT>();
+    __syncthreads();
     SPHP_FOR_ITEMS(NE * Q * Q, w) {  // S7 i -> p
       int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
       double t[Q], f0[Q], c[M];
@@ -772,7 +772,7 @@ struct HexHelmJEO {
       X::project2(tab, t, f0, c);
       st_pencil<M, Q * QK>(W1 + e * SW + j * QK + k, c);
     }
-    cta_bar<NT>();
+    __syncthreads();
     SPHP_FOR_ITEMS(NE * M * Q, w) {  // S8 j -> q
       int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
       double v[Q], c[M];
@@ -781,7 +781,7 @@ struct HexHelmJEO {
       st_pencil<M, QK>(W0 + e * SW + p * M * QK + k, c);
     }
     pre_out();
-    cta_bar<NT>();
+    __syncthreads();
     SPHP_FOR_ITEMS(NE * M * M, w) {  // S9 k -> r
       int e = w / (M * M), pq = w - e * (M * M);
       double v[Q], c[M];

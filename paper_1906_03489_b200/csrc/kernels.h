@@ -11,16 +11,7 @@ namespace sphp {
 // LOCAL: block in/out.  PERIODIC / EXPLICIT: one colour class, gather in,
 // scatter-add out.  PERIODIC_GATHER / EXPLICIT_GATHER: all elements, gather
 // in, local block out (the owner-computes assembly then sums it).
-// PERIODIC_FUSED: local block in, local block out plus the owner-computes
-// sum into yg inside the same launch (fused_owner.cuh; hex Helmholtz only).
-enum class AsmMode : int {
-  LOCAL = 0,
-  PERIODIC = 1,
-  EXPLICIT = 2,
-  PERIODIC_GATHER = 3,
-  EXPLICIT_GATHER = 4,
-  PERIODIC_FUSED = 5
-};
+enum class AsmMode : int { LOCAL = 0, PERIODIC = 1, EXPLICIT = 2, PERIODIC_GATHER = 3, EXPLICIT_GATHER = 4 };
 
 struct OpArgs {
   int M, Q;          // modes / points per direction
@@ -42,14 +33,7 @@ struct OpArgs {
   const int* ent_g;   // PERIODIC_GATHER: precomputed (E, 27) entity bases (optional)
   int n;              // PERIODIC: grid size
   int colour;         // PERIODIC: colour id 0..7
-  int* sync = nullptr;  // PERIODIC_FUSED: two counters + per-tile flags (>= E + 2 ints)
-  int accumulate = 0;   // PERIODIC_FUSED: add the owner sums into yg
 };
-
-// PERIODIC_FUSED host helpers (periodic_ops.cu): owner segment length and
-// the owner-segment queue in dependency order (device, cached per key)
-int fused_segment_length(int n);
-const int* fused_queue(int n, int ne, int L, int* nqueue);
 
 // hex (3D) sum-factorisation kernels
 cudaError_t hex_helmholtz(const OpArgs& a, cudaStream_t s);

@@ -114,8 +114,6 @@ cudaError_t launch_mode(const OpArgs& oa, int64_t gstride, int64_t goff, cudaStr
       return launch_pipe<Op, 3>(oa, gstride, goff, s);
     case AsmMode::EXPLICIT_GATHER:
       return launch_pipe<Op, 4>(oa, gstride, goff, s);
-    case AsmMode::PERIODIC_FUSED:  // hex Helmholtz only (hex_helm.cu)
-      return cudaErrorNotSupported;
   }
   return cudaErrorInvalidValue;
 }

@@ -17,18 +17,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include <algorithm>
 #include <atomic>
-#include <map>
-#include <mutex>
-#include <tuple>
-#include <vector>
 #include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
 #include "misc.h"
-#include "kernels.h"
 #include "periodic.cuh"
 
 namespace sphp {
@@ -37,6 +31,55 @@ namespace {
 
 constexpr int kThreads = 256;
 
+__device__ __forceinline__ int class_size(int k, int b) {
+  return k < 8 ? 1 : (k < 20 ? b : (k < 26 ? b * b : b * b * b));
+}
+// does class k's entity sit at x + 1 (the element's high-x side)?
+__device__ __forceinline__ int class_dx(int k) {
+  return k < 8    ? (k >> 2)
+         : k < 20 ? ((((k - 8) >> 2) != 0) ? ((k - 8) >> 1) & 1 : 0)  // edge off the x axis
+         : k < 26 ? ((((k - 20) >> 1) == 0) ? (k - 20) & 1 : 0)       // x-normal face
+                  : 0;
+}
+// class k's entity of element (x, y, z) is gid = R + size * vid(x + dx,
+// y + dy, z + dz) (periodic wrap): the closed form of entity_base
+// (periodic.cuh) that per-segment code evaluates with a few integer ops
+struct ClassGeom {
+  int R, s, d;  // region base, entity size, dx | dy << 1 | dz << 2
+};
+__device__ __forceinline__ ClassGeom class_geom(int k, int n, int P) {
+  const int N3 = n * n * n, b = P - 1;
+  if (k < 8) return {0, 1, ((k >> 2) & 1) | (((k >> 1) & 1) << 1) | ((k & 1) << 2)};
+  if (k < 20) {
+    const int j = k - 8, dir = j >> 2, s0 = (j >> 1) & 1, s1 = j & 1;
+    // the two shifts go to the axes other than dir, in order
+    const int d = dir == 0 ? (s0 << 1) | (s1 << 2) : (dir == 1 ? s0 | (s1 << 2) : s0 | (s1 << 1));
+    return {N3 + dir * N3 * b, b, d};
+  }
+  if (k < 26) {
+    const int j = k - 20, dir = j >> 1, side = j & 1;
+    return {N3 + 3 * N3 * b + dir * N3 * b * b, b * b, side << dir};
+  }
+  return {N3 * (1 + 3 * b + 3 * b * b), b * b * b, 0};
+}
+__device__ __forceinline__ int class_gid(const ClassGeom& g, int n, int x, int y, int z) {
+  x += g.d & 1;
+  y += (g.d >> 1) & 1;
+  z += (g.d >> 2) & 1;
+  x -= x >= n ? n : 0;
+  y -= y >= n ? n : 0;
+  z -= z >= n ? n : 0;
+  return g.R + g.s * (x + n * (y + n * z));
+}
+// owned classes of an element: vertex 0, edges 8/12/16, faces 20/22/24, interior 26
+__device__ __forceinline__ int owned_class(int c) {
+  return c == 0 ? 0 : (c < 4 ? 8 + 4 * (c - 1) : (c < 7 ? 20 + 2 * (c - 4) : 26));
+}
+__device__ __forceinline__ int owned_size(int c, int b) {
+  return c == 0 ? 1 : (c < 4 ? b : (c < 7 ? b * b : b * b * b));
+}
+// log2 of the number of elements contributing to a dof of owned class c
+__device__ __forceinline__ int owned_log(int c) { return c == 0 ? 3 : (c < 4 ? 2 : (c < 7 ? 1 : 0)); }
 
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -453,70 +496,6 @@ cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int ac
                                                                  row1 * segs);
     return cudaGetLastError();
   });
-}
-
-}  // namespace sphp
-
-// ---------------------------------------------------------------------------
-// Host helpers of the fused owner kernel (fused_owner.cuh)
-// ---------------------------------------------------------------------------
-namespace sphp {
-
-// owner segment length: largest of 32/16/8/4 dividing n (one warp sums a
-// segment; longer segments amortise the dependency waits)
-int fused_segment_length(int n) {
-  static const int force = env_int("SPHP_FUSED_L", 0);  // tuning override
-  if (force >= 4 && force <= 32 && n % force == 0) return force;
-  for (int L = 32; L >= 4; L /= 2)
-    if (n % L == 0) return L;
-  return 0;
-}
-
-namespace {
-std::mutex g_fused_mu;
-std::map<std::tuple<int, int, int, int>, std::pair<int*, int>> g_fused_queues;
-}  // namespace
-
-// owner segments sorted (stably) by the last K4 tile they read: the owner
-// warps then trail the tile frontier and read the local outputs from L2
-const int* fused_queue(int n, int ne, int L, int* nqueue) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lock(g_fused_mu);
-  auto key = std::make_tuple(dev, n, ne, L);
-  auto it = g_fused_queues.find(key);
-  if (it != g_fused_queues.end()) {
-    *nqueue = it->second.second;
-    return it->second.first;
-  }
-  const int segs = n / L;
-  const int64_t S = (int64_t)n * n * segs;
-  std::vector<std::pair<int64_t, int>> order;
-  order.reserve(S);
-  for (int64_t sg = 0; sg < S; ++sg) {
-    const int seg = (int)(sg % segs), row = (int)(sg / segs);
-    const int ey = row % n, ez = row / n, ex0 = seg * L;
-    int64_t maxdep = 0;
-    for (int q = 0; q < 4; ++q) {
-      int sy = ey - ((q >> 1) & 1), sz = ez - (q & 1);
-      sy += sy < 0 ? n : 0;
-      sz += sz < 0 ? n : 0;
-      const int64_t base = (int64_t)n * (sy + (int64_t)n * sz);
-      maxdep = std::max(maxdep, (base + ex0 + L - 1) / ne);
-      maxdep = std::max(maxdep, (base + (ex0 == 0 ? n - 1 : ex0 - 1)) / ne);
-    }
-    order.emplace_back(maxdep, (int)sg);
-  }
-  std::stable_sort(order.begin(), order.end(),
-                   [](const std::pair<int64_t, int>& a, const std::pair<int64_t, int>& b) { return a.first < b.first; });
-  std::vector<int> q(S);
-  for (int64_t i = 0; i < S; ++i) q[i] = order[i].second;
-  int* d = nullptr;
-  if (cudaMalloc(&d, sizeof(int) * (S ? S : 1)) != cudaSuccess) return nullptr;
-  if (S && cudaMemcpy(d, q.data(), sizeof(int) * S, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
-  g_fused_queues[key] = {d, (int)S};
-  *nqueue = (int)S;
-  return d;
 }
 
 }  // namespace sphp

@@ -31,10 +31,9 @@ def oracle_assembled(amap, oe_by_el, coeff_x, lam, G_by_el, wj_by_el):
 
 
 ALGS = ("owner", "colour", "split")
-PERIODIC_ALGS = ALGS + ("fused",)  # fused: periodic hex maps only
 
 
-@pytest.mark.parametrize("alg", PERIODIC_ALGS)
+@pytest.mark.parametrize("alg", ALGS)
 @pytest.mark.parametrize("P", [2, 3, 4, 5, 6, 7, 8])
 def test_periodic_hex_assembled(sp, P, alg):
     n = 4
@@ -57,28 +56,7 @@ def test_periodic_hex_assembled(sp, P, alg):
     assert y.tobytes() == y2.tobytes()
 
 
-@pytest.mark.parametrize("n,P", [(8, 2), (12, 3), (16, 4), (8, 5), (8, 6), (4, 7), (4, 8), (20, 4)])
-def test_fused_owner_bitwise_split(sp, n, P):
-    """FUSED (operator tiles + owner sums from one queue) sums in the split
-    algorithm's order: bitwise the same y, also when accumulating."""
-    exp = sp.make_hex(P, P + 2)
-    batch = sp.ElementBatch.structured(exp, n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE, amp=0.03)
-    coll = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC, lam=0.7)
-    split = sp.AssemblyMap.hex_periodic(n, P).set_algorithm("split")
-    fused = sp.AssemblyMap.hex_periodic(n, P).set_algorithm("fused")
-    assert fused.algorithm == "fused"
-    x = torch.as_tensor(np.random.default_rng(n * P).uniform(-1, 1, split.num_global), device="cuda")
-    ys = sp.GlobalHelmholtz([(coll, split)], split.num_global).apply(x)
-    opf = sp.GlobalHelmholtz([(coll, fused)], fused.num_global)
-    for _ in range(3):  # repeated launches reuse the queue and the flags
-        yf = opf.apply(x)
-        assert torch.equal(yf, ys)
-    # two batches on one map: the second accumulates into y
-    op2 = sp.GlobalHelmholtz([(coll, fused), (coll, fused)], fused.num_global)
-    assert torch.equal(op2.apply(x), ys + ys)
-
-
-@pytest.mark.parametrize("alg", ["split", "owner", "fused"])
+@pytest.mark.parametrize("alg", ["split", "owner"])
 @pytest.mark.parametrize("n,P", [(8, 2), (12, 3), (16, 4), (8, 5), (4, 8)])
 def test_host_buffer_apply_matches_device(sp, n, P, alg):
     """sphp_helmholtz_assembled_host (slab-pipelined copies on split maps)
@@ -98,7 +76,7 @@ def test_host_buffer_apply_matches_device(sp, n, P, alg):
         assert yp.numpy().tobytes() == ref.tobytes()
 
 
-@pytest.mark.parametrize("alg", PERIODIC_ALGS)
+@pytest.mark.parametrize("alg", ALGS)
 def test_scatter_assemble_duality(sp, alg):
     """<A x, v> == <x, A^T v> (test_assembly.py:120-129) on the device."""
     n, P = 4, 3
@@ -181,7 +159,7 @@ def test_hex_variable_order(sp, alg):
     assert_parity(y, ref, what="hex variable order")
 
 
-@pytest.mark.parametrize("alg", PERIODIC_ALGS)
+@pytest.mark.parametrize("alg", ALGS)
 def test_stdmat_assembled_matches_sumfac(sp, alg):
     n, P = 4, 2
     exp = sp.make_hex(P, P + 2)
@@ -232,7 +210,7 @@ def test_colour_vs_owner_large_mesh(sp, P):
     per = sp.AssemblyMap.hex_periodic(n, P)
     x = torch.as_tensor(np.random.default_rng(P).uniform(-1, 1, per.num_global), device="cuda")
     ys = {}
-    for alg in ("owner", "colour", "colour", "split", "fused"):
+    for alg in ("owner", "colour", "colour", "split"):
         per.set_algorithm(alg)
         y = sp.GlobalHelmholtz([(coll, per)], per.num_global).apply(x).cpu().numpy()
         if alg in ys:
@@ -240,7 +218,6 @@ def test_colour_vs_owner_large_mesh(sp, P):
         ys[alg] = y
     assert_parity(ys["colour"], ys["owner"], what=f"colour vs owner P{P} n{n}")
     assert_parity(ys["split"], ys["owner"], what=f"split vs owner P{P} n{n}")
-    assert ys["fused"].tobytes() == ys["split"].tobytes()
 
 
 def test_slab_operator_single_rank_gpu(sp):
