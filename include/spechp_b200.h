@@ -209,6 +209,18 @@ int sphp_helmholtz_assembled_host(sphp_coll* c, const sphp_amap* a,
                                   const double* x, double* y,
                                   sphp_stream stream);
 
+/* GlobalSystem over several per-order Helmholtz batches on explicit maps
+ * sharing one numbering (assembly.py:185-215 with per-order element groups,
+ * the variable-order configuration): per batch a scatter and the fused
+ * operator on one concatenated local block, then ONE owner-computes pass
+ * (fixed (batch, element, mode) order: deterministic).  The handle keeps
+ * the collections and maps by pointer: they must outlive it.             */
+typedef struct sphp_gsys sphp_gsys;
+int sphp_gsys_create(sphp_coll* const* colls, const sphp_amap* const* maps,
+                     int nbatch, int64_t num_global, sphp_gsys** out);
+int sphp_gsys_apply(sphp_gsys* g, const double* x, double* y, sphp_stream stream);
+int sphp_gsys_destroy(sphp_gsys* g);
+
 /* ---- solver support: GlobalSystem.diag / solve_pcg (assembly.py:185-266) -- */
 /* diagonal of every elemental Helmholtz matrix (E, nmodes) — assemble it
  * with sphp_assemble for the Jacobi preconditioner                          */

@@ -11,13 +11,19 @@
     excess modes pinned) and splits it into per-order batches.
 
 `scatter` / `assemble` mirror assembly.py:141-160; `GlobalHelmholtz.apply`
-is `GlobalSystem.apply` (assembly.py:177-182).  Two deterministic,
-atomic-free assembly algorithms (`AssemblyMap.set_algorithm`):
-  "owner"  (default) one kernel gathers x, applies the fused elemental
-           operator and writes the local block; a second sums every global
-           dof from its contributions in a fixed order (owner computes);
+is `GlobalSystem.apply` (assembly.py:177-182).  Deterministic, atomic-free
+assembly algorithms (`AssemblyMap.set_algorithm`):
+  "owner"  (default on explicit maps) one kernel gathers x, applies the
+           fused elemental operator and writes the local block; a second
+           sums every global dof from its contributions in a fixed order;
+  "split"  (default on periodic hex maps) scatter kernel -> fused operator
+           on the local block -> owner-computes sum;
   "colour" one fused gather -> operator -> scatter-add kernel per colour
            class, colours in a fixed order.
+Several per-order batches on explicit "owner" maps (the variable-order
+configuration) run as one C-ABI global system (`sphp_gsys_*`): a scatter and
+the fused operator per batch into one concatenated local block, then a
+single owner-computes pass over the global dofs.
 """
 from __future__ import annotations
 
@@ -62,6 +68,7 @@ class AssemblyMap:
                                            C.byref(nc)))
         self.num_elements, self.nmodes = ne.value, nm.value
         self.num_global, self.num_colours = ng.value, nc.value
+        self.periodic = False
 
     @property
     def algorithm(self):
@@ -97,7 +104,9 @@ class AssemblyMap:
         h = C.c_void_p()
         _lib.check(_lib.lib.sphp_amap_create_hex_periodic(int(n), int(P), C.byref(h)),
                    AssemblyError)
-        return cls(h)
+        m = cls(h)
+        m.periodic = True
+        return m
 
     def set_algorithm(self, alg):
         """'owner' (gather -> local -> owner-computes sum), 'split' (scatter
@@ -179,10 +188,32 @@ class GlobalHelmholtz:
         for coll, amap in self.batches:
             if amap.num_global != self.num_global:
                 raise AssemblyError("batches disagree on num_global")
+        self._gsys = None
+        if len(self.batches) > 1 and all(not a.periodic and a.algorithm == "owner"
+                                         for _, a in self.batches):
+            # several per-order batches on explicit maps: one C-ABI global
+            # system (concatenated local block, one owner-computes pass)
+            n = len(self.batches)
+            colls = (C.c_void_p * n)(*[c._handle for c, _ in self.batches])
+            maps = (C.c_void_p * n)(*[a._h for _, a in self.batches])
+            h = C.c_void_p()
+            _lib.check(_lib.lib.sphp_gsys_create(colls, maps, n, self.num_global, C.byref(h)),
+                       AssemblyError)
+            self._gsys = h
+
+    def __del__(self):
+        h = getattr(self, "_gsys", None)
+        if h and _lib is not None and _lib.lib is not None:
+            _lib.lib.sphp_gsys_destroy(h)
+            self._gsys = None
 
     def apply(self, x, out=None, stream=None):
         if out is None:
             out = torch.empty(self.num_global, dtype=torch.float64, device=x.device)
+        if self._gsys is not None:
+            _lib.check(_lib.lib.sphp_gsys_apply(self._gsys, _lib.ptr(x), _lib.ptr(out),
+                                                _lib.stream_ptr(stream)), AssemblyError)
+            return out
         for k, (coll, amap) in enumerate(self.batches):
             rc = _lib.lib.sphp_helmholtz_assembled(coll._handle, amap._h, _lib.ptr(x), _lib.ptr(out),
                                                    1 if k else 0, _lib.stream_ptr(stream))

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <memory>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -1471,6 +1472,108 @@ std::vector<int> host_slabs(int n) {
   }
   for (int t : tail) zb.push_back(zb.back() + t);
   return zb;
+}
+
+// ---------------------------------------------------------------------------
+// Global system over several per-order batches that share one numbering
+// (GlobalSystem with per-order element groups, assembly.py:185-215; the
+// variable-order configuration).  Per batch: scatter x into the batch's
+// slice of one concatenated local block, the fused operator on that slice
+// (block in / block out, the tuned local tile shapes); then ONE
+// owner-computes pass over the global dofs whose CSR entries index the
+// concatenated output block, in (batch, element, mode) order — instead of
+// one gathering launch plus one full-length owner pass per batch.
+// ---------------------------------------------------------------------------
+struct sphp_gsys {
+  std::vector<sphp_coll*> colls;
+  std::vector<const sphp_amap*> maps;
+  std::vector<int64_t> off;  // batch slice offsets (doubles, 16-byte aligned)
+  int64_t num_global = 0, total = 0;
+  DevBuf loc_x, loc_y, rowp, ent;
+};
+
+int sphp_gsys_create(sphp_coll* const* colls, const sphp_amap* const* maps, int nbatch, int64_t num_global,
+                     sphp_gsys** out) {
+  if (!out || !colls || !maps || nbatch < 1 || num_global < 0) return fail(SPHP_ERR_BAD_ARG, "bad arguments");
+  if (num_global > 2147483645LL) return fail(SPHP_ERR_UNSUPPORTED, "more than 2^31-3 global dofs");
+  auto g = std::make_unique<sphp_gsys>();
+  g->num_global = num_global;
+  int64_t acc = 0;
+  for (int b = 0; b < nbatch; ++b) {
+    sphp_coll* c = colls[b];
+    const sphp_amap* a = maps[b];
+    if (!c || !a) return fail(SPHP_ERR_BAD_ARG, "null batch");
+    if (c->op != SPHP_OP_HELMHOLTZ) return fail(SPHP_ERR_BAD_ARG, "collection is not a Helmholtz operator");
+    if (a->periodic) return fail(SPHP_ERR_UNSUPPORTED, "gsys batches take explicit maps");
+    if (a->E != c->E || a->nm != c->t->nm)
+      return fail(SPHP_ERR_BAD_SHAPE, "assembly map and collection disagree on (E, nmodes)");
+    if (a->num_global != num_global) return fail(SPHP_ERR_BAD_ARG, "batches disagree on num_global");
+    g->colls.push_back(c);
+    g->maps.push_back(a);
+    g->off.push_back(acc);
+    acc += (c->E * c->t->nm + 1) & ~(int64_t)1;
+  }
+  g->total = acc;
+  if (acc > 2147483647LL) return fail(SPHP_ERR_UNSUPPORTED, "more than 2^31-1 local entries");
+  // CSR over the global dofs: entries in (batch, element, mode) order
+  std::vector<int> rowp(num_global + 1, 0);
+  for (int b = 0; b < nbatch; ++b)
+    for (int64_t c : g->maps[b]->codes_host)
+      if (c != -1) rowp[(c >= 0 ? c : -c - 2) + 1]++;
+  for (int64_t i = 0; i < num_global; ++i) rowp[i + 1] += rowp[i];
+  std::vector<int> ent(rowp[num_global]);
+  std::vector<int> fill(rowp.begin(), rowp.end() - 1);
+  for (int b = 0; b < nbatch; ++b) {
+    const auto& codes = g->maps[b]->codes_host;
+    for (int64_t i = 0; i < (int64_t)codes.size(); ++i) {
+      const int64_t c = codes[i];
+      if (c == -1) continue;
+      const int64_t gid = c >= 0 ? c : -c - 2;
+      const int64_t idx = g->off[b] + i;
+      ent[fill[gid]++] = c >= 0 ? (int)idx : -(int)idx - 1;
+    }
+  }
+  for (int b = 0; b < nbatch; ++b)
+    if (int rc = amap_device(g->maps[b])) return rc;
+  CK(g->rowp.ensure(sizeof(int) * rowp.size()));
+  CK(cudaMemcpy(g->rowp.p, rowp.data(), sizeof(int) * rowp.size(), cudaMemcpyHostToDevice));
+  CK(g->ent.ensure(sizeof(int) * (ent.size() + 1)));
+  if (!ent.empty()) CK(cudaMemcpy(g->ent.p, ent.data(), sizeof(int) * ent.size(), cudaMemcpyHostToDevice));
+  CK(g->loc_x.ensure(sizeof(double) * (acc + 2)));
+  CK(g->loc_y.ensure(sizeof(double) * (acc + 2)));
+  *out = g.release();
+  return SPHP_OK;
+}
+
+int sphp_gsys_apply(sphp_gsys* g, const double* x, double* y, sphp_stream stream) {
+  if (!g || !x || !y) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  for (size_t b = 0; b < g->colls.size(); ++b) {
+    sphp_coll* c = g->colls[b];
+    const sphp_amap* a = g->maps[b];
+    double* lx = g->loc_x.as<double>() + g->off[b];
+    double* ly = g->loc_y.as<double>() + g->off[b];
+    CK(amap_scatter(a->dev(), x, lx, s));
+    if (c->strategy == SPHP_STRATEGY_CUDA_STDMAT) {
+      if (int rc = stdmat_prepare(c, s)) return rc;
+      CK(elem_matvec(c->E, (int)c->t->nm, c->helm_H.as<double>(), lx, ly, s));
+      continue;
+    }
+    OpArgs o = base_args(c);
+    o.in = lx;
+    o.out = ly;
+    o.mode = AsmMode::LOCAL;
+    cudaError_t e = sumfac_launch(c, o, s);
+    if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no kernel for this key");
+    if (e != cudaSuccess) return cuda_fail(e, "sphp_gsys_apply");
+  }
+  CK(owner_assemble_csr32(g->num_global, g->rowp.as<int>(), g->ent.as<int>(), g->loc_y.as<double>(), y, s));
+  return SPHP_OK;
+}
+
+int sphp_gsys_destroy(sphp_gsys* g) {
+  delete g;
+  return SPHP_OK;
 }
 
 // e2e path with HOST vectors: x (num_global) -> device, fused assembled

@@ -648,6 +648,28 @@ cudaError_t owner_assemble_periodic(int n, int P, const double* loc, double* y, 
   return cudaGetLastError();
 }
 
+// several batches: entries index the concatenation of the batches' local
+// blocks (int32 rows and entries); one pass over the global dofs
+__global__ void owner_csr32_kernel(int64_t ng, const int* __restrict__ rowp, const int* __restrict__ ent,
+                                   const double* __restrict__ loc, double* __restrict__ y) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  const int k0 = __ldg(rowp + g), k1 = __ldg(rowp + g + 1);
+  double acc = 0.0;
+  for (int k = k0; k < k1; ++k) {
+    const int c = __ldg(ent + k);
+    acc += c >= 0 ? __ldg(loc + c) : -__ldg(loc + (-(int64_t)c - 1));
+  }
+  y[g] = acc;
+}
+
+cudaError_t owner_assemble_csr32(int64_t ng, const int* rowp, const int* ent, const double* loc, double* y,
+                                 cudaStream_t s) {
+  if (ng == 0) return cudaSuccess;
+  owner_csr32_kernel<<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(ng, rowp, ent, loc, y);
+  return cudaGetLastError();
+}
+
 cudaError_t owner_assemble_csr(int64_t ng, const int64_t* rowp, const int* ent, const double* loc,
                                double* y, int accumulate, int nm, int64_t E, int mode_major,
                                cudaStream_t s) {

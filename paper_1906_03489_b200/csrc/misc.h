@@ -47,6 +47,8 @@ cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cuda
                                 int row0 = 0, int row1 = -1);
 cudaError_t periodic_entity_table(int n, int P, int* ent, cudaStream_t s);
 cudaError_t amap_scatter(const AmapDev& m, const double* g, double* loc, cudaStream_t s);
+cudaError_t owner_assemble_csr32(int64_t ng, const int* rowp, const int* ent, const double* loc, double* y,
+                                 cudaStream_t s);
 cudaError_t amap_assemble(const AmapDev& m, const double* loc, double* g, int ncolours,
                           const int* elist_dev, const int64_t* colour_off, int accumulate,
                           cudaStream_t s);
