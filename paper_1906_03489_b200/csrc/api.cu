@@ -1490,6 +1490,14 @@ struct sphp_gsys {
   std::vector<int64_t> off;  // batch slice offsets (doubles, 16-byte aligned)
   int64_t num_global = 0, total = 0;
   DevBuf loc_x, loc_y, rowp, ent;
+  // one stream per batch: the batches' scatter + operator launches overlap
+  // (each batch alone leaves the GPU half idle in its ramp and tail)
+  std::vector<cudaStream_t> bs;
+  std::vector<cudaEvent_t> ev;  // [0] start, [1 + b] batch b done
+  ~sphp_gsys() {
+    for (auto q : bs) cudaStreamDestroy(q);
+    for (auto e : ev) cudaEventDestroy(e);
+  }
 };
 
 int sphp_gsys_create(sphp_coll* const* colls, const sphp_amap* const* maps, int nbatch, int64_t num_global,
@@ -1541,33 +1549,48 @@ int sphp_gsys_create(sphp_coll* const* colls, const sphp_amap* const* maps, int 
   if (!ent.empty()) CK(cudaMemcpy(g->ent.p, ent.data(), sizeof(int) * ent.size(), cudaMemcpyHostToDevice));
   CK(g->loc_x.ensure(sizeof(double) * (acc + 2)));
   CK(g->loc_y.ensure(sizeof(double) * (acc + 2)));
+  for (int b = 0; b <= nbatch; ++b) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    g->ev.push_back(e);
+    if (b < nbatch) {
+      cudaStream_t q;
+      CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
+      g->bs.push_back(q);
+    }
+  }
   *out = g.release();
   return SPHP_OK;
 }
 
 int sphp_gsys_apply(sphp_gsys* g, const double* x, double* y, sphp_stream stream) {
   if (!g || !x || !y) return fail(SPHP_ERR_BAD_ARG, "null argument");
-  cudaStream_t s = (cudaStream_t)stream;
+  cudaStream_t s0 = (cudaStream_t)stream;
+  CK(cudaEventRecord(g->ev[0], s0));
   for (size_t b = 0; b < g->colls.size(); ++b) {
     sphp_coll* c = g->colls[b];
     const sphp_amap* a = g->maps[b];
     double* lx = g->loc_x.as<double>() + g->off[b];
     double* ly = g->loc_y.as<double>() + g->off[b];
+    cudaStream_t s = g->bs[b];
+    CK(cudaStreamWaitEvent(s, g->ev[0], 0));
     CK(amap_scatter(a->dev(), x, lx, s));
     if (c->strategy == SPHP_STRATEGY_CUDA_STDMAT) {
       if (int rc = stdmat_prepare(c, s)) return rc;
       CK(elem_matvec(c->E, (int)c->t->nm, c->helm_H.as<double>(), lx, ly, s));
-      continue;
+    } else {
+      OpArgs o = base_args(c);
+      o.in = lx;
+      o.out = ly;
+      o.mode = AsmMode::LOCAL;
+      cudaError_t e = sumfac_launch(c, o, s);
+      if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no kernel for this key");
+      if (e != cudaSuccess) return cuda_fail(e, "sphp_gsys_apply");
     }
-    OpArgs o = base_args(c);
-    o.in = lx;
-    o.out = ly;
-    o.mode = AsmMode::LOCAL;
-    cudaError_t e = sumfac_launch(c, o, s);
-    if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no kernel for this key");
-    if (e != cudaSuccess) return cuda_fail(e, "sphp_gsys_apply");
+    CK(cudaEventRecord(g->ev[1 + b], s));
+    CK(cudaStreamWaitEvent(s0, g->ev[1 + b], 0));
   }
-  CK(owner_assemble_csr32(g->num_global, g->rowp.as<int>(), g->ent.as<int>(), g->loc_y.as<double>(), y, s));
+  CK(owner_assemble_csr32(g->num_global, g->rowp.as<int>(), g->ent.as<int>(), g->loc_y.as<double>(), y, s0));
   return SPHP_OK;
 }
 
