@@ -100,7 +100,16 @@ struct Scaffold {
   static constexpr int GEO_T = NE * GEO_S;
   static constexpr int STAGE = IN_T + GEO_T;
   static constexpr int OUT_OFF = out_off_impl<Op>(0);
-  static constexpr int OUT_T = OUT_OFF >= 0 ? 0 : even_up(NE * Op::OUT);
+  // block-input (MODE 0) ops stream the output block back with one TMA bulk
+  // store per tile; the buffer is shifted by one double when the tile's
+  // global start is odd so both ends share 16-byte alignment (an Op staging
+  // it in its work area, OUT_OFF, leaves at least one spare double there)
+#ifndef SPHP_NO_BULK_OUT
+  static constexpr bool BULK_OUT = MODE == 0;
+#else
+  static constexpr bool BULK_OUT = false;  // tuning build: plain store loop
+#endif
+  static constexpr int OUT_T = OUT_OFF >= 0 ? 0 : even_up(NE * Op::OUT + (BULK_OUT ? 2 : 0));
   static constexpr int WORK_T = even_up(NE * Op::WORK);
   // assembled-mode integer tables (in doubles): per stage ids + entities,
   // current-tile copies, and the per-mode code table
@@ -329,6 +338,8 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
       for (int i = r * IN + tid; i < NE * IN; i += NT) in_s[(in_p - in_s) + i] = 0.0;
       if (GEO > 0)
         for (int i = r * GEO_S + tid; i < NE * GEO_S; i += NT) geo_s[i] = 0.0;
+      // the previous tile's bulk store must have read the output buffer
+      if (S::BULK_OUT && tid == 0) bulk_wait_read0();
     } else {
       cp_async_wait<NST - 1>();
       if (GEO > 0) {
@@ -363,11 +374,29 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
       }
     };
     auto pre_out = [&]() {};
-    Op::compute(in_p, geo_s, work, out_s, a.lam, release, pre_out, c_tab);
+    const bool bulk_out = S::BULK_OUT && a.use_tma && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0;
+    // out_t + i and a.out + w0 * OUT + i agree mod 16 bytes (the buffer
+    // starts OUT_OFF doubles into the 16-byte aligned work area)
+    const int head = bulk_out ? (int)((w0 * OUT) & 1) : 0;
+    const int sh = bulk_out ? (head + (S::OUT_OFF > 0 ? S::OUT_OFF : 0)) & 1 : 0;
+    double* out_t = out_s + sh;
+    Op::compute(in_p, geo_s, work, out_t, a.lam, release, pre_out, c_tab);
+    if (bulk_out) fence_proxy_async();  // this thread's buffer writes -> async proxy
     __syncthreads();
 
     // ---- write back ------------------------------------------------------
-    if (!MT::SCATTER) {
+    if (bulk_out) {
+      const int n = r * OUT, body = (n - head) & ~1;
+      double* dst = a.out + w0 * OUT;
+      if (tid == 0) {
+        if (body > 0) {
+          bulk_s2g(dst + head, out_t + head, (uint32_t)(sizeof(double) * body));
+          bulk_commit();
+        }
+        if (head) dst[0] = out_t[0];
+      }
+      if (tid == NT - 1 && head + body < n) dst[n - 1] = out_t[n - 1];
+    } else if (!MT::SCATTER) {
       // element-major local block (a mode-major layout, coalesced for the
       // owner-computes sum, measured slower overall: profiles/r01_bench_*.log)
       for (int i = tid; i < r * OUT; i += NT) a.out[w0 * OUT + i] = out_s[i];
@@ -410,6 +439,7 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     }
   }
   if (MODE != 0) cp_async_wait<0>();
+  if (S::BULK_OUT && tid == 0) bulk_wait0();
 }
 
 }  // namespace sphp
