@@ -62,6 +62,92 @@ __device__ __forceinline__ void store_row(double* __restrict__ p, const double* 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Element-block rows (M contiguous doubles, one lane per row R of the tile):
+// lane R hits bank R*M + r.  For even M consecutive rows share banks (4-way
+// at M = 4, 8-way at M = 8 in the Helmholtz S1/S9 stages).  Reading /
+// writing the row in the order r = (it + s) mod M with s = (R / PER) & MASK,
+// PER = 16 / gcd(M, 16), makes the 16 lanes of a half-warp distinct; the
+// registers are put back in order by log2(MASK + 1) conditional rotations.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int gcd16(int m) { return (m % 16 == 0) ? 16 : (m % 8 == 0) ? 8 : (m % 4 == 0) ? 4 : (m % 2 == 0) ? 2 : 1; }
+template <int M>
+struct RowRot {
+  static constexpr int PER = 16 / gcd16(M);
+  static constexpr int NV = 16 / PER;  // distinct rotations needed in a half-warp
+  static constexpr int MASK = NV - 1;  // NV is 1, 2, 4, 8 or 16 (<= M for M in 2..10)
+  __device__ static __forceinline__ int shift(int R) { return (R / PER) & MASK; }
+  // y[r] = x[(r + SH) % M] where the bit is set
+  template <int SH>
+  __device__ static __forceinline__ void rotl_if(double* x, bool c) {
+    double t[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) t[r] = x[(r + SH) % M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) x[r] = c ? t[r] : x[r];
+  }
+  // x <- rotate left by s (x[r] = old[(r + s) % M]), s in [0, NV)
+  __device__ static __forceinline__ void rotl(double* x, int s) {
+    if constexpr (NV > 1) rotl_if<1 % M>(x, s & 1);
+    if constexpr (NV > 2) rotl_if<2 % M>(x, s & 2);
+    if constexpr (NV > 4) rotl_if<4 % M>(x, s & 4);
+    if constexpr (NV > 8) rotl_if<8 % M>(x, s & 8);
+  }
+  template <int SH>
+  __device__ static __forceinline__ void rotr_if(double* x, bool c) {
+    double t[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) t[r] = x[(r - SH % M + M) % M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) x[r] = c ? t[r] : x[r];
+  }
+  __device__ static __forceinline__ void rotr(double* x, int s) {
+    if constexpr (NV > 1) rotr_if<1>(x, s & 1);
+    if constexpr (NV > 2) rotr_if<2>(x, s & 2);
+    if constexpr (NV > 4) rotr_if<4>(x, s & 4);
+    if constexpr (NV > 8) rotr_if<8>(x, s & 8);
+  }
+  // p[(it + s) % M] = c[(it + s) % M]: stores in rotated order
+  __device__ static __forceinline__ void store(double* __restrict__ p, int R, const double* c) {
+    if constexpr (NV == 1) {
+#pragma unroll
+      for (int r = 0; r < M; ++r) p[r] = c[r];
+    } else {
+      const int s = shift(R);
+      double cr[M];
+#pragma unroll
+      for (int r = 0; r < M; ++r) cr[r] = c[r];
+      rotl(cr, s);  // cr[it] = c[(it + s) % M]
+#pragma unroll
+      for (int it = 0; it < M; ++it) {
+        int r = it + s;
+        r -= r >= M ? M : 0;
+        p[r] = cr[it];
+      }
+    }
+  }
+  __device__ static __forceinline__ void load(const double* __restrict__ p, int R, double* x) {
+    if constexpr (NV == 1) {
+#pragma unroll
+      for (int r = 0; r < M; ++r) x[r] = p[r];
+    } else {
+      const int s = shift(R);
+      double xr[M];
+#pragma unroll
+      for (int it = 0; it < M; ++it) {
+        int r = it + s;
+        r -= r >= M ? M : 0;
+        xr[it] = p[r];  // xr[it] = x[(it + s) % M]
+      }
+      // x[r] = xr[(r - s) mod M]: undo the left rotation by s
+      rotr(xr, s);
+#pragma unroll
+      for (int r = 0; r < M; ++r) x[r] = xr[r];
+    }
+  }
+};
+
 // ===========================================================================
 // Fused matrix-free Helmholtz (K4): y = sum_ab B_a^T G_ab B_b uhat + lam B^T wJ B uhat
 // (geometry.py:171-184 as one sum-factorised pass; no quadrature data
@@ -478,9 +564,15 @@ struct HexHelmEO {
   static constexpr int CS = pt_stride(Q3);
   static constexpr int GEO = (GK == SPHP_GEOM_METRIC) ? 7 * CS : 10;
   static constexpr int QK = odd_up(Q);
-  static constexpr int PP1 = pitch_mod16(M * QK, Q);
+  // pitches: the mod-16 rule below, except where the wavefront model's
+  // search (tools/layout_search_eo.py, odd Q with the RowRot S1/S9 rows)
+  // found fewer shared-memory wavefronts: P=3 -14 %, P=5 -6 %
+  static constexpr int PP1 = (M == 4 && Q == 5) ? 28 : (M == 6 && Q == 7) ? 42 : pitch_mod16(M * QK, Q);
   static constexpr int PP2 = pitch_mod16(Q * Q, Q);
-  static constexpr int SE = even_up(cmax(Q3, cmax(M * PP1, M * PP2)));
+  static constexpr int SE = (M == 4 && Q == 5) ? 157 : (M == 6 && Q == 7) ? 343
+                                                     : even_up(cmax(Q3, cmax(M * PP1, M * PP2)));
+  static_assert(SE >= Q3 && SE >= M * PP1 && SE >= M * PP2, "element tensors overlap");
+  static_assert(Q % 2 == 1 || SE % 2 == 0, "128-bit rows need an even element stride");
   static constexpr int WORK = 3 * SE;
   static constexpr int OUT_OFF = NE * SE;  // S9 writes the block into W1 (free after S8)
   using T = Tab<M, Q>;
@@ -497,7 +589,7 @@ struct HexHelmEO {
     SPHP_FOR_ITEMS(NE * M * M, w) {
       int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
       double x[M], u[Q];
-      ld_pencil<M, 1>(cin + e * M3 + pq * M, x);
+      RowRot<M>::load(cin + e * M3 + pq * M, w, x);
       X::interp(tab, x, u);
       st_pencil<Q, 1>(W0 + e * SE + p * PP1 + q * QK, u);
     }
@@ -637,7 +729,7 @@ struct HexHelmEO {
       double v[Q], c[M];
       ld_pencil<Q, 1>(W0 + e * SE + p * PP1 + q * QK, v);
       X::project(tab, v, c);
-      st_pencil<M, 1>(out + e * M3 + pq * M, c);
+      RowRot<M>::store(out + e * M3 + pq * M, w, c);
     }
   }
 };
