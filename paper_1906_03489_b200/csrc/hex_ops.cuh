@@ -148,6 +148,54 @@ struct RowRot {
   }
 };
 
+
+// Pencils of N values at stride S (one lane per pencil) accessed in the
+// rotated order n = (it + tau) mod N, tau in [0, N) per lane: spreads lanes
+// whose pencils start on the same bank pair (the j-pencil stages at Q = 7,
+// where lane (i, k) starts on bank i + k); registers are put back in order
+// by ceil(log2 N) conditional rotations.
+template <int N>
+struct Rot {
+  template <int SH, bool LEFT>
+  __device__ static __forceinline__ void rot_if(double* x, bool c) {
+    double t[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) t[r] = LEFT ? x[(r + SH) % N] : x[(r - SH % N + N) % N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) x[r] = c ? t[r] : x[r];
+  }
+  template <bool LEFT>
+  __device__ static __forceinline__ void rot(double* x, int s) {
+    if constexpr (N > 1) rot_if<1, LEFT>(x, s & 1);
+    if constexpr (N > 2) rot_if<2, LEFT>(x, s & 2);
+    if constexpr (N > 4) rot_if<4, LEFT>(x, s & 4);
+    if constexpr (N > 8) rot_if<8, LEFT>(x, s & 8);
+  }
+  template <int S>
+  __device__ static __forceinline__ void load(const double* __restrict__ p, int tau, double* x) {
+#pragma unroll
+    for (int it = 0; it < N; ++it) {
+      int n = it + tau;
+      n -= n >= N ? N : 0;
+      x[it] = p[n * S];
+    }
+    rot<false>(x, tau);  // x[n] = loaded[(n - tau) mod N]
+  }
+  template <int S>
+  __device__ static __forceinline__ void store(double* __restrict__ p, int tau, const double* x) {
+    double xr[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) xr[n] = x[n];
+    rot<true>(xr, tau);  // xr[it] = x[(it + tau) % N]
+#pragma unroll
+    for (int it = 0; it < N; ++it) {
+      int n = it + tau;
+      n -= n >= N ? N : 0;
+      p[n * S] = xr[it];
+    }
+  }
+};
+
 // ===========================================================================
 // Fused matrix-free Helmholtz (K4): y = sum_ab B_a^T G_ab B_b uhat + lam B^T wJ B uhat
 // (geometry.py:171-184 as one sum-factorised pass; no quadrature data
@@ -575,6 +623,9 @@ struct HexHelmEO {
   static_assert(Q % 2 == 1 || SE % 2 == 0, "128-bit rows need an even element stride");
   static constexpr int WORK = 3 * SE;
   static constexpr int OUT_OFF = NE * SE;  // S9 writes the block into W1 (free after S8)
+  // j-pencil stages S4/S6 in rotated order tau = i at Q = 7 (model: 2.71x ->
+  // 1.84x of the ideal wavefronts there); a no-op rotation elsewhere
+  static constexpr bool JROT = (Q == 7);
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
 
@@ -617,9 +668,10 @@ struct HexHelmEO {
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
       double v[Q], r[Q];
-      ld_pencil<Q, Q>(W0 + e * SE + i * Q * Q + k, v);
+      const int tau = JROT ? i : 0;
+      Rot<Q>::template load<Q>(W0 + e * SE + i * Q * Q + k, tau, v);
       X::template deriv<false, false>(tab, v, r);
-      st_pencil<Q, Q>(W1 + e * SE + i * Q * Q + k, r);
+      Rot<Q>::template store<Q>(W1 + e * SE + i * Q * Q + k, tau, r);
     }
     __syncthreads();
     // S5: k rows
@@ -697,10 +749,11 @@ struct HexHelmEO {
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
       double f[Q], t[Q];
-      ld_pencil<Q, Q>(W1 + e * SE + i * Q * Q + k, f);
-      ld_pencil<Q, Q>(W0 + e * SE + i * Q * Q + k, t);
+      const int tau = JROT ? i : 0;
+      Rot<Q>::template load<Q>(W1 + e * SE + i * Q * Q + k, tau, f);
+      Rot<Q>::template load<Q>(W0 + e * SE + i * Q * Q + k, tau, t);
       X::template deriv<true, true>(tab, f, t);
-      st_pencil<Q, Q>(W0 + e * SE + i * Q * Q + k, t);
+      Rot<Q>::template store<Q>(W0 + e * SE + i * Q * Q + k, tau, t);
     }
     __syncthreads();
     // S7: i -> p, B t + dB f0
