@@ -1268,6 +1268,14 @@ int sphp_assemble(const sphp_amap* a, const double* loc, double* g, sphp_stream 
   return amap_assemble_any(a, loc, g, 0, (cudaStream_t)stream);
 }
 
+static int split_reverse() {
+  static const int v = [] {
+    const char* e = getenv("SPHP_SPLIT_REVERSE");  // tuning override
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 // assembly.GlobalSystem.apply (assembly.py:177-182), fused
 int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, double* y, int accumulate,
                              sphp_stream stream) {
@@ -1300,6 +1308,10 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
     o.in = c->loc_x.as<double>();
     o.out = c->loc_y.as<double>();
     o.mode = AsmMode::LOCAL;
+    // the operator walks the elements backwards: it starts on the block the
+    // scatter wrote last and ends on the elements the owner sum reads first,
+    // both still in L2
+    o.reverse = split_reverse();
     cudaError_t e = sumfac_launch(c, o, s);
     if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no kernel for this key");
     if (e != cudaSuccess) return cuda_fail(e, "sphp_helmholtz_assembled");

@@ -33,6 +33,7 @@ struct OpArgs {
   const int* ent_g;   // PERIODIC_GATHER: precomputed (E, 27) entity bases (optional)
   int n;              // PERIODIC: grid size
   int colour;         // PERIODIC: colour id 0..7
+  int reverse = 0;    // LOCAL: walk the tiles last to first
 };
 
 // hex (3D) sum-factorisation kernels

@@ -76,6 +76,7 @@ cudaError_t launch_pipe(const OpArgs& oa, int64_t gstride, int64_t goff, cudaStr
   a.ent_g = oa.ent_g;
   a.n = oa.n;
   a.colour = oa.colour;
+  a.reverse = oa.reverse;
   const int64_t count = (MODE == 0 || MODE >= 3) ? oa.E : oa.nlist;
   if (count <= 0) return cudaSuccess;
   const int64_t ntiles = (count + Op::NE - 1) / Op::NE;

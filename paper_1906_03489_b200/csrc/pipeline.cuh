@@ -45,6 +45,7 @@ struct DevArgs {
   const int* ent_g;  // PERIODIC_GATHER: precomputed (E, 27) entity bases, or null
   int n;
   int colour;
+  int reverse;  // MODE 0: walk the tiles last to first (L2 reuse, see launch)
 };
 
 
@@ -169,9 +170,12 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     return a.use_tma && a1 <= in_total;
   };
 
-  // thread 0: TMA bulk copies of tile t into stage s (local mode)
-  auto issue_local = [&](int t, int s) {
-    if (t >= ntiles) return;
+  // schedule slot -> tile (MODE 0 may walk the tiles in reverse)
+  auto phys = [&](int ts) { return (MODE == 0 && a.reverse) ? ntiles - 1 - ts : ts; };
+  // thread 0: TMA bulk copies of the tile of schedule slot ts into stage s
+  auto issue_local = [&](int ts, int s) {
+    if (ts >= ntiles) return;
+    const int t = phys(ts);
     double* in_s = stage_base + s * S::STAGE;
     double* geo_s = in_s + S::IN_T;
     const int64_t w0 = (int64_t)t * NE;
@@ -309,7 +313,8 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
   }
 
   int it = 0;
-  for (int t = blockIdx.x; t < ntiles; t += G, ++it) {
+  for (int ts = blockIdx.x; ts < ntiles; ts += G, ++it) {
+    const int t = phys(ts);
     const int s = (NST == 2) ? (it & 1) : 0;
     double* in_s = stage_base + s * S::STAGE;
     double* geo_s = in_s + S::IN_T;
@@ -367,10 +372,10 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
       if (MODE == 0) {
         if (tid == 0) {
           fence_proxy_async();
-          issue_local(t + NST * G, s);
+          issue_local(ts + NST * G, s);
         }
       } else {
-        issue_asm(t + NST * G, s);
+        issue_asm(ts + NST * G, s);
       }
     };
     auto pre_out = [&]() {};
