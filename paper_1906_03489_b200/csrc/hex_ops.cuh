@@ -623,9 +623,12 @@ struct HexHelmEO {
   static_assert(Q % 2 == 1 || SE % 2 == 0, "128-bit rows need an even element stride");
   static constexpr int WORK = 3 * SE;
   static constexpr int OUT_OFF = NE * SE;  // S9 writes the block into W1 (free after S8)
-  // j-pencil stages S4/S6 in rotated order tau = i at Q = 7 (model: 2.71x ->
-  // 1.84x of the ideal wavefronts there); a no-op rotation elsewhere
-  static constexpr bool JROT = (Q == 7);
+  // j-pencil stages S4/S6 in rotated order tau = JROT * i mod Q at Q = 7
+  // (wavefront model tools/bank_sim.py: 2.71x -> 1.84x of the ideal there;
+  // measured P=5 -1 %).  Also modelled better but measured no gain at Q = 6
+  // and slower at Q = 10 (P=8 3.34 -> 3.66 ms: the rotation selects cost
+  // more than the conflicts): natural order there.
+  static constexpr int JROT = (Q == 7) ? 1 : 0;
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
 
@@ -668,7 +671,7 @@ struct HexHelmEO {
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
       double v[Q], r[Q];
-      const int tau = JROT ? i : 0;
+      const int tau = (JROT * i) % Q;
       Rot<Q>::template load<Q>(W0 + e * SE + i * Q * Q + k, tau, v);
       X::template deriv<false, false>(tab, v, r);
       Rot<Q>::template store<Q>(W1 + e * SE + i * Q * Q + k, tau, r);
@@ -749,7 +752,7 @@ struct HexHelmEO {
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
       double f[Q], t[Q];
-      const int tau = JROT ? i : 0;
+      const int tau = (JROT * i) % Q;
       Rot<Q>::template load<Q>(W1 + e * SE + i * Q * Q + k, tau, f);
       Rot<Q>::template load<Q>(W0 + e * SE + i * Q * Q + k, tau, t);
       X::template deriv<true, true>(tab, f, t);
