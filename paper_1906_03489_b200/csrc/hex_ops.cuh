@@ -617,9 +617,15 @@ struct HexHelmEO {
   // found fewer shared-memory wavefronts: P=3 -14 %, P=5 -6 %
   static constexpr int PP1 = (M == 4 && Q == 5) ? 28 : (M == 6 && Q == 7) ? 42 : pitch_mod16(M * QK, Q);
   static constexpr int PP2 = pitch_mod16(Q * Q, Q);
+  // plane pitch of the dense (i, j, k) work tensors: Q^2 (contiguous), except
+  // Q = 10 where Q^2 = 4 mod 16 puts the j-pencil lanes (i, k) on banks 4i + k
+  // (ncu P=8: 105 M of 144 M excess wavefronts); SI = 10 mod 16 makes them
+  // consecutive while the 128-bit k-rows stay conflict free but for the
+  // phases that cross an i
+  static constexpr int SI = (Q == 10) ? pitch_mod16(Q * Q, Q) : Q * Q;
   static constexpr int SE = (M == 4 && Q == 5) ? 157 : (M == 6 && Q == 7) ? 343
-                                                     : even_up(cmax(Q3, cmax(M * PP1, M * PP2)));
-  static_assert(SE >= Q3 && SE >= M * PP1 && SE >= M * PP2, "element tensors overlap");
+                                                     : even_up(cmax(Q * SI, cmax(M * PP1, M * PP2)));
+  static_assert(SE >= Q * SI && SE >= M * PP1 && SE >= M * PP2, "element tensors overlap");
   static_assert(Q % 2 == 1 || SE % 2 == 0, "128-bit rows need an even element stride");
   static constexpr int WORK = 3 * SE;
   static constexpr int OUT_OFF = NE * SE;  // S9 writes the block into W1 (free after S8)
@@ -663,8 +669,8 @@ struct HexHelmEO {
       double x[M], u[Q], d[Q];
       ld_pencil<M, PP2>(W1 + e * SE + jk, x);
       X::interp_and_deriv(tab, x, u, d);
-      st_pencil<Q, Q * Q>(W0 + e * SE + jk, u);
-      st_pencil<Q, Q * Q>(W2 + e * SE + jk, d);
+      st_pencil<Q, SI>(W0 + e * SE + jk, u);
+      st_pencil<Q, SI>(W2 + e * SE + jk, d);
     }
     __syncthreads();
     // S4: d1 = D along j
@@ -672,15 +678,15 @@ struct HexHelmEO {
       int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
       double v[Q], r[Q];
       const int tau = (JROT * i) % Q;
-      Rot<Q>::template load<Q>(W0 + e * SE + i * Q * Q + k, tau, v);
+      Rot<Q>::template load<Q>(W0 + e * SE + i * SI + k, tau, v);
       X::template deriv<false, false>(tab, v, r);
-      Rot<Q>::template store<Q>(W1 + e * SE + i * Q * Q + k, tau, r);
+      Rot<Q>::template store<Q>(W1 + e * SE + i * SI + k, tau, r);
     }
     __syncthreads();
     // S5: k rows
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), ij = w - e * (Q * Q), i = ij / Q, j = ij - i * Q;
-      const int row = e * SE + ij * Q;
+      const int row = e * SE + i * SI + j * Q;
       double u[Q], d[Q], f0[Q], f1[Q], f2[Q], g[Q], d2[Q];
       load_row<Q>(W0 + row, u);
       X::template deriv<false, false>(tab, u, d2);
@@ -753,18 +759,18 @@ struct HexHelmEO {
       int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
       double f[Q], t[Q];
       const int tau = (JROT * i) % Q;
-      Rot<Q>::template load<Q>(W1 + e * SE + i * Q * Q + k, tau, f);
-      Rot<Q>::template load<Q>(W0 + e * SE + i * Q * Q + k, tau, t);
+      Rot<Q>::template load<Q>(W1 + e * SE + i * SI + k, tau, f);
+      Rot<Q>::template load<Q>(W0 + e * SE + i * SI + k, tau, t);
       X::template deriv<true, true>(tab, f, t);
-      Rot<Q>::template store<Q>(W0 + e * SE + i * Q * Q + k, tau, t);
+      Rot<Q>::template store<Q>(W0 + e * SE + i * SI + k, tau, t);
     }
     __syncthreads();
     // S7: i -> p, B t + dB f0
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), jk = w - e * (Q * Q);
       double t[Q], f0[Q], c[M];
-      ld_pencil<Q, Q * Q>(W0 + e * SE + jk, t);
-      ld_pencil<Q, Q * Q>(W2 + e * SE + jk, f0);
+      ld_pencil<Q, SI>(W0 + e * SE + jk, t);
+      ld_pencil<Q, SI>(W2 + e * SE + jk, f0);
       X::project2(tab, t, f0, c);
       st_pencil<M, PP2>(W1 + e * SE + jk, c);
     }
