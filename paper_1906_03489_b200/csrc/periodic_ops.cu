@@ -259,16 +259,21 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) periodic_scatter_v2_
 #pragma unroll
     for (int u = 0; u < U; ++u) blk[d[u]] = v[u];
     grab(blockIdx.x + k * gridDim.x, buf ^ 1);
-    __syncthreads();  // block complete, next bases visible
+    fence_proxy_async();  // this thread's block writes -> the bulk copy
+    __syncthreads();      // block complete, next bases visible
     const int nxt = ids[buf ^ 1];
     issue(nxt, buf ^ 1);  // next segment's loads overlap the write-out
-    // L * nm is even and the block start is 16-byte aligned (L % 4 == 0)
-    double2* out = reinterpret_cast<double2*>(loc + (size_t)cur * total);
-    const double2* src = reinterpret_cast<const double2*>(blk);
-    for (int i = threadIdx.x; i < total / 2; i += kThreads) out[i] = src[i];
+    // one TMA bulk store of the block (L * nm is even and the block start
+    // 16-byte aligned, L % 4 == 0); the threads only wait for its reads
+    if (threadIdx.x == 0) {
+      bulk_s2g(loc + (size_t)cur * total, blk, (uint32_t)(sizeof(double) * total));
+      bulk_commit();
+      bulk_wait_read0();
+    }
     __syncthreads();  // block consumed
     cur = nxt;
   }
+  if (threadIdx.x == 0) bulk_wait0();
 }
 
 // per-thread register batch: U * kThreads >= L * nm
