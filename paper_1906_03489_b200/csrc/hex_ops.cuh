@@ -1210,7 +1210,11 @@ struct HexBwd {
   static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
   static constexpr int IN = M3, OUT = Q3, GEO = 0;
   static constexpr int QK = odd_up(Q);
-  static constexpr int SA = odd_up(M * M * QK), SB = odd_up(M * Q * QK);
+  // B[p][j][k]: contiguous rows, plane pitch = Q (mod 16) so the (p, k)
+  // lanes of the j-stage hit consecutive banks (wavefront model,
+  // tools/layout_search_bwd.py: -18 % at P=4 and fewer at every fast key)
+  static constexpr int PB = pitch_mod16(Q * Q, Q);
+  static constexpr int SA = odd_up(M * M * QK), SB = M * PB;
   static constexpr int WORK = SA + SB;
   using T = Tab<M, Q>;
 
@@ -1228,15 +1232,13 @@ struct HexBwd {
     release();
     SPHP_FOR_ITEMS(NE * M * Q, w) {
       int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
-      eo_interp<M, Q, QK, QK>(tab, A + e * SA + p * M * QK + k,
-                                              Bb + e * SB + p * Q * QK + k);
+      eo_interp<M, Q, QK, Q>(tab, A + e * SA + p * M * QK + k, Bb + e * SB + p * PB + k);
     }
     pre_out();
     __syncthreads();
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
-      eo_interp<M, Q, Q * QK, Q * Q>(tab, Bb + e * SB + j * QK + k,
-                                                     out + e * Q3 + j * Q + k);
+      eo_interp<M, Q, PB, Q * Q>(tab, Bb + e * SB + j * Q + k, out + e * Q3 + j * Q + k);
     }
   }
 };
@@ -1253,7 +1255,9 @@ struct HexIprod {
   static constexpr int CS = pt_stride(Q3);
   static constexpr int GEO = (GK == SPHP_GEOM_POINT) ? CS : (GK == SPHP_GEOM_AFFINE ? 10 : 0);
   static constexpr int QK = odd_up(Q);
-  static constexpr int SA = odd_up(M * M * QK), SB = odd_up(M * Q * QK);
+  // B[p][j][k] as in HexBwd: contiguous rows, plane pitch = Q (mod 16)
+  static constexpr int PB = pitch_mod16(Q * Q, Q);
+  static constexpr int SA = odd_up(M * M * QK), SB = M * PB;
   static constexpr int WORK = SA + SB;
   using T = Tab<M, Q>;
 
@@ -1284,15 +1288,14 @@ struct HexIprod {
         double acc = 0.0;
 #pragma unroll
         for (int i = 0; i < Q; ++i) acc = fma(tab[T::B + p * Q + i], x[i], acc);
-        Bb[e * SB + (p * Q + j) * QK + k] = acc;
+        Bb[e * SB + p * PB + j * Q + k] = acc;
       }
     }
     __syncthreads();
     release();
     SPHP_FOR_ITEMS(NE * M * Q, w) {
       int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
-      eo_project<M, Q, QK, QK>(tab, Bb + e * SB + p * Q * QK + k,
-                                              A + e * SA + p * M * QK + k);
+      eo_project<M, Q, Q, QK>(tab, Bb + e * SB + p * PB + k, A + e * SA + p * M * QK + k);
     }
     pre_out();
     __syncthreads();
