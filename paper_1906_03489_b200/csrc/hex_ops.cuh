@@ -1321,6 +1321,7 @@ struct HexPhysDeriv {
   static constexpr int QK = odd_up(Q);
   static constexpr int SW = odd_up(Q * Q * QK);
   static constexpr int WORK = 2 * SW;
+  static constexpr bool ROWROT = (Q % 4 == 0);
   using T = Tab<M, Q>;
 
   template <class R, class W>
@@ -1347,9 +1348,16 @@ struct HexPhysDeriv {
     // pencil along k: d2 in registers, metric transform, write 3 comps
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), ij = w - e * (Q * Q), i = ij / Q, j = ij - i * Q;
-      double x[Q];
+      double x[Q], r0[Q], r1[Q], r2[Q];
+      // rows of Q doubles one lane each: rotated order (RowRot) when Q = 0
+      // mod 4 (4-8-way conflicts otherwise; P=6: 908 -> 697 us); at Q = 2
+      // mod 4 the 2-way conflicts cost less than the rotation (measured)
+      if constexpr (ROWROT) {
+        RowRot<Q>::load(uin + e * Q3 + ij * Q, w, x);
+      } else {
 #pragma unroll
-      for (int k = 0; k < Q; ++k) x[k] = uin[e * Q3 + ij * Q + k];
+        for (int k = 0; k < Q; ++k) x[k] = uin[e * Q3 + ij * Q + k];
+      }
       const double* g = geo + e * GEO;
 #pragma unroll
       for (int k = 0; k < Q; ++k) {
@@ -1369,9 +1377,22 @@ struct HexPhysDeriv {
           o1 = iv[1] * d0 + iv[4] * d1 + iv[7] * d2;
           o2 = iv[2] * d0 + iv[5] * d1 + iv[8] * d2;
         }
-        out[e * OUT + 0 * Q3 + pt] = o0;
-        out[e * OUT + 1 * Q3 + pt] = o1;
-        out[e * OUT + 2 * Q3 + pt] = o2;
+        r0[k] = o0;
+        r1[k] = o1;
+        r2[k] = o2;
+      }
+      const int row = e * 3 * Q * Q + ij;  // row index of component 0 in the output block
+      if constexpr (ROWROT) {
+        RowRot<Q>::store(out + e * OUT + 0 * Q3 + ij * Q, row, r0);
+        RowRot<Q>::store(out + e * OUT + 1 * Q3 + ij * Q, row + Q * Q, r1);
+        RowRot<Q>::store(out + e * OUT + 2 * Q3 + ij * Q, row + 2 * Q * Q, r2);
+      } else {
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          out[e * OUT + 0 * Q3 + ij * Q + k] = r0[k];
+          out[e * OUT + 1 * Q3 + ij * Q + k] = r1[k];
+          out[e * OUT + 2 * Q3 + ij * Q + k] = r2[k];
+        }
       }
     }
     __syncthreads();
