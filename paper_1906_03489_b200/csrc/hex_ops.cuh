@@ -1428,11 +1428,26 @@ struct HexIPDeriv {
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), ij = w - e * (Q * Q), i = ij / Q, j = ij - i * Q;
       const double* g = geo + e * GEO;
-      double g2[Q];
+      double g2[Q], rx[Q], ry[Q], rz[Q];
+      // the three input rows, in rotated order when Q = 0 mod 4 (RowRot;
+      // see HexPhysDeriv)
+      if constexpr (Q % 4 == 0) {
+        const int row = e * 3 * Q * Q + ij;
+        RowRot<Q>::load(fin + e * IN + ij * Q, row, rx);
+        RowRot<Q>::load(fin + e * IN + Q3 + ij * Q, row + Q * Q, ry);
+        RowRot<Q>::load(fin + e * IN + 2 * Q3 + ij * Q, row + 2 * Q * Q, rz);
+      } else {
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          rx[k] = fin[e * IN + ij * Q + k];
+          ry[k] = fin[e * IN + Q3 + ij * Q + k];
+          rz[k] = fin[e * IN + 2 * Q3 + ij * Q + k];
+        }
+      }
 #pragma unroll
       for (int k = 0; k < Q; ++k) {
         const int pt = ij * Q + k;
-        const double fx = fin[e * IN + pt], fy = fin[e * IN + Q3 + pt], fz = fin[e * IN + 2 * Q3 + pt];
+        const double fx = rx[k], fy = ry[k], fz = rz[k];
         double a0, a1, a2;
         if (GK == SPHP_GEOM_NONE) {
           const double wq = tab[T::W + i] * tab[T::W + j] * tab[T::W + k];
