@@ -256,36 +256,64 @@ struct QuadPhysDeriv {
     __syncthreads();
     SPHP_FOR_ITEMS(NE * Q, w) {  // along j: d1, metric (collections.py:181-185)
       int e = w / Q, i = w - e * Q;
-      double x[Q];
+      // rows of Q doubles one lane each (input, 4 metric rows, 2 output
+      // rows): rotated order for Q = 0 mod 4 (RowRot, 4-8-way conflicts
+      // otherwise), plain order at Q = 2 mod 4
+      constexpr bool ROT = (Q % 4 == 0) && (CS % Q == 0) && (GEO % Q == 0);
+      double x[Q], gi[4][Q], o0[Q], o1[Q];
+      if constexpr (ROT) {
+        RowRot<Q>::load(uin + e * Q2 + i * Q, w, x);
+      } else {
 #pragma unroll
-      for (int j = 0; j < Q; ++j) x[j] = uin[e * Q2 + i * Q + j];
+        for (int j = 0; j < Q; ++j) x[j] = uin[e * Q2 + i * Q + j];
+      }
       const double* g = geo + e * GEO;
+      if constexpr (GK == SPHP_GEOM_POINT) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if constexpr (ROT) {
+            RowRot<Q>::load(g + c * CS + i * Q, (e * GEO + c * CS) / Q + i, gi[c]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < Q; ++j) gi[c][j] = g[c * CS + i * Q + j];
+          }
+        }
+      }
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
         double d1 = 0.0;
 #pragma unroll
         for (int l = 0; l < Q; ++l) d1 = fma(tab[T::D + j * Q + l], x[l], d1);
         const double d0 = work[e * SW + i * QK + j];
-        const int pt = i * Q + j;
-        double o0 = d0, o1 = d1;
+        double r0 = d0, r1 = d1;
         if (GK != SPHP_GEOM_NONE) {
           double i00, i01, i10, i11;
           if (GK == SPHP_GEOM_POINT) {
-            i00 = g[pt];
-            i01 = g[CS + pt];
-            i10 = g[2 * CS + pt];
-            i11 = g[3 * CS + pt];
+            i00 = gi[0][j];
+            i01 = gi[1][j];
+            i10 = gi[2][j];
+            i11 = gi[3][j];
           } else {
             i00 = g[1];
             i01 = g[2];
             i10 = g[3];
             i11 = g[4];
           }
-          o0 = i00 * d0 + i10 * d1;
-          o1 = i01 * d0 + i11 * d1;
+          r0 = i00 * d0 + i10 * d1;
+          r1 = i01 * d0 + i11 * d1;
         }
-        out[e * OUT + pt] = o0;
-        out[e * OUT + Q2 + pt] = o1;
+        o0[j] = r0;
+        o1[j] = r1;
+      }
+      if constexpr (ROT) {
+        RowRot<Q>::store(out + e * OUT + i * Q, e * 2 * Q + i, o0);
+        RowRot<Q>::store(out + e * OUT + Q2 + i * Q, e * 2 * Q + Q + i, o1);
+      } else {
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          out[e * OUT + i * Q + j] = o0[j];
+          out[e * OUT + Q2 + i * Q + j] = o1[j];
+        }
       }
     }
     __syncthreads();
