@@ -11,6 +11,10 @@
 #pragma once
 #include <type_traits>
 
+#ifndef SPHP_SI_Q
+#define SPHP_SI_Q 0  // tuning: another Q with the padded dense plane pitch
+#endif
+
 #include "pipeline.cuh"
 #include "eo.cuh"
 
@@ -618,11 +622,12 @@ struct HexHelmEO {
   static constexpr int PP1 = (M == 4 && Q == 5) ? 28 : (M == 6 && Q == 7) ? 42 : pitch_mod16(M * QK, Q);
   static constexpr int PP2 = pitch_mod16(Q * Q, Q);
   // plane pitch of the dense (i, j, k) work tensors: Q^2 (contiguous), except
-  // Q = 10 where Q^2 = 4 mod 16 puts the j-pencil lanes (i, k) on banks 4i + k
-  // (ncu P=8: 105 M of 144 M excess wavefronts); SI = 10 mod 16 makes them
-  // consecutive while the 128-bit k-rows stay conflict free but for the
-  // phases that cross an i
-  static constexpr int SI = (Q == 10) ? pitch_mod16(Q * Q, Q) : Q * Q;
+  // Q = 6 and Q = 10 where Q^2 = 4 mod 16 puts the j-pencil lanes (i, k) on
+  // banks 4i + k (ncu P=8: 105 M of 144 M excess wavefronts); SI = Q mod 16
+  // makes them consecutive while the 128-bit k-rows stay conflict free but
+  // for the phases that cross an i.  Measured: P=4 0.636 -> 0.623 ms, P=8
+  // 3.341 -> 3.256 ms.  (Odd Q: the scalar k-rows would conflict instead.)
+  static constexpr int SI = (Q == 6 || Q == 10 || Q == SPHP_SI_Q) ? pitch_mod16(Q * Q, Q) : Q * Q;
   static constexpr int SE = (M == 4 && Q == 5) ? 157 : (M == 6 && Q == 7) ? 343
                                                      : even_up(cmax(Q * SI, cmax(M * PP1, M * PP2)));
   static_assert(SE >= Q * SI && SE >= M * PP1 && SE >= M * PP2, "element tensors overlap");
