@@ -95,7 +95,7 @@ int segment_length(int n, int P, bool owner) {
   static const int force = env_int("SPHP_PERIODIC_L", 0);  // tuning override
   if (force >= 4 && n % force == 0 && force * nm < 8192 && force <= 32) return force;
   auto fits = [&](int L) {
-    return n % L == 0 && L * nm < 8192 &&
+    return n % L == 0 && L * (nm + 2) < 8192 &&
            (size_t)L * nm * 12 + (size_t)L * P * P * P * 4 <= 48 * 1024;
   };
   if (owner)
@@ -171,8 +171,12 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) periodic_scatter_v2_
   __shared__ int cb[28];
   __shared__ int2 cseg[2][27];  // per class: (base, wrap correction)
   const int m = P + 1, nm = m * m * m, b = P - 1, total = L * nm;
-  double* blk = smem;                                              // L * nm + 2 (scratch)
-  uint32_t* word = reinterpret_cast<uint32_t*>(blk + total + 2);  // U * kThreads
+  // element stride of the staged block: nm, or nm + 2 for even nm (an
+  // element stride = 0 or 8 mod 16 put the consecutive-element slots of one
+  // class on 1-2 bank pairs: 8-16-way conflicts at P = 3, 5, 7)
+  const int nmp = (nm & 1) ? nm : nm + 2, total_p = L * nmp;
+  double* blk = smem;                                                // L * nmp + 2 (scratch)
+  uint32_t* word = reinterpret_cast<uint32_t*>(blk + total_p + 2);  // U * kThreads
   int* inv = reinterpret_cast<int*>(word + U * kThreads);          // nm: class slot -> local mode
   const int segs = n / L, nseg = sg1;  // segments [sg0, sg1) (x-rows of L elements)
   if (threadIdx.x == 0) {
@@ -193,14 +197,14 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) periodic_scatter_v2_
   // the scratch double after the block, so the streaming loop is branch-free
   for (int t = threadIdx.x; t < U * kThreads; t += kThreads) {
     if (t >= total) {
-      word[t] = (uint32_t)total << 18;
+      word[t] = (uint32_t)total_p << 18;
       continue;
     }
     int k = 0;
     while (L * cb[k + 1] <= t) ++k;
     const int s = class_size(k, b);
     const int r = t - L * cb[k], el = r / s, o = r - el * s;
-    const uint32_t dest = el * nm + inv[cb[k] + o];
+    const uint32_t dest = el * nmp + inv[cb[k] + o];
     const uint32_t wrap = (class_dx(k) && el == L - 1) ? 1u : 0u;
     word[t] = (uint32_t)k | ((uint32_t)r << 5) | (dest << 18) | (wrap << 31);
   }
@@ -265,15 +269,22 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) periodic_scatter_v2_
     issue(nxt, buf ^ 1);  // next segment's loads overlap the write-out
     // one TMA bulk store of the block (L * nm is even and the block start
     // 16-byte aligned, L % 4 == 0); the threads only wait for its reads
-    if (threadIdx.x == 0) {
-      bulk_s2g(loc + (size_t)cur * total, blk, (uint32_t)(sizeof(double) * total));
+    if (nmp == nm) {
+      if (threadIdx.x == 0) {
+        bulk_s2g(loc + (size_t)cur * total, blk, (uint32_t)(sizeof(double) * total));
+        bulk_commit();
+        bulk_wait_read0();
+      }
+    } else if (threadIdx.x < 32) {  // padded: one bulk copy per element
+      for (int el = threadIdx.x; el < L; el += 32)
+        bulk_s2g(loc + (size_t)cur * total + (size_t)el * nm, blk + el * nmp, (uint32_t)(sizeof(double) * nm));
       bulk_commit();
       bulk_wait_read0();
     }
     __syncthreads();  // block consumed
     cur = nxt;
   }
-  if (threadIdx.x == 0) bulk_wait0();
+  if (threadIdx.x < 32) bulk_wait0();
 }
 
 // per-thread register batch: U * kThreads >= L * nm
@@ -295,7 +306,8 @@ cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cuda
   const int nm = (P + 1) * (P + 1) * (P + 1);
   return with_unroll(L * nm, [&](auto uc) {
     constexpr int U = decltype(uc)::value;
-    const size_t smem = sizeof(double) * (L * nm + 2) + sizeof(uint32_t) * U * kThreads + sizeof(int) * nm;
+    const int nmp = (nm & 1) ? nm : nm + 2;
+    const size_t smem = sizeof(double) * (L * nmp + 2) + sizeof(uint32_t) * U * kThreads + sizeof(int) * nm;
     static int configured = 0;
     allow_smem(periodic_scatter_v2_kernel<U>, configured);
     if (row1 < 0) row1 = n * n;  // rows ey + n ez
