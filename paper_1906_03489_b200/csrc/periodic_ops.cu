@@ -346,8 +346,10 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
   __shared__ long long rowoff[2][4];  // per neighbour row: (row element + ex0 - 1) * nm
   const int m = P + 1, nm = m * m * m, b = P - 1, per = P * P * P;
   const int total1 = L * nm, total2 = L * per;
+  // staged element stride: nm + 2 for even nm (bank spread, as the scatter)
+  const int nmp = (nm & 1) ? nm : nm + 2, total1p = L * nmp;
   double* S = smem;                                              // L * nm + 2 (scratch)
-  uint32_t* w1 = reinterpret_cast<uint32_t*>(S + total1 + 2);  // U * kThreads
+  uint32_t* w1 = reinterpret_cast<uint32_t*>(S + total1p + 2);  // U * kThreads
   uint32_t* w2 = w1 + U * kThreads;                              // L * P^3
   const int segs = n / L, nseg = sg1;  // segments [sg0, sg1) (x-rows of L elements)
   if (threadIdx.x == 0) {
@@ -361,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
   __syncthreads();
   for (int t = threadIdx.x; t < U * kThreads; t += kThreads) {
     if (t >= total1) {  // padding: a valid load into the scratch double
-      w1[t] = ((uint32_t)nm << 2) | ((uint32_t)total1 << 17);
+      w1[t] = ((uint32_t)nm << 2) | ((uint32_t)total1p << 17);
       continue;
     }
     // offset o8 = (a, b, c) bits; its index set has P or 1 entries per axis
@@ -398,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
     int pos = 0, nb = 0;
     for (int d = 0; d < 3; ++d)
       if (zmask >> d & 1) pos |= ((o8 >> d) & 1) << nb++;
-    const uint32_t dest = el * nm + cstart[cc] + (off << owned_log(cc)) + pos;
+    const uint32_t dest = el * nmp + cstart[cc] + (off << owned_log(cc)) + pos;
     const uint32_t mode = (np * m + nq) * m + nr;
     const uint32_t elx = el - a + 1, wrap = elx == 0 ? 1u : 0u;
     w1[t] = (uint32_t)(o8 & 3) | ((elx * nm + mode) << 2) | (dest << 17) | (wrap << 31);
@@ -407,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
     int cc = 0, first = 0;
     while (t >= first + L * owned_size(cc, b)) first += L * owned_size(cc++, b);
     const int s = owned_size(cc, b), r0 = t - first, el = r0 / s, off = r0 - el * s;
-    const uint32_t start = el * nm + cstart[cc] + (off << owned_log(cc));
+    const uint32_t start = el * nmp + cstart[cc] + (off << owned_log(cc));
     w2[t] = (uint32_t)cc | ((uint32_t)r0 << 3) | (start << 16) | ((uint32_t)owned_log(cc) << 29);
   }
   // per segment: owned-class output bases and the 4 neighbour rows
@@ -499,8 +501,9 @@ cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int ac
   const int nm = (P + 1) * (P + 1) * (P + 1);
   return with_unroll(L * nm, [&](auto uc) {
     constexpr int U = decltype(uc)::value;
+    const int nmp = (nm & 1) ? nm : nm + 2;
     const size_t smem =
-        sizeof(double) * (L * nm + 2) + sizeof(uint32_t) * (U * kThreads + L * P * P * P);
+        sizeof(double) * (L * nmp + 2) + sizeof(uint32_t) * (U * kThreads + L * P * P * P);
     static int configured = 0;
     allow_smem(owner_periodic_v3_kernel<U>, configured);
     if (row1 < 0) row1 = n * n;
