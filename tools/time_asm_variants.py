@@ -24,7 +24,7 @@ def timed(fn, reps=10):
 
 
 n = 64
-for P in (2, 4, 6, 8):
+for P in [int(p) for p in (sys.argv[1] if len(sys.argv) > 1 else "2,4,6,8").split(",")]:
     exp = sp.make_hex(P, P + 2)
     batch = sp.ElementBatch.structured(exp, n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE, amp=0.03)
     coll = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC)
