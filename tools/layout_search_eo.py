@@ -19,7 +19,7 @@ def rowrot(M, R):
 
 
 def stages(M, Q, NE, NT, SE, SI, PP1, PP2, GS, CS):
-    QK = Q
+    QK = Q | 1  # odd_up(Q), as HexHelmEO
     M3 = M ** 3
     OUT0 = NE * SE  # output block staged in W1 (OUT_OFF)
     W0, W1, W2 = 0, NE * SE, 2 * NE * SE
