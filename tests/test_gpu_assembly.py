@@ -197,7 +197,7 @@ def test_reference_map_signs_explicit(sp):
         assert_parity(y.cpu().numpy(), ref, what=f"signed explicit map {alg}")
 
 
-@pytest.mark.parametrize("P", [6, 8])
+@pytest.mark.parametrize("P", [3, 5, 6, 7, 8])
 def test_colour_vs_owner_large_mesh(sp, P):
     """Regression: many tiles per CTA and several scatter rounds per thread
     (NE = 1) — the colour-ordered path must agree with the owner-computes
