@@ -138,11 +138,13 @@ def test_zero_input_zero_output(sp):
         assert np.all(out == 0)
 
 
+@pytest.mark.parametrize("PQ", [(2, 4), (3, 5), (4, 6), (7, 9)])
 @pytest.mark.parametrize("op", OPS)
-def test_unaligned_and_tiny_inputs(sp, op):
+def test_unaligned_and_tiny_inputs(sp, op, PQ):
     """Inputs not 16-byte aligned take the synchronous (non-TMA) load path;
-    E = 1 and E = 2 exercise single partial tiles."""
-    shape, P, Q = "hex", 4, 6
+    E = 1 and E = 2 exercise single partial tiles.  Orders cover the skewed
+    Q=4 plan, the rotated even-M rows (P=3, 7) and the K-row plan."""
+    shape, (P, Q) = "hex", PQ
     n = 4
     for E in (1, 2, 37):
         ids = np.arange(E)
@@ -156,7 +158,15 @@ def test_unaligned_and_tiny_inputs(sp, op):
         assert view.data_ptr() % 16 == 8
         got = coll.apply(view).cpu().numpy()
         ref = oracle_apply(op, oe, x, inv, wj, geom)
-        assert_parity(got.reshape(ref.shape), ref, what=f"unaligned {op} E{E}")
+        assert_parity(got.reshape(ref.shape), ref, what=f"unaligned {op} P{P} E{E}")
+        # an output not 16-byte aligned: the store loop instead of the TMA
+        # bulk write-back, bitwise the same values
+        osz = got.size // E
+        obuf = torch.zeros(E * osz + 1, dtype=torch.float64, device="cuda")
+        oview = obuf[1:].view(got.shape)
+        assert oview.data_ptr() % 16 == 8
+        coll.apply(view, oview)
+        assert np.array_equal(oview.cpu().numpy(), got)
 
 
 def test_multi_tile_walk_small_grid(sp):
