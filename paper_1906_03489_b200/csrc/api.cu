@@ -796,6 +796,7 @@ int sphp_geom_from_factors(const sphp_tables* tc, int kind, int64_t E, const dou
   GeomJob j;
   std::memset(&j, 0, sizeof(j));
   j.dim = t->dim;
+  j.Q = t->q[0];
   j.kind = kind;
   j.E = E;
   j.npts = t->np;

@@ -130,6 +130,21 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // ---------------------------------------------------------------------------
+// Storage slot of quadrature point pt = (i*Q + j)*Q + k inside one METRIC
+// component of a hex element record.  Q = 8 stores the points j-major,
+// (j*Q + i)*Q + k: the Q = 8 Helmholtz reads the metric on j-pencils with
+// lanes (i, k), which in point order would put 16 lanes on 8 bank pairs
+// (ncu P=6: 59 M of 133 M excess wavefronts); j-major puts lanes i and i+1
+// 8 banks apart.  Every producer (geometry kernels) and consumer (the
+// Helmholtz kernels, the Jacobi diagonal) goes through this function.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int metric_slot(int dim, int Q, int pt) {
+  if (dim != 3 || Q != 8) return pt;
+  const int i = pt >> 6, j = (pt >> 3) & 7, k = pt & 7;
+  return (j << 6) | (i << 3) | k;
+}
+
+// ---------------------------------------------------------------------------
 // Pencil contraction: out[o*OS] (+)= sum_l T(o,l) in[l*IS], T(o,l) read from
 // constant memory at TOFF + o*TSO + l*TSI.  Summation order l = 0..NIN-1
 // (fixed, so repeated applies are bitwise identical).

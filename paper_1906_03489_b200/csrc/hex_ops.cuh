@@ -523,7 +523,7 @@ struct HexHelmJ {
         const double d2 = W1[base + j * QK];
         double G00, G01, G02, G11, G12, G22, wj;
         if (GK == SPHP_GEOM_METRIC) {
-          const int pt = (i * Q + j) * Q + k;
+          const int pt = metric_slot(3, Q, (i * Q + j) * Q + k);
           G00 = g[0 * CS + pt];
           G01 = g[1 * CS + pt];
           G02 = g[2 * CS + pt];
@@ -890,7 +890,7 @@ struct HexHelmJEO {
         const double d2 = W1[base + j * QK];
         double G00, G01, G02, G11, G12, G22, wj;
         if (GK == SPHP_GEOM_METRIC) {
-          const int pt = (i * Q + j) * Q + k;
+          const int pt = metric_slot(3, Q, (i * Q + j) * Q + k);
           G00 = g[0 * CS + pt];
           G01 = g[1 * CS + pt];
           G02 = g[2 * CS + pt];
@@ -1101,7 +1101,7 @@ struct HexHelmQ4 {
       for (int i = 0; i < Q; ++i) {
         double G00, G01, G02, G11, G12, G22, wj;
         if constexpr (GK == SPHP_GEOM_METRIC) {
-          const int pt = (i * Q + j) * Q + k;
+          const int pt = metric_slot(3, Q, (i * Q + j) * Q + k);
           G00 = g[0 * CS + pt];
           G01 = g[1 * CS + pt];
           G02 = g[2 * CS + pt];

@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include "../../include/spechp_b200.h"
+#include "common.cuh"
 #include "misc.h"
 #include "periodic.cuh"
 
@@ -100,14 +101,15 @@ __global__ void geom_analytic_kernel(GeomJob j, int* bad) {
       for (int k = 0; k < dim; ++k) rec[(c++) * cs + pt] = inv[a][k];
   } else {  // METRIC: G_ab = wJ sum_k inv[a,k] inv[b,k]
     const double wj = wq * det;
+    const int ms = metric_slot(dim, j.Q, pt);
     int c = 0;
     for (int a = 0; a < dim; ++a)
       for (int b = a; b < dim; ++b) {
         double g = 0.0;
         for (int k = 0; k < dim; ++k) g += inv[a][k] * inv[b][k];
-        rec[(c++) * cs + pt] = wj * g;
+        rec[(c++) * cs + ms] = wj * g;
       }
-    rec[c * cs + pt] = wj;
+    rec[c * cs + ms] = wj;
   }
 }
 
@@ -136,14 +138,15 @@ __global__ void geom_convert_kernel(GeomJob j, const double* wj, const double* i
     rec[pt] = w;
     for (int c = 0; c < dim * dim; ++c) rec[(1 + c) * cs + pt] = iv[c];
   } else {
+    const int ms = metric_slot(dim, j.Q, pt);
     int c = 0;
     for (int a = 0; a < dim; ++a)
       for (int b = a; b < dim; ++b) {
         double g = 0.0;
         for (int k = 0; k < dim; ++k) g += iv[a * dim + k] * iv[b * dim + k];
-        rec[(c++) * cs + pt] = w * g;
+        rec[(c++) * cs + ms] = w * g;
       }
-    rec[c * cs + pt] = w;
+    rec[c * cs + ms] = w;
   }
 }
 

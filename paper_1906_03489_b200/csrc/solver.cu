@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include "../../include/spechp_b200.h"
+#include "common.cuh"
 #include "solver.h"
 
 namespace sphp {
@@ -42,7 +43,7 @@ __global__ void helm_diag_kernel(DiagJob j) {
     for (int i = 0; i < Q; ++i)
       for (int jj = 0; jj < Q; ++jj)
         for (int k = 0; k < Q; ++k) {
-          const int pt = (i * Q + jj) * Q + k;
+          const int pt = sphp::metric_slot(3, Q, (i * Q + jj) * Q + k);
           double g00, g01, g02, g11, g12, g22, wq;
           if (j.kind == SPHP_GEOM_METRIC) {
             g00 = g[pt];
