@@ -37,6 +37,9 @@ struct QuadHelm {
   static constexpr int QK = odd_up(Q);
   static constexpr int SW = spread16(Q * QK);
   static constexpr int WORK = 3 * SW;
+  // the last stage reads only W0: the output block is staged in W1 (one
+  // buffer fewer per CTA -> more resident CTAs; the kernel is latency bound)
+  static constexpr int OUT_OFF = NE * SW;
   using T = Tab<M, Q>;
 
   template <class R, class W>
