@@ -1424,6 +1424,7 @@ struct HexIPDeriv {
   static constexpr int QK = odd_up(Q);
   static constexpr int SW = odd_up(Q * Q * QK);
   static constexpr int WORK = 3 * SW;
+  static constexpr int OUT_OFF = NE * SW;  // the last stage reads W0: the block is staged in W1
   using T = Tab<M, Q>;
 
   template <class R, class W>
