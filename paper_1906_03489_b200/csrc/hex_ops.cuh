@@ -1268,6 +1268,7 @@ struct HexIprod {
   static constexpr int PB = pitch_mod16(Q * Q, Q);
   static constexpr int SA = odd_up(M * M * QK), SB = M * PB;
   static constexpr int WORK = SA + SB;
+  static constexpr int OUT_OFF = NE * SA;  // the last stage reads A: the block is staged in B
   using T = Tab<M, Q>;
 
   template <class R, class W>
