@@ -11,6 +11,9 @@
 #pragma once
 #include <type_traits>
 
+#ifndef SPHP_Q7_EFAST
+#define SPHP_Q7_EFAST 1  // tuning: 0 = rotated j-pencils at Q = 7 instead
+#endif
 #ifndef SPHP_SI_Q
 #define SPHP_SI_Q 0  // tuning: another Q with the padded dense plane pitch
 #endif
@@ -642,7 +645,8 @@ struct HexHelmEO {
   // measured P=5 -1 %).  Also modelled better but measured no gain at Q = 6
   // and slower at Q = 10 (P=8 3.34 -> 3.66 ms: the rotation selects cost
   // more than the conflicts): natural order there.
-  static constexpr int JROT = (Q == 7) ? 1 : 0;
+  static constexpr bool EFAST = (Q == 7 && NE == 2 && SPHP_Q7_EFAST);
+  static constexpr int JROT = (Q == 7 && !EFAST) ? 1 : 0;
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
 
@@ -683,7 +687,11 @@ struct HexHelmEO {
     __syncthreads();
     // S4: d1 = D along j
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
+      // element-fastest lanes at Q = 7 (EFAST): two elements' pencils share
+      // a half-warp, their banks 7 apart (model: 2.71x -> 1.86x of the ideal
+      // wavefronts, as the rotation, without its selects)
+      const int e = EFAST ? w % NE : w / (Q * Q);
+      const int ik = EFAST ? w / NE : w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
       double v[Q], r[Q];
       const int tau = (JROT * i) % Q;
       Rot<Q>::template load<Q>(W0 + e * SE + i * SI + k, tau, v);
@@ -765,7 +773,8 @@ struct HexHelmEO {
     release();
     // S6: t += D1^T f1 along j
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
+      const int e = EFAST ? w % NE : w / (Q * Q);
+      const int ik = EFAST ? w / NE : w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
       double f[Q], t[Q];
       const int tau = (JROT * i) % Q;
       Rot<Q>::template load<Q>(W1 + e * SE + i * SI + k, tau, f);
