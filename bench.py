@@ -406,14 +406,35 @@ def config_extras(sp, dev, timed, peak):
     out = {}
     rng = np.random.default_rng(SEED)
 
+    def graph_ms(coll, x, y, reps=20):
+        """Device time per apply without the Python call overhead: `reps`
+        applies captured in one CUDA graph, replayed (small configs are
+        host-bound when launched one call at a time)."""
+        try:
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                coll.apply(x, y)
+            torch.cuda.current_stream(dev).wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(reps):
+                    coll.apply(x, y)
+            return timed(lambda: g.replay(), 5, 2) / reps
+        except Exception:  # capture unsupported here: report the plain timing only
+            return None
+
     def op_entry(name, coll, x):
         y = torch.empty(coll.output_shape, dtype=torch.float64, device=dev)
         ms = timed(lambda: coll.apply(x, y), 20, 3)
         b = coll.hbm_bytes()
+        gms = graph_ms(coll, x, y)
         out[name] = {"ms": ms, "elements": coll.num_elements, "hbm_bytes": b,
                      "hbm_gbs": b / (ms * 1e-3) / 1e9, "frac": b / (ms * 1e-3) / 1e9 / peak,
                      "dof_s": coll.num_elements * (x.shape[1] if coll.operator.value == "bwdtrans"
-                                                   else coll.output_shape[-1]) / (ms * 1e-3)}
+                                                   else coll.output_shape[-1]) / (ms * 1e-3),
+                     "graph_ms": gms,
+                     "graph_frac": (b / (gms * 1e-3) / 1e9 / peak) if gms else None}
 
     # cfg1: 32x32 affine quads, P=4, Q=6: BwdTrans + IProductWRTBase
     q = sp.make_quad(4, 6)
