@@ -88,8 +88,10 @@ int env_int(const char* name, int dflt) {
 
 // L: largest of 32/16/8/4 dividing n with L * nm < 2^13 (packed slot
 // indices) and block + tables within 48 KB (4+ CTAs per SM).  The owner sum
-// prefers segments of at most ~1800 slots (fewer registers per thread, more
-// resident CTAs): measured P=4 108 us at L=8 vs 113 us at L=16.
+// prefers segments of at most ~3000 slots (fewer registers per thread, more
+// resident CTAs); re-measured after the padded staging (tools/time_periodic.py,
+// SPHP_PERIODIC_L): P=4 121 us at L=8 vs 116 us at L=16, P=6 314 us at L=4
+// vs 294 us at L=8.
 int segment_length(int n, int P, bool owner) {
   const int nm = (P + 1) * (P + 1) * (P + 1);
   static const int force = env_int("SPHP_PERIODIC_L", 0);  // tuning override
@@ -100,7 +102,7 @@ int segment_length(int n, int P, bool owner) {
   };
   if (owner)
     for (int L = 32; L >= 4; L /= 2)
-      if (fits(L) && L * nm <= 1800) return L;
+      if (fits(L) && L * nm <= 3000) return L;
   for (int L = 32; L >= 4; L /= 2)
     if (fits(L)) return L;
   return 0;
