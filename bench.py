@@ -197,6 +197,46 @@ def cpu_port_assembled(P, n_sample, seconds, seed=SEED):
     return runs * E * (P + 1) ** 3 / el, runs, el, os.cpu_count() or 1, E
 
 
+def parity_sample(P, n, x, y, c, yl, seed=SEED):
+    """Parity of the measured applies against the oracle (the checker; run
+    outside every timed region): the assembled y on the global dofs of 24
+    sampled elements (exact given their 27-element neighbourhoods, map =
+    the oracle's numbering of assembly.py:72-138) and the local K4 output
+    on 512 sampled elements including the first and last ones."""
+    from oracle import assembly as oa
+    from oracle import geometry as og
+    from oracle import ops as oo
+
+    E = n ** 3
+    oe = oo.Expansion("hex", P, P + 2)
+    rng = np.random.default_rng(seed)
+
+    def helm(ids, coeffs):
+        _, _, inv, wj = og.factors(oe, n, ids, og.MAP_HEX_SINE, AMP)
+        return oo.helmholtz(oe, coeffs, 1.0, oo.metric_from_inv(wj, inv), wj)
+
+    def errs(got, ref):
+        return {"rel_l2": float(np.linalg.norm(got - ref) / np.linalg.norm(ref)),
+                "max_abs": float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))}
+
+    _, _, codes = oa.hex_periodic_codes(n, P)
+    codes = codes.reshape(E, -1)
+    sample = np.unique(np.concatenate([[0, E - 1], rng.choice(E, 22, replace=False)]))
+    ex, ey, ez = sample % n, (sample // n) % n, sample // (n * n)
+    nb = np.unique(np.concatenate([((ex + a) % n) + n * (((ey + b) % n) + n * ((ez + cc) % n))
+                                   for a in (-1, 0, 1) for b in (-1, 0, 1) for cc in (-1, 0, 1)]))
+    ylo = helm(nb, x[codes[nb]])
+    yref = np.bincount(codes[nb].ravel(), weights=ylo.ravel(), minlength=x.size)
+    dofs = np.unique(codes[sample])
+    out = {"assembled": dict(errs(y[dofs], yref[dofs]), dofs=int(dofs.size)),
+           "tolerance": {"rel_l2": 1e-12, "max_abs": 1e-11}}
+    ids = np.unique(np.concatenate([np.arange(128), np.arange(E - 128, E),
+                                    rng.choice(E, 256, replace=False)]))
+    out["local"] = dict(errs(yl[ids], helm(ids, c[ids])), elements=int(ids.size))
+    out["ok"] = all(out[k]["rel_l2"] < 1e-12 and out[k]["max_abs"] < 1e-11 for k in ("assembled", "local"))
+    return out
+
+
 # ---------------------------------------------------------------------------
 def run_reference(args, rank, world):
     if rank != 0:
@@ -316,6 +356,12 @@ def run_ours(args, rank, world, local_rank):
     # assembled apply as a whole against the same roofline
     ab = workload_bytes(P, n)
     a_achieved = ab / (ms * 1e-3) / 1e9
+    parity = None
+    if rank == 0:
+        # checked outside every timed region: the last timed outputs y, yl
+        op.apply(x, y)
+        coll.apply(c, yl)
+        parity = parity_sample(P, n, x_host.numpy(), y.cpu().numpy(), c.cpu().numpy(), yl.cpu().numpy())
     del c, yl
 
     sweep = None
@@ -390,6 +436,7 @@ def run_ours(args, rank, world, local_rank):
         # split: scatter, fused local Helmholtz, owner sum; owner: gather-fused + owner sum
         "gpu_launches": args.steps * (3 if amap.algorithm == "split" else 2),
         "replicas_identical": replicas_identical,
+        "parity": parity,
     }
     if sweep is not None:
         line["sweep"] = sweep

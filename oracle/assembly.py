@@ -282,3 +282,108 @@ def hex_periodic(n, orders):
 
 def hex_periodic_map(n, orders):
     return build_map(hex_periodic(n, orders))
+
+
+# ---------------------------------------------------------------------------
+# vectorised periodic hex numbering (BASELINE sizes: 64^3, 48^3)
+# ---------------------------------------------------------------------------
+
+def hex_periodic_codes(n, orders):
+    """build_map(hex_periodic(n, orders)) without per-element Python objects.
+
+    The same numbering rules (assembly.py:89-133 generalised): on the periodic
+    grid every vertex and every edge/face is used and there is no Dirichlet
+    block, so vertex gid = vertex id; edge dofs follow in (edge id, degree)
+    order, edge order = min over the 4 sharing elements (assembly.py:74-79);
+    face dofs in (face id, deg1, deg2) order, face order = min over the 2
+    sharing elements; interiors element by element in local flat order;
+    excess modes pinned (-1).  Signs are all +1 (every edge traversed
+    forward), so a code is the gid.  `tests/test_oracle.py` pins this to
+    `build_map` at small n; it exists so the 64^3 / 48^3 maps can be
+    compared bit for bit with the native ones.
+
+    Returns (num_global, offsets (n^3 + 1,), codes (sum m_e^3,)) with element
+    e's codes at codes[offsets[e]:offsets[e+1]] in local flat order
+    (p*m + q)*m + r.
+    """
+    N3 = n ** 3
+    orders = np.broadcast_to(np.asarray(orders, dtype=np.int64).ravel(), (N3,)) \
+        if np.ndim(orders) == 0 else np.asarray(orders, dtype=np.int64).ravel()
+    if orders.size != N3:
+        raise ValueError(f"need {N3} orders")
+    e = np.arange(N3, dtype=np.int64)
+    b = (e % n, (e // n) % n, e // (n * n))
+
+    def vid(o):
+        return ((b[0] + o[0]) % n) + n * (((b[1] + o[1]) % n) + n * ((b[2] + o[2]) % n))
+
+    def edge_id(d, s, t):
+        o = [s, t]
+        o.insert(d, 0)
+        return d * N3 + vid(o)
+
+    def face_id(d, side):
+        o = [0, 0, 0]
+        o[d] = side
+        return d * N3 + vid(o)
+
+    big = np.iinfo(np.int64).max
+    eord = np.full(3 * N3, big, dtype=np.int64)
+    ford = np.full(3 * N3, big, dtype=np.int64)
+    for d in range(3):
+        for s in (0, 1):
+            for t in (0, 1):
+                np.minimum.at(eord, edge_id(d, s, t), orders)
+        for side in (0, 1):
+            np.minimum.at(ford, face_id(d, side), orders)
+    eoff = np.concatenate([[0], np.cumsum(np.maximum(eord - 1, 0))])
+    foff = np.concatenate([[0], np.cumsum(np.maximum(ford - 1, 0) ** 2)])
+    ebase = N3
+    fbase = ebase + eoff[-1]
+    ibase = fbase + foff[-1]
+    nint = np.maximum(orders - 1, 0) ** 3
+    ioff = ibase + np.concatenate([[0], np.cumsum(nint)])[:-1]
+    offsets = np.concatenate([[0], np.cumsum((orders + 1) ** 3)])
+    uniform = np.all(orders == orders[0])
+    codes = None if uniform else np.empty(offsets[-1], dtype=np.int64)
+    for P in np.unique(orders):
+        ids = np.nonzero(orders == P)[0]
+        m = int(P) + 1
+        bl = tuple(x[ids] for x in b)
+
+        def vid_l(o):
+            return ((bl[0] + o[0]) % n) + n * (((bl[1] + o[1]) % n) + n * ((bl[2] + o[2]) % n))
+
+        out = np.empty((ids.size, m ** 3), dtype=np.int64)
+        interior_rank = 0
+        for p in range(m):
+            for q in range(m):
+                for r in range(m):
+                    idx = (p, q, r)
+                    nb = (p >= 2) + (q >= 2) + (r >= 2)
+                    col = (p * m + q) * m + r
+                    if nb == 0:
+                        out[:, col] = vid_l(idx)
+                    elif nb == 1:
+                        d = 0 if p >= 2 else (1 if q >= 2 else 2)
+                        o = [idx[a] if a != d else 0 for a in range(3)]
+                        eid = d * N3 + vid_l(o)
+                        deg = idx[d]
+                        out[:, col] = np.where(deg <= eord[eid], ebase + eoff[eid] + (deg - 2), -1)
+                    elif nb == 2:
+                        d = 0 if p < 2 else (1 if q < 2 else 2)
+                        o = [idx[a] if a == d else 0 for a in range(3)]
+                        fid = d * N3 + vid_l(o)
+                        k1, k2 = [idx[a] for a in range(3) if a != d]
+                        pf = ford[fid]
+                        ok = (k1 <= pf) & (k2 <= pf)
+                        out[:, col] = np.where(ok, fbase + foff[fid] + (k1 - 2) * (pf - 1) + (k2 - 2), -1)
+                    else:
+                        out[:, col] = ioff[ids] + interior_rank
+                        interior_rank += 1
+        if uniform:
+            codes = out.reshape(-1)
+        else:
+            flat_idx = (offsets[ids][:, None] + np.arange(m ** 3)[None, :]).ravel()
+            codes[flat_idx] = out.ravel()
+    return int(ibase + nint.sum()), offsets, codes

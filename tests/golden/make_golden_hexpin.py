@@ -35,7 +35,7 @@ from spechp.stdregions import make_seg  # noqa: E402
 H = 0.5
 LAM = 1.3
 out = {"h": np.float64(H), "lam": np.float64(LAM)}
-for P in (1, 2, 3, 4, 5, 6):
+for P in (1, 2, 3, 4, 5, 6, 7, 8):
     Q = P + 2
     mesh = structured_quad_mesh(1, 1, x1=H, y1=H)
     el = build_elements(mesh, orders=P, num_points=Q)[0]

@@ -4,7 +4,7 @@ The reference has no hexahedra, but on an affine brick every hex operator
 factors exactly into the reference's quad and segment operators
 (tests/golden/make_golden_hexpin.py).  The numpy oracle (CPU) and the CUDA
 kernels (GPU) are checked against those Kronecker compositions:
-BwdTrans, IProductWRTBase, PhysDeriv and the fused Helmholtz, P = 1..6,
+BwdTrans, IProductWRTBase, PhysDeriv and the fused Helmholtz, P = 1..8,
 Q = P+2, on the brick [0, 1/2]^3 (the n = 2 structured grid)."""
 from pathlib import Path
 
@@ -15,7 +15,7 @@ from oracle import geometry as og
 from oracle import ops
 
 G = np.load(Path(__file__).resolve().parent / "golden" / "reference_hexpin.npz")
-PS = (1, 2, 3, 4, 5, 6)
+PS = (1, 2, 3, 4, 5, 6, 7, 8)
 H, LAM = float(G["h"]), float(G["lam"])
 TOL = 1e-12
 
