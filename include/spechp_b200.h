@@ -184,6 +184,7 @@ int sphp_amap_destroy(sphp_amap* a);
 #define SPHP_ASSEMBLY_OWNER 0
 #define SPHP_ASSEMBLY_COLOUR 1
 #define SPHP_ASSEMBLY_SPLIT 2
+#define SPHP_ASSEMBLY_CLASS 3
 int sphp_amap_set_algorithm(sphp_amap* a, int alg);
 int sphp_amap_algorithm(const sphp_amap* a, int* alg);
 int sphp_amap_info(const sphp_amap* a, int64_t* num_elements, int* nmodes,

@@ -13,7 +13,7 @@ from pathlib import Path
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libspechp_b200.so"
 # tuning experiments may point at an alternative in-tree build
-if os.environ.get("SPHP_LIBRARY_VARIANT"):
+if os.environ.get("SPHP_LIBRARY_VARIANT", ""):
     LIB_PATH = _HERE.parent / "build" / "variants" / os.environ["SPHP_LIBRARY_VARIANT"] / "libspechp_b200.so"
 
 # error codes (include/spechp_b200.h)
@@ -31,7 +31,7 @@ OP_BWD_TRANS, OP_IPRODUCT_WRT_BASE, OP_PHYS_DERIV, OP_IPRODUCT_WRT_DERIV_BASE, O
 STRATEGY_CUDA_SUMFAC, STRATEGY_CUDA_STDMAT = 0, 1
 GEOM_NONE, GEOM_AFFINE, GEOM_POINT, GEOM_METRIC = 0, 1, 2, 3
 MAP_AFFINE, MAP_QUAD_SINE, MAP_HEX_SINE = 0, 1, 2
-ASSEMBLY_OWNER, ASSEMBLY_COLOUR, ASSEMBLY_SPLIT = 0, 1, 2
+ASSEMBLY_OWNER, ASSEMBLY_COLOUR, ASSEMBLY_SPLIT, ASSEMBLY_CLASS = 0, 1, 2, 3
 RIEMANN = {"upwind": 0, "laxfriedrichs": 1}
 BC_INTERIOR, BC_RIGID_WALL, BC_FARFIELD, BC_DIRICHLET = 0, 1, 2, 3
 

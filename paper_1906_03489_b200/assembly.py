@@ -77,7 +77,7 @@ class AssemblyMap:
         a = C.c_int()
         _lib.check(_lib.lib.sphp_amap_algorithm(self._h, C.byref(a)), AssemblyError)
         return {_lib.ASSEMBLY_OWNER: "owner", _lib.ASSEMBLY_COLOUR: "colour",
-                _lib.ASSEMBLY_SPLIT: "split"}[a.value]
+                _lib.ASSEMBLY_SPLIT: "split", _lib.ASSEMBLY_CLASS: "class"}[a.value]
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -113,7 +113,7 @@ class AssemblyMap:
         kernel -> local operator -> owner sum) or 'colour' (fused
         colour-ordered scatter-add)."""
         code = {"owner": _lib.ASSEMBLY_OWNER, "colour": _lib.ASSEMBLY_COLOUR,
-                "split": _lib.ASSEMBLY_SPLIT}[alg]
+                "split": _lib.ASSEMBLY_SPLIT, "class": _lib.ASSEMBLY_CLASS}[alg]
         _lib.check(_lib.lib.sphp_amap_set_algorithm(self._h, code), AssemblyError)
         return self
 

@@ -1074,7 +1074,7 @@ static int amap_device(const sphp_amap* ac) {
 // local (E, nm) -> global with the map's algorithm; accumulate adds to g
 static int amap_assemble_any(const sphp_amap* a, const double* loc, double* g, int accumulate,
                              cudaStream_t s, int mode_major = 0) {
-  if (a->alg == SPHP_ASSEMBLY_OWNER || a->alg == SPHP_ASSEMBLY_SPLIT) {
+  if (a->alg == SPHP_ASSEMBLY_OWNER || a->alg == SPHP_ASSEMBLY_SPLIT || a->alg == SPHP_ASSEMBLY_CLASS) {
     if (a->periodic) {
       CK(owner_assemble_periodic(a->n, a->P, loc, g, accumulate, mode_major, s));
     } else {
@@ -1219,8 +1219,11 @@ int sphp_hexmap_variable(int n, const int* orders, int64_t* num_global, int64_t*
 
 int sphp_amap_set_algorithm(sphp_amap* a, int alg) {
   if (!a) return fail(SPHP_ERR_BAD_ARG, "null map");
-  if (alg != SPHP_ASSEMBLY_OWNER && alg != SPHP_ASSEMBLY_COLOUR && alg != SPHP_ASSEMBLY_SPLIT)
+  if (alg != SPHP_ASSEMBLY_OWNER && alg != SPHP_ASSEMBLY_COLOUR && alg != SPHP_ASSEMBLY_SPLIT &&
+      alg != SPHP_ASSEMBLY_CLASS)
     return fail(SPHP_ERR_BAD_ARG, "unknown assembly algorithm");
+  if (alg == SPHP_ASSEMBLY_CLASS && !a->periodic)
+    return fail(SPHP_ERR_UNSUPPORTED, "class-range assembly needs a periodic map");
   a->alg = alg;
   return SPHP_OK;
 }
@@ -1300,7 +1303,26 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
   OpArgs o = base_args(c);
   o.xg = x;
   o.yg = y;
-  if (a->alg == SPHP_ASSEMBLY_SPLIT) {
+  if (a->alg == SPHP_ASSEMBLY_CLASS) {
+    // the operator gathers x by entity-class ranges and writes a class-major
+    // block (interiors straight into y), then one owner-computes sum over it
+    // (two launches, the local block never exists)
+    CK(c->loc_y.ensure(sizeof(double) * class_block_doubles(a->n, a->P)));
+    o.mode = AsmMode::PERIODIC_CLASS;
+    o.n = a->n;
+    o.zbuf = c->loc_y.as<double>();
+    o.direct_interior = accumulate ? 0 : 1;
+    int ne = 0;
+    o.ne_out = &ne;
+    cudaError_t e = sumfac_launch(c, o, s);
+    if (e == cudaSuccess) {
+      CK(class_owner_sum(a->n, a->P, ne, o.zbuf, y, accumulate, !o.direct_interior, s));
+      return SPHP_OK;
+    }
+    if (e != cudaErrorNotSupported) return cuda_fail(e, "sphp_helmholtz_assembled");
+    // no class-mode tile for this key / mesh: the split algorithm below
+  }
+  if (a->alg == SPHP_ASSEMBLY_SPLIT || a->alg == SPHP_ASSEMBLY_CLASS) {
     // scatter -> fused local operator -> owner-computes sum (three launches;
     // the fused kernel then runs in its block-input form)
     CK(c->loc_x.ensure(sizeof(double) * c->E * c->t->nm));

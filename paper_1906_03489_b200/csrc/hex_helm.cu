@@ -42,8 +42,40 @@ static int helm_variant_env() {
 // one input stage and ~74 KB (local) / ~55 KB (gathering modes) per CTA
 // beat double buffering at every order: more resident CTAs hide more latency
 // than a second stage does.  SPHP_HELM_VARIANT=0..4 overrides for tuning.
+// PERIODIC_CLASS (pipeline MODE 5) needs an even NE dividing n: the largest
+// of 8 / 4 / 2 elements whose tile fits the budget (SPHP_CLASS_BUDGET_KB,
+// default 74 KB: three resident CTAs per SM at P = 4)
+#ifndef SPHP_CLASS_BUDGET_KB
+#define SPHP_CLASS_BUDGET_KB 75
+#endif
+template <int M, int Q, int GK, int NE>
+constexpr size_t class_smem() {
+  using Op = HexHelm<M, Q, GK, NE, choose_nt(NE, Q * Q), 1>;
+  return Scaffold<Op, 5>::SMEM_BYTES;
+}
+template <int M, int Q, int GK>
+constexpr int class_ne() {
+  return class_smem<M, Q, GK, 8>() <= SPHP_CLASS_BUDGET_KB * 1024 && 8 * Q * Q <= 512   ? 8
+         : class_smem<M, Q, GK, 4>() <= SPHP_CLASS_BUDGET_KB * 1024 && 4 * Q * Q <= 512 ? 4
+                                                                                          : 2;
+}
+template <int M, int Q, int GK>
+static cudaError_t helm_class(const OpArgs& oa, cudaStream_t s) {
+  constexpr int NE = class_ne<M, Q, GK>();
+  if constexpr (M < 3 || class_smem<M, Q, GK, NE>() > 227 * 1024) {
+    return cudaErrorNotSupported;  // not even a two-element tile fits: split
+  } else {
+    constexpr int NT = choose_nt(NE, Q * Q);
+    using Op = HexHelm<M, Q, GK, NE, NT, 1>;
+    if (M < 3 || oa.n % NE != 0 || oa.n % 2 != 0 || oa.E % NE != 0) return cudaErrorNotSupported;
+    if (oa.ne_out) *oa.ne_out = NE;
+    return launch_pipe<Op, 5>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
+  }
+}
+
 template <int M, int Q, int GK>
 static cudaError_t helm_go(const OpArgs& oa, cudaStream_t s) {
+  if (oa.mode == AsmMode::PERIODIC_CLASS) return helm_class<M, Q, GK>(oa, s);
   if (oa.mode == AsmMode::LOCAL || oa.mode == AsmMode::PERIODIC_GATHER) {
 #ifdef SPHP_TUNING  // tile-shape sweep build (make EXTRA_NVFLAGS=-DSPHP_TUNING)
     switch (helm_variant_env()) {

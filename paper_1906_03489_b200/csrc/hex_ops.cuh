@@ -221,394 +221,11 @@ struct Rot {
 //   S7 i->p   T2'[p,j,k] = B t + dB f0          pencils (j,k)
 //   S8 j->q, S9 k->r    -> y[p,q,r]
 // ===========================================================================
-template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
-struct HexHelmK {
-  static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
-  static constexpr int NSTP = NSTP_;  // preferred input stages (1 or 2)
-  static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
-  static constexpr int IN = M3, OUT = M3;
-  static constexpr int CS = pt_stride(Q3);
-  static constexpr int GEO = (GK == SPHP_GEOM_METRIC) ? 7 * CS : 10;
-  static constexpr int QK = odd_up(Q);  // T1 row pitch (odd: row stores conflict free)
-  // plane pitches congruent to Q mod 16: lanes (p, k) then address
-  // consecutive banks in the q/j-pencil stages
-  static constexpr int PP1 = pitch_mod16(M * QK, Q);  // T1[p][q][k]
-  static constexpr int PP2 = pitch_mod16(Q * Q, Q);   // T2[p][j][k], rows of Q
-  static constexpr int SE = even_up(cmax(Q3, cmax(M * PP1, M * PP2)));  // element stride
-  static constexpr int WORK = 3 * SE;
-  using T = Tab<M, Q>;
-
-  template <class R, class W>
-  __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
-                                 double* __restrict__ work, double* __restrict__ out, double lam,
-                                 R release, W pre_out, const double* tab) {
-    double* W0 = work;                // T1 | u, t | T1'
-    double* W1 = work + NE * SE;      // T2 | d1, f1 | T2'
-    double* W2 = work + 2 * NE * SE;  // d0, f0
-
-    // S1: r-contraction  c[p,q,r] -> T1[p,q,k]
-    SPHP_FOR_ITEMS(NE * M * M, w) {
-      int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
-      pencil<M, Q, T::B, 1, Q, 1, 1, false>(tab, cin + e * M3 + pq * M,
-                                            W0 + e * SE + p * PP1 + q * QK);
-    }
-    __syncthreads();
-    // S2: q-contraction  T1[p,q,k] -> T2[p,j,k]
-    SPHP_FOR_ITEMS(NE * M * Q, w) {
-      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
-      pencil<M, Q, T::B, 1, Q, QK, Q, false>(tab, W0 + e * SE + p * PP1 + k,
-                                             W1 + e * SE + p * PP2 + k);
-    }
-    __syncthreads();
-    // S3: p-contraction  T2 -> u (W0) and d0 (W2), dense (i,j,k)
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
-      const double* src = W1 + e * SE + jk;
-      double x[M];
-#pragma unroll
-      for (int p = 0; p < M; ++p) x[p] = src[p * PP2];
-      double* du = W0 + e * SE + jk;
-      double* d0 = W2 + e * SE + jk;
-#pragma unroll
-      for (int i = 0; i < Q; ++i) {
-        double a = 0.0, b = 0.0;
-#pragma unroll
-        for (int p = 0; p < M; ++p) {
-          a = fma(tab[T::B + p * Q + i], x[p], a);
-          b = fma(tab[T::BD + p * Q + i], x[p], b);
-        }
-        du[i * Q * Q] = a;
-        d0[i * Q * Q] = b;
-      }
-    }
-    __syncthreads();
-    // S4: d1 = D along j of u
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
-      pencil<Q, Q, T::D, Q, 1, Q, Q, false>(tab, W0 + e * SE + i * Q * Q + k,
-                                            W1 + e * SE + i * Q * Q + k);
-    }
-    __syncthreads();
-    // S5: rows along k: d2, fluxes, mass, t = lam wJ u + D2^T f2
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      int e = w / (Q * Q), ij = w - e * (Q * Q), i = ij / Q, j = ij - i * Q;
-      const int row = e * SE + ij * Q;
-      double u[Q], d[Q], f0[Q], f1[Q], f2[Q], g[Q];
-      load_row<Q>(W0 + row, u);
-      // d2 = D u (registers)
-      double d2[Q];
-#pragma unroll
-      for (int k = 0; k < Q; ++k) {
-        double acc = 0.0;
-#pragma unroll
-        for (int l = 0; l < Q; ++l) acc = fma(tab[T::D + k * Q + l], u[l], acc);
-        d2[k] = acc;
-      }
-      if constexpr (GK == SPHP_GEOM_METRIC) {
-        const double* gr = geo + e * GEO + ij * Q;
-        load_row<Q>(W2 + row, d);  // d0
-        load_row<Q>(gr + 0 * CS, g);  // G00
-#pragma unroll
-        for (int k = 0; k < Q; ++k) f0[k] = g[k] * d[k];
-        load_row<Q>(gr + 1 * CS, g);  // G01
-#pragma unroll
-        for (int k = 0; k < Q; ++k) f1[k] = g[k] * d[k];
-        double h[Q];
-        load_row<Q>(W1 + row, h);  // d1
-#pragma unroll
-        for (int k = 0; k < Q; ++k) f0[k] = fma(g[k], h[k], f0[k]);
-        load_row<Q>(gr + 2 * CS, g);  // G02
-#pragma unroll
-        for (int k = 0; k < Q; ++k) {
-          f2[k] = g[k] * d[k];
-          f0[k] = fma(g[k], d2[k], f0[k]);
-        }
-        load_row<Q>(gr + 3 * CS, g);  // G11
-#pragma unroll
-        for (int k = 0; k < Q; ++k) f1[k] = fma(g[k], h[k], f1[k]);
-        load_row<Q>(gr + 4 * CS, g);  // G12
-#pragma unroll
-        for (int k = 0; k < Q; ++k) {
-          f1[k] = fma(g[k], d2[k], f1[k]);
-          f2[k] = fma(g[k], h[k], f2[k]);
-        }
-        load_row<Q>(gr + 5 * CS, g);  // G22
-#pragma unroll
-        for (int k = 0; k < Q; ++k) f2[k] = fma(g[k], d2[k], f2[k]);
-        load_row<Q>(gr + 6 * CS, g);  // wJ
-#pragma unroll
-        for (int k = 0; k < Q; ++k) u[k] = lam * g[k] * u[k];
-      } else {
-        // affine: G_ab = w_i w_j w_k det sum_c inv[a,c] inv[b,c]
-        const double* gg = geo + e * GEO;
-        const double det = gg[0];
-        const double* iv = gg + 1;
-        const double a00 = det * (iv[0] * iv[0] + iv[1] * iv[1] + iv[2] * iv[2]);
-        const double a01 = det * (iv[0] * iv[3] + iv[1] * iv[4] + iv[2] * iv[5]);
-        const double a02 = det * (iv[0] * iv[6] + iv[1] * iv[7] + iv[2] * iv[8]);
-        const double a11 = det * (iv[3] * iv[3] + iv[4] * iv[4] + iv[5] * iv[5]);
-        const double a12 = det * (iv[3] * iv[6] + iv[4] * iv[7] + iv[5] * iv[8]);
-        const double a22 = det * (iv[6] * iv[6] + iv[7] * iv[7] + iv[8] * iv[8]);
-        const double wij = tab[T::W + i] * tab[T::W + j];
-        load_row<Q>(W2 + row, d);
-        double h[Q];
-        load_row<Q>(W1 + row, h);
-#pragma unroll
-        for (int k = 0; k < Q; ++k) {
-          const double wq = wij * tab[T::W + k];
-          f0[k] = wq * (a00 * d[k] + a01 * h[k] + a02 * d2[k]);
-          f1[k] = wq * (a01 * d[k] + a11 * h[k] + a12 * d2[k]);
-          f2[k] = wq * (a02 * d[k] + a12 * h[k] + a22 * d2[k]);
-          u[k] = lam * (wq * det) * u[k];
-        }
-      }
-      // t = mass + D2^T f2
-#pragma unroll
-      for (int k = 0; k < Q; ++k) {
-        double t = u[k];
-#pragma unroll
-        for (int l = 0; l < Q; ++l) t = fma(tab[T::D + l * Q + k], f2[l], t);
-        g[k] = t;
-      }
-      store_row<Q>(W0 + row, g);
-      store_row<Q>(W2 + row, f0);
-      store_row<Q>(W1 + row, f1);
-    }
-    __syncthreads();
-    release();
-    // S6: t += D1^T f1 along j
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
-      pencil<Q, Q, T::D, 1, Q, Q, Q, true>(tab, W1 + e * SE + i * Q * Q + k,
-                                           W0 + e * SE + i * Q * Q + k);
-    }
-    __syncthreads();
-    // S7: i -> p: T2'[p,j,k] = sum_i B[p,i] t + Bd[p,i] f0   (into W1)
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
-      const int base = e * SE + jk;
-      double t[Q], f0[Q];
-#pragma unroll
-      for (int i = 0; i < Q; ++i) {
-        t[i] = W0[base + i * Q * Q];
-        f0[i] = W2[base + i * Q * Q];
-      }
-#pragma unroll
-      for (int p = 0; p < M; ++p) {
-        double acc = 0.0;
-#pragma unroll
-        for (int i = 0; i < Q; ++i) {
-          acc = fma(tab[T::B + p * Q + i], t[i], acc);
-          acc = fma(tab[T::BD + p * Q + i], f0[i], acc);
-        }
-        W1[e * SE + p * PP2 + jk] = acc;
-      }
-    }
-    __syncthreads();
-    // S8: j -> q  (W1 -> W0)
-    SPHP_FOR_ITEMS(NE * M * Q, w) {
-      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
-      pencil<Q, M, T::B, Q, 1, Q, QK, false>(tab, W1 + e * SE + p * PP2 + k,
-                                             W0 + e * SE + p * PP1 + k);
-    }
-    pre_out();
-    __syncthreads();
-    // S9: k -> r  (W0 -> out, dense)
-    SPHP_FOR_ITEMS(NE * M * M, w) {
-      int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
-      pencil<Q, M, T::B, Q, 1, 1, 1, false>(tab, W0 + e * SE + p * PP1 + q * QK,
-                                            out + e * M3 + pq * M);
-    }
-  }
-};
 
 // ===========================================================================
-// Fused Helmholtz, variant J: the pointwise stage runs on pencils along j
-// (used when Q % 4 == 0, where contiguous k-rows of Q doubles map every
-// 128-bit access of an 8-lane phase to two bank groups).
-// GK: SPHP_GEOM_METRIC (7 per-point comps) or SPHP_GEOM_AFFINE (det, inv).
-// ===========================================================================
-template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
-struct HexHelmJ {
-  static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
-  static constexpr int NSTP = NSTP_;  // preferred input stages (1 or 2)
-  static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
-  static constexpr int IN = M3, OUT = M3;
-  static constexpr int CS = pt_stride(Q3);
-  static constexpr int GEO = (GK == SPHP_GEOM_METRIC) ? 7 * CS : 10;
-  static constexpr int QK = odd_up(Q);
-  static constexpr int SW = odd_up(Q * Q * QK);
-  static constexpr int WORK = 3 * SW;
-  using T = Tab<M, Q>;
-
-  template <class R, class W>
-  __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
-                                 double* __restrict__ work, double* __restrict__ out, double lam,
-                                 R release, W pre_out, const double* tab) {
-    double* W0 = work;            // T1 (M,M,QK) | u / t (Q,Q,QK)
-    double* W1 = work + NE * SW;  // T2 (M,Q,QK) | d2 / f2
-    double* W2 = work + 2 * NE * SW;  // d0 / f0
-
-    // S1: r-contraction  c[p,q,r] -> T1[p,q,k]
-    SPHP_FOR_ITEMS(NE * M * M, w) {
-      int e = w / (M * M), pq = w - e * (M * M);
-      pencil<M, Q, T::B, 1, Q, 1, 1, false>(tab, cin + e * M3 + pq * M, W0 + e * SW + pq * QK);
-    }
-    __syncthreads();
-    // S2: q-contraction  T1[p,q,k] -> T2[p,j,k]
-    SPHP_FOR_ITEMS(NE * M * Q, w) {
-      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
-      pencil<M, Q, T::B, 1, Q, QK, QK, false>(tab, W0 + e * SW + p * M * QK + k,
-                                              W1 + e * SW + p * Q * QK + k);
-    }
-    __syncthreads();
-    // S3: p-contraction  T2 -> u (W0) and d0 = Bd-contraction (W2)
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
-      const double* src = W1 + e * SW + j * QK + k;
-      double x[M];
-#pragma unroll
-      for (int p = 0; p < M; ++p) x[p] = src[p * Q * QK];
-      double* du = W0 + e * SW + j * QK + k;
-      double* d0 = W2 + e * SW + j * QK + k;
-#pragma unroll
-      for (int i = 0; i < Q; ++i) {
-        double a = 0.0, b = 0.0;
-#pragma unroll
-        for (int p = 0; p < M; ++p) {
-          a = fma(tab[T::B + p * Q + i], x[p], a);
-          b = fma(tab[T::BD + p * Q + i], x[p], b);
-        }
-        du[i * Q * QK] = a;
-        d0[i * Q * QK] = b;
-      }
-    }
-    __syncthreads();
-    // S4: d2 = D along k of u
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      int e = w / (Q * Q), ij = w - e * (Q * Q);
-      pencil<Q, Q, T::D, Q, 1, 1, 1, false>(tab, W0 + e * SW + ij * QK, W1 + e * SW + ij * QK);
-    }
-    __syncthreads();
-    // S5: pencil along j: d1 = D u, fluxes f = G grad u, t = lam wJ u + D1^T f1
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
-      const int base = e * SW + i * Q * QK + k;
-      double u[Q], f1[Q];
-#pragma unroll
-      for (int j = 0; j < Q; ++j) u[j] = W0[base + j * QK];
-      const double* g = geo + e * GEO;
-      double a00, a01, a02, a11, a12, a22, adet;
-      if (GK == SPHP_GEOM_AFFINE) {
-        // G_ab = det * sum_k inv[a,k] inv[b,k] (point weights applied below)
-        const double det = g[0];
-        const double* iv = g + 1;
-        a00 = det * (iv[0] * iv[0] + iv[1] * iv[1] + iv[2] * iv[2]);
-        a01 = det * (iv[0] * iv[3] + iv[1] * iv[4] + iv[2] * iv[5]);
-        a02 = det * (iv[0] * iv[6] + iv[1] * iv[7] + iv[2] * iv[8]);
-        a11 = det * (iv[3] * iv[3] + iv[4] * iv[4] + iv[5] * iv[5]);
-        a12 = det * (iv[3] * iv[6] + iv[4] * iv[7] + iv[5] * iv[8]);
-        a22 = det * (iv[6] * iv[6] + iv[7] * iv[7] + iv[8] * iv[8]);
-        adet = det;
-      }
-      double d1v[Q];
-#pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        double acc = 0.0;
-#pragma unroll
-        for (int l = 0; l < Q; ++l) acc = fma(tab[T::D + j * Q + l], u[l], acc);
-        d1v[j] = acc;
-      }
-#pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        const double d1 = d1v[j];
-        const double d0 = W2[base + j * QK];
-        const double d2 = W1[base + j * QK];
-        double G00, G01, G02, G11, G12, G22, wj;
-        if (GK == SPHP_GEOM_METRIC) {
-          const int pt = metric_slot(3, Q, (i * Q + j) * Q + k);
-          G00 = g[0 * CS + pt];
-          G01 = g[1 * CS + pt];
-          G02 = g[2 * CS + pt];
-          G11 = g[3 * CS + pt];
-          G12 = g[4 * CS + pt];
-          G22 = g[5 * CS + pt];
-          wj = g[6 * CS + pt];
-        } else {
-          const double wq = tab[T::W + i] * tab[T::W + j] * tab[T::W + k];
-          G00 = wq * a00;
-          G01 = wq * a01;
-          G02 = wq * a02;
-          G11 = wq * a11;
-          G12 = wq * a12;
-          G22 = wq * a22;
-          wj = wq * adet;
-        }
-        const double f0 = G00 * d0 + G01 * d1 + G02 * d2;
-        f1[j] = G01 * d0 + G11 * d1 + G12 * d2;
-        const double f2 = G02 * d0 + G12 * d1 + G22 * d2;
-        W2[base + j * QK] = f0;
-        W1[base + j * QK] = f2;
-        u[j] = lam * wj * u[j];  // mass term, reuses u's registers
-      }
-#pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        double t = u[j];
-#pragma unroll
-        for (int l = 0; l < Q; ++l) t = fma(tab[T::D + l * Q + j], f1[l], t);
-        W0[base + j * QK] = t;
-      }
-    }
-    __syncthreads();
-    release();
-    // S6: t += D2^T f2 along k
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      int e = w / (Q * Q), ij = w - e * (Q * Q);
-      pencil<Q, Q, T::D, 1, Q, 1, 1, true>(tab, W1 + e * SW + ij * QK, W0 + e * SW + ij * QK);
-    }
-    __syncthreads();
-    // S7: i -> p: T2'[p,j,k] = sum_i B[p,i] t + Bd[p,i] f0   (into W1)
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
-      const int base = e * SW + j * QK + k;
-      double t[Q], f0[Q];
-#pragma unroll
-      for (int i = 0; i < Q; ++i) {
-        t[i] = W0[base + i * Q * QK];
-        f0[i] = W2[base + i * Q * QK];
-      }
-#pragma unroll
-      for (int p = 0; p < M; ++p) {
-        double acc = 0.0;
-#pragma unroll
-        for (int i = 0; i < Q; ++i) {
-          acc = fma(tab[T::B + p * Q + i], t[i], acc);
-          acc = fma(tab[T::BD + p * Q + i], f0[i], acc);
-        }
-        W1[e * SW + p * Q * QK + j * QK + k] = acc;
-      }
-    }
-    __syncthreads();
-    // S8: j -> q  (W1 -> W0)
-    SPHP_FOR_ITEMS(NE * M * Q, w) {
-      int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
-      pencil<Q, M, T::B, Q, 1, QK, QK, false>(tab, W1 + e * SW + p * Q * QK + k,
-                                              W0 + e * SW + p * M * QK + k);
-    }
-    pre_out();
-    __syncthreads();
-    // S9: k -> r  (W0 -> out, dense)
-    SPHP_FOR_ITEMS(NE * M * M, w) {
-      int e = w / (M * M), pq = w - e * (M * M);
-      pencil<Q, M, T::B, Q, 1, 1, 1, false>(tab, W0 + e * SW + pq * QK, out + e * M3 + pq * M);
-    }
-  }
-};
-
-// ===========================================================================
-// Fused Helmholtz, K-row plan with even-odd contractions (HexHelmEO): the
-// same stages, layouts and memory traffic as HexHelmK, every 1D contraction
-// evaluated through eo.cuh (half the DFMAs and table loads).
+// Fused Helmholtz, K-row plan (HexHelmEO): the stages above, every 1D
+// contraction evaluated through eo.cuh (half the DFMAs and table loads of
+// the plain pencil form).
 // ===========================================================================
 template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
 struct HexHelmEO {
@@ -650,10 +267,11 @@ struct HexHelmEO {
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
 
-  template <class R, class W>
+  template <class R, class W, class IO = BlockIO, class H = NoHook>
   __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
                                  double* __restrict__ work, double* __restrict__ out, double lam,
-                                 R release, W pre_out, const double* tab) {
+                                 R release, W pre_out, const double* tab, IO io = IO(),
+                                 IO oio = IO(), H after_in = H()) {
     double* W0 = work;
     double* W1 = work + NE * SE;
     double* W2 = work + 2 * NE * SE;
@@ -661,11 +279,15 @@ struct HexHelmEO {
     SPHP_FOR_ITEMS(NE * M * M, w) {
       int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
       double x[M], u[Q];
-      RowRot<M>::load(cin + e * M3 + pq * M, w, x);
+      if constexpr (IO::DENSE)
+        RowRot<M>::load(cin + e * M3 + pq * M, w, x);
+      else
+        io.template load_row<M>(cin, e, pq, x);
       X::interp(tab, x, u);
       st_pencil<Q, 1>(W0 + e * SE + p * PP1 + q * QK, u);
     }
     __syncthreads();
+    after_in();
     // S2: q -> j
     SPHP_FOR_ITEMS(NE * M * Q, w) {
       int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
@@ -809,14 +431,19 @@ struct HexHelmEO {
       double v[Q], c[M];
       ld_pencil<Q, 1>(W0 + e * SE + p * PP1 + q * QK, v);
       X::project(tab, v, c);
-      RowRot<M>::store(out + e * M3 + pq * M, w, c);
+      if constexpr (IO::DENSE)
+        RowRot<M>::store(out + e * M3 + pq * M, w, c);
+      else
+        oio.template store_row<M>(out, e, pq, c);
     }
   }
 };
 
 // ===========================================================================
-// Fused Helmholtz, J-pencil plan with even-odd contractions (Q % 4 == 0):
-// HexHelmJ's stages and layouts, 1D contractions through eo.cuh.
+// Fused Helmholtz, J-pencil plan with even-odd contractions (Q % 4 == 0,
+// where contiguous k-rows of Q doubles would map every 128-bit access of an
+// 8-lane phase to two bank groups): the pointwise stage runs on pencils
+// along j; 1D contractions through eo.cuh.
 // ===========================================================================
 template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
 struct HexHelmJEO {
@@ -833,21 +460,26 @@ struct HexHelmJEO {
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
 
-  template <class R, class W>
+  template <class R, class W, class IO = BlockIO, class H = NoHook>
   __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
                                  double* __restrict__ work, double* __restrict__ out, double lam,
-                                 R release, W pre_out, const double* tab) {
+                                 R release, W pre_out, const double* tab, IO io = IO(),
+                                 IO oio = IO(), H after_in = H()) {
     double* W0 = work;
     double* W1 = work + NE * SW;
     double* W2 = work + 2 * NE * SW;
     SPHP_FOR_ITEMS(NE * M * M, w) {  // S1 r -> k
       int e = w / (M * M), pq = w - e * (M * M);
       double x[M], u[Q];
-      ld_pencil<M, 1>(cin + e * M3 + pq * M, x);
+      if constexpr (IO::DENSE)
+        ld_pencil<M, 1>(cin + e * M3 + pq * M, x);
+      else
+        io.template load_row<M>(cin, e, pq, x);
       X::interp(tab, x, u);
       st_pencil<Q, 1>(W0 + e * SW + pq * QK, u);
     }
     __syncthreads();
+    after_in();
     SPHP_FOR_ITEMS(NE * M * Q, w) {  // S2 q -> j
       int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
       double x[M], u[Q];
@@ -959,7 +591,10 @@ struct HexHelmJEO {
       double v[Q], c[M];
       ld_pencil<Q, 1>(W0 + e * SW + pq * QK, v);
       X::project(tab, v, c);
-      st_pencil<M, 1>(out + e * M3 + pq * M, c);
+      if constexpr (IO::DENSE)
+        st_pencil<M, 1>(out + e * M3 + pq * M, c);
+      else
+        oio.template store_row<M>(out, e, pq, c);
     }
   }
 };
@@ -1009,10 +644,11 @@ struct HexHelmQ4 {
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
 
-  template <class R, class W>
+  template <class R, class W, class IO = BlockIO, class H = NoHook>
   __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
                                  double* __restrict__ work, double* __restrict__ out, double lam,
-                                 R release, W pre_out, const double* tab) {
+                                 R release, W pre_out, const double* tab, IO io = IO(),
+                                 IO oio = IO(), H after_in = H()) {
     double* W0 = work;
     double* W1 = work + NE * ES;
     double* W2 = work + 2 * NE * ES;
@@ -1020,13 +656,17 @@ struct HexHelmQ4 {
     SPHP_FOR_ITEMS(NE * M * M, w) {
       const int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
       double x[M], u[Q];
-      ld_pencil<M, 1>(cin + e * M3 + pq * M, x);
+      if constexpr (IO::DENSE)
+        ld_pencil<M, 1>(cin + e * M3 + pq * M, x);
+      else
+        io.template load_row<M>(cin, e, pq, x);
       X::interp(tab, x, u);
       double* d = W0 + e * ES;
 #pragma unroll
       for (int k = 0; k < Q; ++k) d[q4_off(p, q, k)] = u[k];
     }
     __syncthreads();
+    after_in();
     // S2: q -> j
     SPHP_FOR_ITEMS(NE * M * Q, w) {
       const int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
@@ -1201,23 +841,21 @@ struct HexHelmQ4 {
 #pragma unroll
       for (int k = 0; k < Q; ++k) x[k] = s[q4_off(p, q, k)];
       X::project(tab, x, c);
-      st_pencil<M, 1>(out + e * M3 + pq * M, c);
+      if constexpr (IO::DENSE)
+        st_pencil<M, 1>(out + e * M3 + pq * M, c);
+      else
+        oio.template store_row<M>(out, e, pq, c);
     }
   }
 };
 
-// variant selection: k-row pointwise stage unless Q % 4 == 0
-#ifndef SPHP_HELM_K_PLAIN
+// variant selection: skewed Q = 4 layout, j-pencil plan at Q % 4 == 0,
+// k-row plan otherwise
 template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
 using HexHelm = typename std::conditional<
     (Q_ == 4), HexHelmQ4<M_, Q_, GK, NE_, NT_, NSTP_>,
     typename std::conditional<(Q_ % 4 == 0), HexHelmJEO<M_, Q_, GK, NE_, NT_, NSTP_>,
                               HexHelmEO<M_, Q_, GK, NE_, NT_, NSTP_>>::type>::type;
-#else
-template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
-using HexHelm = typename std::conditional<(Q_ % 4 == 0), HexHelmJ<M_, Q_, GK, NE_, NT_, NSTP_>,
-                                          HexHelmK<M_, Q_, GK, NE_, NT_, NSTP_>>::type;
-#endif
 
 // ===========================================================================
 // BwdTrans (K1): u = (B x B x B)^T c   (collections.py:133-150)

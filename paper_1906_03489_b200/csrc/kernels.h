@@ -11,7 +11,19 @@ namespace sphp {
 // LOCAL: block in/out.  PERIODIC / EXPLICIT: one colour class, gather in,
 // scatter-add out.  PERIODIC_GATHER / EXPLICIT_GATHER: all elements, gather
 // in, local block out (the owner-computes assembly then sums it).
-enum class AsmMode : int { LOCAL = 0, PERIODIC = 1, EXPLICIT = 2, PERIODIC_GATHER = 3, EXPLICIT_GATHER = 4 };
+// PERIODIC_CLASS: periodic hex, all elements in order: the tile's modes are
+// gathered by entity-class ranges of the global vector (16-byte cp.async
+// chunks) and the results leave, class-major within each tile, into the
+// tile-major block Z (the interiors straight into y), which
+// class_owner_sum then reduces.
+enum class AsmMode : int {
+  LOCAL = 0,
+  PERIODIC = 1,
+  EXPLICIT = 2,
+  PERIODIC_GATHER = 3,
+  EXPLICIT_GATHER = 4,
+  PERIODIC_CLASS = 5
+};
 
 struct OpArgs {
   int M, Q;          // modes / points per direction
@@ -34,6 +46,14 @@ struct OpArgs {
   int n;              // PERIODIC: grid size
   int colour;         // PERIODIC: colour id 0..7
   int reverse = 0;    // LOCAL: walk the tiles last to first
+  // PERIODIC_CLASS: absolute index of the launch's first element (z-slab
+  // pipelines), the output block Z (per tile of NE elements: classes 0..25,
+  // class-major, NE * (nm - (P-1)^3) doubles; then n^3 (P-1)^3 interior
+  // values when they do not go straight into yg)
+  int64_t e0 = 0;
+  double* zbuf = nullptr;
+  int direct_interior = 0;
+  int* ne_out = nullptr;  // PERIODIC_CLASS: receives the tile size NE (Z layout)
 };
 
 // hex (3D) sum-factorisation kernels

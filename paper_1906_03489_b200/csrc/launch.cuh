@@ -77,6 +77,9 @@ cudaError_t launch_pipe(const OpArgs& oa, int64_t gstride, int64_t goff, cudaStr
   a.n = oa.n;
   a.colour = oa.colour;
   a.reverse = oa.reverse;
+  a.e0 = oa.e0;
+  a.zbuf = oa.zbuf;
+  a.direct_interior = oa.direct_interior;
   const int64_t count = (MODE == 0 || MODE >= 3) ? oa.E : oa.nlist;
   if (count <= 0) return cudaSuccess;
   const int64_t ntiles = (count + Op::NE - 1) / Op::NE;
@@ -115,6 +118,8 @@ cudaError_t launch_mode(const OpArgs& oa, int64_t gstride, int64_t goff, cudaStr
       return launch_pipe<Op, 3>(oa, gstride, goff, s);
     case AsmMode::EXPLICIT_GATHER:
       return launch_pipe<Op, 4>(oa, gstride, goff, s);
+    case AsmMode::PERIODIC_CLASS:
+      return cudaErrorNotSupported;  // Helmholtz only (hex_helm.cu: helm_class)
   }
   return cudaErrorInvalidValue;
 }

@@ -41,6 +41,12 @@ cudaError_t jacobian_factors(int64_t E, int64_t np, const double* dx, const doub
 // class-range kernels (periodic_ops.cu) over the x-rows [row0, row1) of
 // rows ey + n ez (row1 < 0: all); cudaErrorNotSupported if the grid or
 // order is outside their range
+// block Z of the PERIODIC_CLASS operator mode (tiles of ne elements):
+// doubles needed, and its owner-computes sum into y (rows [row0, row1) of
+// (ey, ez); with or without the interior region)
+int64_t class_block_doubles(int n, int P);
+cudaError_t class_owner_sum(int n, int P, int ne, const double* Z, double* y, int accumulate,
+                            int with_interior, cudaStream_t s, int row0 = 0, int row1 = -1);
 cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int accumulate,
                               cudaStream_t s, int row0 = 0, int row1 = -1);
 cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cudaStream_t s,

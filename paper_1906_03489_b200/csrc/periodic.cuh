@@ -43,6 +43,52 @@ __device__ __forceinline__ int mode_code(int M, int nl) {
   return cls | (off << 5);
 }
 
+// ---------------------------------------------------------------------------
+// Entity classes in closed form: class k of element (x, y, z) is the entity
+// R + size * vid(x + dx, y + dy, z + dz) (periodic wrap), the form that the
+// class-range kernels (periodic_ops.cu, pipeline MODE 5) evaluate per
+// segment / tile with a few integer ops.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int class_size(int k, int b) {
+  return k < 8 ? 1 : (k < 20 ? b : (k < 26 ? b * b : b * b * b));
+}
+// does class k's entity sit at x + 1 (the element's high-x side)?
+__host__ __device__ __forceinline__ int class_dx(int k) {
+  return k < 8    ? (k >> 2)
+         : k < 20 ? ((((k - 8) >> 2) != 0) ? ((k - 8) >> 1) & 1 : 0)  // edge off the x axis
+         : k < 26 ? ((((k - 20) >> 1) == 0) ? (k - 20) & 1 : 0)       // x-normal face
+                  : 0;
+}
+// class k's entity of element (x, y, z) is gid = R + size * vid(x + dx,
+// y + dy, z + dz) (periodic wrap): the closed form of entity_base
+// (periodic.cuh) that per-segment code evaluates with a few integer ops
+struct ClassGeom {
+  int R, s, d;  // region base, entity size, dx | dy << 1 | dz << 2
+};
+__host__ __device__ __forceinline__ ClassGeom class_geom(int k, int n, int P) {
+  const int N3 = n * n * n, b = P - 1;
+  if (k < 8) return {0, 1, ((k >> 2) & 1) | (((k >> 1) & 1) << 1) | ((k & 1) << 2)};
+  if (k < 20) {
+    const int j = k - 8, dir = j >> 2, s0 = (j >> 1) & 1, s1 = j & 1;
+    // the two shifts go to the axes other than dir, in order
+    const int d = dir == 0 ? (s0 << 1) | (s1 << 2) : (dir == 1 ? s0 | (s1 << 2) : s0 | (s1 << 1));
+    return {N3 + dir * N3 * b, b, d};
+  }
+  if (k < 26) {
+    const int j = k - 20, dir = j >> 1, side = j & 1;
+    return {N3 + 3 * N3 * b + dir * N3 * b * b, b * b, side << dir};
+  }
+  return {N3 * (1 + 3 * b + 3 * b * b), b * b * b, 0};
+}
+__host__ __device__ __forceinline__ int class_gid(const ClassGeom& g, int n, int x, int y, int z) {
+  x += g.d & 1;
+  y += (g.d >> 1) & 1;
+  z += (g.d >> 2) & 1;
+  x -= x >= n ? n : 0;
+  y -= y >= n ? n : 0;
+  z -= z >= n ? n : 0;
+  return g.R + g.s * (x + n * (y + n * z));
+}
 __device__ __forceinline__ int entity_base(int n, int P, int ex, int ey, int ez, int k) {
   const int N3 = n * n * n, b = P - 1;
   auto wrap = [n](int i) { return i >= n ? i - n : i; };

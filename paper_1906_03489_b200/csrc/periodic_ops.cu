@@ -31,46 +31,6 @@ namespace {
 
 constexpr int kThreads = 256;
 
-__device__ __forceinline__ int class_size(int k, int b) {
-  return k < 8 ? 1 : (k < 20 ? b : (k < 26 ? b * b : b * b * b));
-}
-// does class k's entity sit at x + 1 (the element's high-x side)?
-__device__ __forceinline__ int class_dx(int k) {
-  return k < 8    ? (k >> 2)
-         : k < 20 ? ((((k - 8) >> 2) != 0) ? ((k - 8) >> 1) & 1 : 0)  // edge off the x axis
-         : k < 26 ? ((((k - 20) >> 1) == 0) ? (k - 20) & 1 : 0)       // x-normal face
-                  : 0;
-}
-// class k's entity of element (x, y, z) is gid = R + size * vid(x + dx,
-// y + dy, z + dz) (periodic wrap): the closed form of entity_base
-// (periodic.cuh) that per-segment code evaluates with a few integer ops
-struct ClassGeom {
-  int R, s, d;  // region base, entity size, dx | dy << 1 | dz << 2
-};
-__device__ __forceinline__ ClassGeom class_geom(int k, int n, int P) {
-  const int N3 = n * n * n, b = P - 1;
-  if (k < 8) return {0, 1, ((k >> 2) & 1) | (((k >> 1) & 1) << 1) | ((k & 1) << 2)};
-  if (k < 20) {
-    const int j = k - 8, dir = j >> 2, s0 = (j >> 1) & 1, s1 = j & 1;
-    // the two shifts go to the axes other than dir, in order
-    const int d = dir == 0 ? (s0 << 1) | (s1 << 2) : (dir == 1 ? s0 | (s1 << 2) : s0 | (s1 << 1));
-    return {N3 + dir * N3 * b, b, d};
-  }
-  if (k < 26) {
-    const int j = k - 20, dir = j >> 1, side = j & 1;
-    return {N3 + 3 * N3 * b + dir * N3 * b * b, b * b, side << dir};
-  }
-  return {N3 * (1 + 3 * b + 3 * b * b), b * b * b, 0};
-}
-__device__ __forceinline__ int class_gid(const ClassGeom& g, int n, int x, int y, int z) {
-  x += g.d & 1;
-  y += (g.d >> 1) & 1;
-  z += (g.d >> 2) & 1;
-  x -= x >= n ? n : 0;
-  y -= y >= n ? n : 0;
-  z -= z >= n ? n : 0;
-  return g.R + g.s * (x + n * (y + n * z));
-}
 // owned classes of an element: vertex 0, edges 8/12/16, faces 20/22/24, interior 26
 __device__ __forceinline__ int owned_class(int c) {
   return c == 0 ? 0 : (c < 4 ? 8 + 4 * (c - 1) : (c < 7 ? 20 + 2 * (c - 4) : 26));
@@ -518,6 +478,181 @@ cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int ac
                                                                  row1 * segs);
     return cudaGetLastError();
   });
+}
+
+// ---------------------------------------------------------------------------
+// Owner-computes sum over the block Z written by the operator's
+// PERIODIC_CLASS mode (pipeline.cuh MODE 5): per tile of NE consecutive
+// elements of an x-row, the classes 0..25 of its elements, class-major
+// (class k at NE * cb[k], element i at + i * size(k)); the interiors, when
+// not written straight into y, follow as an element-major n^3 (P-1)^3 block.
+// Every owned dof of region r (vertices, x/y/z edges, x/y/z faces,
+// interiors: the layout of y itself) is the sum of 8/4/2/1 values at the
+// same offset of the neighbours e - (a, b, c) in classes fixed by r.  One
+// CTA per (ey, ez) row: its neighbour rows are fixed, so each contributor
+// is a stream of NE * size runs; every Z value is read once.  Terms are
+// summed in increasing (a, b, c) order, as owner_periodic_v3 does, so both
+// give bitwise-identical results.
+// ---------------------------------------------------------------------------
+#ifndef CLASS_OWNER_MINB
+#define CLASS_OWNER_MINB 8
+#endif
+namespace {
+
+// offset of class k inside an element's class-major record
+__host__ __device__ constexpr int class_cb(int k, int b) {
+  return k < 8 ? k : (k < 20 ? 8 + (k - 8) * b : (k < 26 ? 8 + 12 * b + (k - 20) * b * b : 8 + 12 * b + 6 * b * b));
+}
+
+// contributor j of region R: neighbour offset (a, b, c) and the class of
+// its entity; j in increasing o8 = a << 2 | b << 1 | c
+template <int R>
+struct Region {
+  static constexpr int NC = R == 0 ? 8 : (R < 4 ? 4 : (R < 7 ? 2 : 1));
+  __host__ __device__ static constexpr int a(int j) {
+    return R == 0 ? j >> 2 : (R == 2 || R == 3) ? j >> 1 : (R == 4 ? j : 0);
+  }
+  __host__ __device__ static constexpr int b(int j) {
+    return R == 0 ? (j >> 1) & 1 : R == 1 ? j >> 1 : R == 3 ? j & 1 : (R == 5 ? j : 0);
+  }
+  __host__ __device__ static constexpr int c(int j) {
+    return R == 0 ? j & 1 : (R == 1 || R == 2) ? j & 1 : (R == 6 ? j : 0);
+  }
+  __host__ __device__ static constexpr int k(int j) {
+    return R == 0 ? j : R == 1 ? 8 + j : R == 2 ? 12 + j : R == 3 ? 16 + j : R == 4 ? 20 + j : R == 5 ? 22 + j
+           : R == 6 ? 24 + j : 26;
+  }
+};
+
+template <int P>
+struct OwnerGeom {
+  static constexpr int b = P - 1;
+  static constexpr int ZS = (P + 1) * (P + 1) * (P + 1) - b * b * b;  // Z doubles per element
+  __host__ __device__ static constexpr int S(int r) { return r == 0 ? 1 : (r < 4 ? b : (r < 7 ? b * b : b * b * b)); }
+  __host__ __device__ static constexpr int start(int r) {  // per-row output offset of region r (units of n)
+    return r == 0 ? 0 : start(r - 1) + S(r - 1);
+  }
+  __host__ __device__ static constexpr int64_t ybase(int r) {  // region base in y (units of n^3)
+    return r == 0 ? 0 : ybase(r - 1) + S(r - 1);
+  }
+};
+
+// output li = ex * S + o of region R in the current row: its NC terms.
+// zr[bc] = Z record of the neighbour row (ey - b, ez - c); within a row the
+// tile t holds elements t * NE .. t * NE + NE - 1, so the output's position
+// u = li % (NE * S) is also the position of the a = 0 terms inside each
+// class run; the a = 1 term is u - S, or the previous tile's last element
+// (x wraps to n - 1 at t = 0) when u < S.
+template <int P, int NE, int R>
+__device__ __forceinline__ double owned_sum(const double* const* zr, const double* const* zi, int T, int li) {
+  using G = OwnerGeom<P>;
+  constexpr int S = G::S(R), NC = Region<R>::NC, RUN = NE * S, REC = NE * G::ZS;
+  const int t = li / RUN, u = li - t * RUN;
+  double v[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const int bc = Region<R>::b(j) * 2 + Region<R>::c(j);
+    if constexpr (R == 7) {
+      v[j] = __ldg(zi[bc] + li);
+    } else {
+      const int cls = NE * class_cb(Region<R>::k(j), G::b);
+      int off = t * REC + cls + u;
+      if (Region<R>::a(j)) off = u >= S ? off - S : (t == 0 ? T - 1 : t - 1) * REC + cls + (NE - 1) * S + u;
+      v[j] = __ldg(zr[bc] + off);
+    }
+  }
+  double acc = v[0];
+#pragma unroll
+  for (int j = 1; j < NC; ++j) acc += v[j];
+  return acc;
+}
+
+// one CTA per (ey, ez) row at a time: all regions' n * (P^3 [- (P-1)^3])
+// owned dofs of the row as one index space (the region of an output is a
+// few compares), so every thread has work at every order
+template <int P, int NE>
+__global__ void __launch_bounds__(256, CLASS_OWNER_MINB) class_owner_sum_kernel(int n, const double* __restrict__ Z,
+                                                              double* __restrict__ y, int accumulate,
+                                                              int nreg, int row0, int row1) {
+  using G = OwnerGeom<P>;
+  const int64_t N3 = (int64_t)n * n * n;
+  const int T = n / NE;  // tiles per row
+  const int per_row = n * (G::start(7) + (nreg > 7 ? G::S(7) : 0));
+  for (int row = row0 + blockIdx.x; row < row1; row += gridDim.x) {
+    const int ez = row / n, ey = row - ez * n;
+    const int ym = ey == 0 ? n - 1 : ey - 1, zm = ez == 0 ? n - 1 : ez - 1;
+    const int nr[4] = {ey + n * ez, ey + n * zm, ym + n * ez, ym + n * zm};  // (b, c) = 00, 01, 10, 11
+    const double* zr[4];
+    const double* zi[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      zr[q] = Z + (int64_t)nr[q] * n * G::ZS;
+      zi[q] = Z + N3 * G::ZS + (int64_t)nr[q] * n * G::S(7);
+    }
+    for (int i = threadIdx.x; i < per_row; i += blockDim.x) {
+      int r = 0;
+#pragma unroll
+      for (int q = 1; q < 8; ++q) r += i >= n * G::start(q) ? 1 : 0;
+      double acc;
+      int64_t g;
+#define REGION(R)                                                \
+  case R: {                                                      \
+    const int li = i - n * G::start(R);                          \
+    acc = owned_sum<P, NE, R>(zr, zi, T, li);                    \
+    g = N3 * G::ybase(R) + (int64_t)row * n * G::S(R) + li;      \
+    break;                                                       \
+  }
+      switch (r) {
+        REGION(0) REGION(1) REGION(2) REGION(3) REGION(4) REGION(5) REGION(6) REGION(7)
+      }
+#undef REGION
+      y[g] = accumulate ? y[g] + acc : acc;
+    }
+  }
+}
+
+}  // namespace
+
+int64_t class_block_doubles(int n, int P) {
+  const int64_t N3 = (int64_t)n * n * n;
+  return N3 * (P + 1) * (P + 1) * (P + 1);
+}
+
+cudaError_t class_owner_sum(int n, int P, int ne, const double* Z, double* y, int accumulate,
+                            int with_interior, cudaStream_t s, int row0, int row1) {
+  if (n < 2 || n % 2 || P < 2 || P > 9 || ne < 1 || (ne & (ne - 1)) || n % ne) return cudaErrorNotSupported;
+  if (row1 < 0) row1 = n * n;
+  if (row1 <= row0) return cudaSuccess;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t blocks = row1 - row0;
+  if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+  auto go = [&](auto pc, auto nc) -> cudaError_t {
+    constexpr int PP = decltype(pc)::value, NE = decltype(nc)::value;
+    class_owner_sum_kernel<PP, NE><<<(unsigned)blocks, 256, 0, s>>>(n, Z, y, accumulate, with_interior ? 8 : 7,
+                                                                    row0, row1);
+    return cudaGetLastError();
+  };
+  auto by_ne = [&](auto pc) -> cudaError_t {
+    switch (ne) {
+      case 2: return go(pc, std::integral_constant<int, 2>());
+      case 4: return go(pc, std::integral_constant<int, 4>());
+      case 8: return go(pc, std::integral_constant<int, 8>());
+    }
+    return cudaErrorNotSupported;
+  };
+  switch (P) {
+    case 2: return by_ne(std::integral_constant<int, 2>());
+    case 3: return by_ne(std::integral_constant<int, 3>());
+    case 4: return by_ne(std::integral_constant<int, 4>());
+    case 5: return by_ne(std::integral_constant<int, 5>());
+    case 6: return by_ne(std::integral_constant<int, 6>());
+    case 7: return by_ne(std::integral_constant<int, 7>());
+    case 8: return by_ne(std::integral_constant<int, 8>());
+    case 9: return by_ne(std::integral_constant<int, 9>());
+  }
+  return cudaErrorNotSupported;
 }
 
 }  // namespace sphp

@@ -26,6 +26,60 @@ namespace sphp {
 
 __host__ __device__ constexpr int even_up(int x) { return (x + 1) & ~1; }
 
+// ===========================================================================
+// Element-block I/O of the fused Helmholtz ops (stages S1 / S9: rows
+// (e, p, q) of M modes).  BlockIO: the packed element-major block
+// (collections.py:316-323).  ClassIO: the tile staged by entity class
+// (pipeline MODE 5, PERIODIC_CLASS): mode (p, q, r) of element e sits at
+// (t & 0xffff) + e * (t >> 16) with t = tab[(p * M + q) * M + r]; along r
+// the modes r >= 2 of a row are consecutive offsets of one entity, so a row
+// costs three table loads.
+// ===========================================================================
+struct BlockIO {
+  static constexpr bool DENSE = true;
+};
+// hook the ops call right after S1's barrier (the element block is dead)
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+template <bool PRE>
+struct ClassIO {
+  static constexpr bool DENSE = false;
+  const int* tab;
+  // PRE: every thread owns at most one (e, p, q) row of S1 / S9, the same
+  // for every tile: its three positions are resolved once per kernel
+  int p0 = 0, p1 = 0, p2 = 0;
+  __device__ __forceinline__ static int at(int t, int e) { return (t & 0xffff) + e * (t >> 16); }
+  template <int M>
+  __device__ __forceinline__ void resolve(int e, int pq, int& a0, int& a1, int& a2) const {
+    if constexpr (PRE) {
+      a0 = p0, a1 = p1, a2 = p2;
+    } else {
+      const int* tr = tab + pq * M;
+      a0 = at(tr[0], e), a1 = at(tr[1], e), a2 = at(tr[2], e);
+    }
+  }
+  template <int M>
+  __device__ __forceinline__ void load_row(const double* __restrict__ base, int e, int pq, double* x) const {
+    static_assert(M > 2, "class staging needs bubbles (P >= 2)");
+    int a0, a1, a2;
+    resolve<M>(e, pq, a0, a1, a2);
+    x[0] = base[a0];
+    x[1] = base[a1];
+#pragma unroll
+    for (int r = 2; r < M; ++r) x[r] = base[a2 + r - 2];
+  }
+  template <int M>
+  __device__ __forceinline__ void store_row(double* __restrict__ base, int e, int pq, const double* c) const {
+    int a0, a1, a2;
+    resolve<M>(e, pq, a0, a1, a2);
+    base[a0] = c[0];
+    base[a1] = c[1];
+#pragma unroll
+    for (int r = 2; r < M; ++r) base[a2 + r - 2] = c[r];
+  }
+};
+
 // device view of the launch arguments (plain POD, passed by value)
 struct DevArgs {
   int64_t E;
@@ -46,6 +100,10 @@ struct DevArgs {
   int n;
   int colour;
   int reverse;  // MODE 0: walk the tiles last to first (L2 reuse, see launch)
+  // MODE 5
+  int64_t e0;        // absolute index of element 0 of this launch
+  double* zbuf;      // class-major output block
+  int direct_interior;
 };
 
 
@@ -59,6 +117,11 @@ struct DevArgs {
 // MODE 2: explicit map, colour class: gather in, scatter-add out.
 // MODE 3: periodic hex, all elements in order: gather in, local block out.
 // MODE 4: explicit map, all elements in order: gather in, local block out.
+// MODE 5: periodic hex, all elements in order, by entity class: the tile's
+//         27 class ranges of x arrive by TMA bulk copies into a class-
+//         staged input, results leave by 27 bulk stores into the class-major
+//         block Z (interiors optionally straight into y).  Needs even NE,
+//         n % NE == 0 and even n (then every copy's 16-byte parity is static).
 // Gathering modes need IN == OUT == nmodes.
 template <int MODE>
 struct ModeTraits {
@@ -67,6 +130,7 @@ struct ModeTraits {
   static constexpr bool EXPLICIT = MODE == 2 || MODE == 4;
   static constexpr bool SCATTER = MODE == 1 || MODE == 2;
   static constexpr bool CONTIG = MODE == 0 || MODE >= 3;
+  static constexpr bool CLASS = MODE == 5;
 };
 // ---------------------------------------------------------------------------
 // preferred number of input stages: Op::NSTP when the Op declares it, else 1
@@ -96,7 +160,10 @@ constexpr int out_off_impl(...) { return -1; }
 template <class Op, int MODE>
 struct Scaffold {
   static constexpr int NE = Op::NE, NT = Op::NT;
-  static constexpr int IN_T = even_up(NE * Op::IN + 2);
+  static constexpr bool CLS = ModeTraits<MODE>::CLASS;
+  // MODE 5 stages each of the 27 classes in its own slot of NE * size + 2
+  // doubles (room for the 16-byte widening of its copy window)
+  static constexpr int IN_T = CLS ? even_up(NE * Op::IN + 2 * 27) : even_up(NE * Op::IN + 2);
   static constexpr int GEO_S = geo_s_impl<Op>(0);  // even, >= GEO
   static constexpr int GEO_T = NE * GEO_S;
   static constexpr int STAGE = IN_T + GEO_T;
@@ -115,8 +182,12 @@ struct Scaffold {
   // assembled-mode integer tables (in doubles): per stage ids + entities,
   // current-tile copies, and the per-mode code table
   static constexpr int ENT = ModeTraits<MODE>::PERIODIC ? 27 : 0;
-  static constexpr int ITAB = (MODE == 0) ? 0 : even_up(NE * (2 + ENT)) / 2 + 1;
-  static constexpr int MTAB = ModeTraits<MODE>::PERIODIC ? even_up(Op::IN) / 2 + 1 : 0;
+  static constexpr int ITAB = (MODE == 0 || CLS) ? 0 : even_up(NE * (2 + ENT)) / 2 + 1;
+  // MODE 5 int tables: per-mode input / output positions (2 * IN), per
+  // class slot base, Z offset, geometry and first 16-byte chunk (5 * 27 + 1)
+  static constexpr int MTAB = ModeTraits<MODE>::PERIODIC ? even_up(Op::IN) / 2 + 1
+                              : CLS                      ? (2 * Op::IN + 5 * 27 + 1) / 2 + 1
+                                                         : 0;
   static constexpr size_t fixed_bytes(int nst) {
     return sizeof(double) * (nst * (STAGE + ITAB) + OUT_T + WORK_T + ITAB + MTAB) + 2 * sizeof(uint64_t);
   }
@@ -124,13 +195,17 @@ struct Scaffold {
   // then overlaps only the part of the compute after the release point)
   static constexpr int NST = (nst_pref<Op>() == 2 && fixed_bytes(2) <= 227 * 1024) ? 2 : 1;
   static constexpr size_t SMEM_BYTES = fixed_bytes(NST);
-  static_assert(SMEM_BYTES <= 227 * 1024, "one pipeline stage does not fit in shared memory");
+  // CTAs per SM that shared memory allows (228 KB per SM, 1 KB reserved per
+  // CTA)
+  static constexpr int SMEM_CTAS = (int)(233472 / (SMEM_BYTES + 1024)) < 1 ? 1 : (int)(233472 / (SMEM_BYTES + 1024));
+  static constexpr int MIN_CTAS = CLS ? (SMEM_CTAS * NT <= 1024 ? SMEM_CTAS : 1024 / NT) : 1;
 };
 
 template <class Op, int MODE>
 __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
   using S = Scaffold<Op, MODE>;
   using MT = ModeTraits<MODE>;
+  static_assert(S::SMEM_BYTES <= 227 * 1024, "one pipeline stage does not fit in shared memory");
   constexpr int NE = Op::NE, NT = Op::NT, IN = Op::IN, OUT = Op::OUT, GEO = Op::GEO;
   constexpr int GEO_S = S::GEO_S;
   constexpr int NST = S::NST, ENT = S::ENT;
@@ -155,6 +230,59 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
   }
   if (MT::PERIODIC)
     for (int i = tid; i < IN; i += NT) mtab[i] = mode_code(Op::M, i);
+  // MODE 5 tables: csb[k] = slot of class k in the input stage, ccb[k] =
+  // offset of class k in an element's class-major record (sum of sizes),
+  // cR / csd[k] = class geometry (region base; size | d << 16 | parity << 20),
+  // cpre[k] = first 16-byte input chunk of class k (cpre[27] = count)
+  int* ptab = mtab;          // IN: input position word per mode
+  int* qtab = mtab + IN;     // IN: output position word per mode
+  int* csb = mtab + 2 * IN;  // 27
+  int* ccb = csb + 27;       // 27
+  int* cR = ccb + 27;        // 27
+  int* csd = cR + 27;        // 27
+  int* cpre = csd + 27;      // 28
+  if constexpr (MT::CLASS) {
+    const int b = Op::M - 2;
+    if (tid == 0) {
+      int sb = 0, cb = 0, nc = 0;
+      for (int k = 0; k < 27; ++k) {
+        const ClassGeom cg = class_geom(k, a.n, Op::M - 1);
+        const int sz = class_size(k, b), par = (sz & 1) & class_dx(k);
+        csb[k] = sb;
+        ccb[k] = cb;
+        cR[k] = cg.R;
+        csd[k] = sz | (cg.d << 16) | (par << 20);
+        cpre[k] = nc;
+        nc += (par + NE * sz + 1) / 2;
+        sb += NE * sz + 2;
+        cb += sz;
+      }
+      cpre[27] = nc;
+    }
+    __syncthreads();
+    for (int i = tid; i < IN; i += NT) {
+      const int c = mode_code(Op::M, i), k = c & 31, off = c >> 5, sz = class_size(k, b);
+      // 16-byte parity of the class's first value: static for even n, even
+      // NE (x-shifted classes of odd size start odd)
+      const int par = (sz & 1) & class_dx(k);
+      ptab[i] = (csb[k] + par + off) | (sz << 16);
+      qtab[i] = (NE * ccb[k] + off) | (sz << 16);
+    }
+  }
+  constexpr bool PRE = NE * Op::M * Op::M <= NT;
+  ClassIO<PRE> cin_io{ptab}, cout_io{qtab};
+  if constexpr (MT::CLASS && PRE) {
+    __syncthreads();
+    if (tid < NE * Op::M * Op::M) {
+      const int e = tid / (Op::M * Op::M), pq = tid - e * (Op::M * Op::M);
+      cin_io.p0 = ClassIO<PRE>::at(ptab[pq * Op::M], e);
+      cin_io.p1 = ClassIO<PRE>::at(ptab[pq * Op::M + 1], e);
+      cin_io.p2 = ClassIO<PRE>::at(ptab[pq * Op::M + 2], e);
+      cout_io.p0 = ClassIO<PRE>::at(qtab[pq * Op::M], e);
+      cout_io.p1 = ClassIO<PRE>::at(qtab[pq * Op::M + 1], e);
+      cout_io.p2 = ClassIO<PRE>::at(qtab[pq * Op::M + 2], e);
+    }
+  }
   __syncthreads();
 
   // ---- local mode: byte window of tile t's input block, widened to 16-byte
@@ -301,8 +429,58 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     cp_async_commit();
   };
 
+  // MODE 5 input, all threads: the tile's 27 class ranges of x as 16-byte
+  // cp.async chunks into the class slots (every chunk's source and slot share
+  // their static 16-byte parity).  At the row end the x-shifted classes wrap:
+  // the last element's entity comes from x = 0 of the row, and since its
+  // slot offset is even no chunk straddles the two pieces.  One cp.async
+  // group per call.
+  auto issue_x = [&](int ts) {
+    if (ts < ntiles) {
+      double* in_s = stage_base;
+      const int w0 = (int)a.e0 + ts * NE;  // 32-bit: n^3 < 2^31
+      const int n = a.n, rowi = w0 / n, ex0 = w0 - rowi * n;
+      const int ez = rowi / n, ey = rowi - ez * n;
+      const bool wrap = ex0 + NE == n;
+      const int nchunk = cpre[27];
+      for (int c = tid; c < nchunk; c += NT) {
+        int k = 0;  // class of chunk c: cpre[k] <= c < cpre[k + 1]
+#pragma unroll
+        for (int h = 16; h > 0; h >>= 1)
+          if (k + h < 27 && cpre[k + h] <= c) k += h;
+        const int d = 2 * (c - cpre[k]);
+        const int sd = csd[k], sz = sd & 0xffff, dx = (sd >> 16) & 1, par = sd >> 20;
+        int y = ey + ((sd >> 17) & 1), z = ez + ((sd >> 18) & 1);
+        y -= y >= n ? n : 0;
+        z -= z >= n ? n : 0;
+        const int rb = cR[k] + sz * n * (y + n * z);  // class region, this row
+        const int plast = par + (NE - 1) * sz;        // slot offset of the last element
+        const int src = (wrap && dx && d >= plast) ? rb + (d - plast) : rb + sz * (ex0 + dx) + d - par;
+        cp_async16(in_s + csb[k] + d, a.xg + src);
+      }
+    }
+    cp_async_commit();
+  };
+  // MODE 5 geometry, thread 0: one TMA bulk copy per tile
+  auto issue_geo = [&](int ts, int s) {
+    if (ts >= ntiles || GEO == 0) return;
+    double* geo_s = stage_base + s * S::STAGE + S::IN_T;
+    const int64_t w0 = a.e0 + (int64_t)ts * NE;
+    mbar_expect_tx(&bar[s], (uint32_t)(sizeof(double) * NE * GEO));
+    if (a.gstride == GEO && a.goff == 0 && GEO_S == GEO) {
+      bulk_g2s(geo_s, a.geom + w0 * a.gstride, (uint32_t)(sizeof(double) * NE * GEO), &bar[s]);
+    } else {
+      for (int e = 0; e < NE; ++e)
+        bulk_g2s(geo_s + e * GEO_S, a.geom + (w0 + e) * a.gstride + a.goff, (uint32_t)(sizeof(double) * GEO),
+                 &bar[s]);
+    }
+  };
+
   uint32_t phase = 0;  // bit s = parity to wait for on stage s
-  if (MODE == 0) {
+  if (MT::CLASS) {
+    issue_x(blockIdx.x);
+    if (tid == 0) issue_geo(blockIdx.x, 0);
+  } else if (MODE == 0) {
     if (tid == 0) {
       issue_local(blockIdx.x, 0);
       if (NST == 2) issue_local(blockIdx.x + G, 1);
@@ -323,7 +501,13 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
 
     // ---- obtain the tile's inputs -------------------------------------
     const double* in_p = in_s;
-    if (MODE == 0) {
+    if constexpr (MT::CLASS) {
+      cp_async_wait<0>();
+      mbar_wait(&bar[s], (phase >> s) & 1);
+      phase ^= (1u << s);
+      // the previous tile's bulk stores must have read the output buffer
+      if (tid == 0) bulk_wait_read0();
+    } else if (MODE == 0) {
       int64_t a0, a1;
       int off;
       if (in_window(t, a0, a1, off)) {
@@ -369,7 +553,12 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     auto release = [&]() {
       // all threads call this right after a __syncthreads that follows the
       // last read of the stage: hand the stage to the copy engines
-      if (MODE == 0) {
+      if (MT::CLASS) {
+        if (tid == 0) {
+          fence_proxy_async();
+          issue_geo(ts + NST * G, s);
+        }
+      } else if (MODE == 0) {
         if (tid == 0) {
           fence_proxy_async();
           issue_local(ts + NST * G, s);
@@ -385,12 +574,35 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
     const int head = bulk_out ? (int)((w0 * OUT) & 1) : 0;
     const int sh = bulk_out ? (head + (S::OUT_OFF > 0 ? S::OUT_OFF : 0)) & 1 : 0;
     double* out_t = out_s + sh;
-    Op::compute(in_p, geo_s, work, out_t, a.lam, release, pre_out, c_tab);
-    if (bulk_out) fence_proxy_async();  // this thread's buffer writes -> async proxy
+    if constexpr (MT::CLASS) {
+      // the class slots are free once S1 has read them: the next tile's x
+      // chunks are issued right after S1 (all of S2..S9 to land)
+      auto after_in = [&]() { issue_x(ts + G); };
+      Op::compute(in_p, geo_s, work, out_s, a.lam, release, pre_out, c_tab, cin_io, cout_io, after_in);
+      fence_proxy_async();
+    } else {
+      Op::compute(in_p, geo_s, work, out_t, a.lam, release, pre_out, c_tab);
+      if (bulk_out) fence_proxy_async();  // this thread's buffer writes -> async proxy
+    }
     __syncthreads();
 
     // ---- write back ------------------------------------------------------
-    if (bulk_out) {
+    if constexpr (MT::CLASS) {
+      // lane k: class k's NE * size results -> Z (class region k, element
+      // w0..w0+NE-1: one contiguous, 16-byte aligned range), interiors
+      // straight into y when the caller does not accumulate
+      // the tile's results leave in two bulk stores: classes 0..25
+      // (class-major within the tile) to its record of the tile-major block
+      // Z, the interiors straight into y (or after Z when accumulating)
+      if (tid == 0) {
+        constexpr int b = Op::M - 2, ZS = IN - b * b * b;
+        const int64_t wa = a.e0 + w0, N3 = (int64_t)a.n * a.n * a.n;
+        bulk_s2g(a.zbuf + wa * ZS, out_s, (uint32_t)(sizeof(double) * NE * ZS));
+        double* yint = a.direct_interior ? a.yg + N3 * (1 + 3 * b + 3 * b * b) : a.zbuf + N3 * ZS;
+        bulk_s2g(yint + wa * (b * b * b), out_s + NE * ZS, (uint32_t)(sizeof(double) * NE * b * b * b));
+        bulk_commit();
+      }
+    } else if (bulk_out) {
       const int n = r * OUT, body = (n - head) & ~1;
       double* dst = a.out + w0 * OUT;
       if (tid == 0) {
@@ -445,6 +657,7 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
   }
   if (MODE != 0) cp_async_wait<0>();
   if (S::BULK_OUT && tid == 0) bulk_wait0();
+  if (MT::CLASS && tid == 0) bulk_wait0();
 }
 
 }  // namespace sphp

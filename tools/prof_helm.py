@@ -15,6 +15,7 @@ ap.add_argument("--P", type=int, default=4)
 ap.add_argument("--n", type=int, default=64)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--mode", default="both", choices=["local", "assembled", "both"])
+ap.add_argument("--alg", default=None)
 a = ap.parse_args()
 exp = sp.make_hex(a.P, a.P + 2)
 batch = sp.ElementBatch.structured(exp, a.n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE, amp=0.03)
@@ -27,6 +28,8 @@ if a.mode in ("local", "both"):
         coll.apply(c, y)
 if a.mode in ("assembled", "both"):
     amap = sp.AssemblyMap.hex_periodic(a.n, a.P)
+    if a.alg:
+        amap.set_algorithm(a.alg)
     op = sp.GlobalHelmholtz([(coll, amap)], amap.num_global)
     x = torch.as_tensor(np.random.default_rng(1).uniform(-1, 1, amap.num_global), device="cuda")
     yg = torch.empty_like(x)
