@@ -4,11 +4,12 @@
 One step = one assembled matrix-free Helmholtz apply y = A^T H A x on the
 64^3 periodic deformed hex mesh (x' = x + 0.03 sin 2πy sin 2πz), P=4, Q=6
 GLL, lambda = 1, per-point geometric factors stored (6 metric terms + |J|):
-the map's default (split) algorithm — class-range scatter kernel, fused
-BwdTrans -> PhysDeriv -> metric -> IProductWRTDerivBase + lambda
-IProductWRTBase on the local block, then the deterministic owner-computes C0
-sum.  `value` is local DoF/s (E (P+1)^3 / step time,
-SURVEY §8(d)); global DoF/s is reported too.
+the map's default (class-range) algorithm — one fused launch gathers x by
+entity-class ranges, runs BwdTrans -> PhysDeriv -> metric ->
+IProductWRTDerivBase + lambda IProductWRTBase and writes the tile-major class
+block (interiors straight into y), then the deterministic streaming
+owner-computes C0 sum.  `value` is local DoF/s (E (P+1)^3 /
+step time); global DoF/s is reported too.
 
 Arms:
   default            the CUDA path (libspechp_b200.so) through the public API
@@ -83,16 +84,28 @@ def helm_flops(P, E):
     return 2 * E * (2 * staged + 6 * Q ** 4 + 11 * Q ** 3)
 
 
+TRAFFIC_FILE = ROOT / "profiles" / "r02_ncu_traffic.json"
+FP64_PEAK_TFS = 34.2   # DFMA microbenchmark on this pool (tools/fp64_peak.cu, profiles/r02_fp64_peak.log)
+NOMINAL_HBM_GBS = 8000.0
+
+
 def ncu_traffic(kernel, P, n):
-    """DRAM bytes per launch of `kernel` at (P, n) from the committed ncu
-    capture (profiles/r01_ncu_traffic.json), or None."""
-    p = ROOT / "profiles" / "r01_ncu_traffic.json"
-    if not p.exists():
-        return None
-    d = json.loads(p.read_text()).get(kernel)
+    """(DRAM bytes per launch, kernel name) of `kernel` at (P, n) from the
+    committed ncu capture (profiles/r02_ncu_traffic.json), or (None, None)."""
+    if not TRAFFIC_FILE.exists():
+        return None, None
+    d = json.loads(TRAFFIC_FILE.read_text()).get(kernel)
     if d and d.get("P") == P and d.get("n") == n:
-        return d["bytes_per_launch"]
-    return None
+        return d["bytes_per_launch"], d.get("kernel")
+    return None, None
+
+
+def class_op_bytes(P, n):
+    """Algorithmic bytes of the class-range operator launch: geometry
+    (7 Q^3 per element) + x read once + every local result written once
+    (tile-major class block + interiors into y)."""
+    E, Q, m = n ** 3, P + 2, P + 1
+    return 8 * (7 * Q ** 3 * E + (n * P) ** 3 + E * m ** 3)
 
 
 def measured_peaks():
@@ -345,14 +358,26 @@ def run_ours(args, rank, world, local_rank):
     e2e_ms = timed(e2e_step, max(3, args.steps // 2), 2)
     e2e_value = world * E * m ** 3 / (e2e_ms * 1e-3)
 
-    # ---- dominant kernel: the fused local Helmholtz, timed alone -----------
+    # ---- dominant kernel of the step: its launches timed by CUDA events on
+    # the launch stream (sphp_helmholtz_assembled_phases), averaged over
+    # `steps` applies; the fused local Helmholtz (block in/out) timed alone
+    phase_runs = [op.apply_phases(x, y, stream) for _ in range(args.steps)]
+    nph = len(phase_runs[0])
+    phase_ms = [statistics.mean(r[i] for r in phase_runs) for i in range(nph)]
     c = torch.as_tensor(np.random.default_rng(SEED).uniform(-1, 1, (E, m ** 3)), device=dev)
     yl = torch.empty_like(c)
     k_ms = timed(lambda: coll.apply(c, yl), args.steps, args.warmup)
     peak, peak_kind = measured_peaks()
-    traffic = ncu_traffic("helmholtz_local", P, n)
     kb = local_bytes(P, E)
-    achieved = kb / (k_ms * 1e-3) / 1e9
+    if amap.algorithm == "class" and nph == 2:
+        dom_ms, dom_bytes = phase_ms[0], class_op_bytes(P, n)
+        dom_name = "pipe_kernel<HexHelm, MODE 5> (class-range fused Helmholtz, launch 1 of 2)"
+        traffic, traffic_kernel = ncu_traffic("helmholtz_class", P, n)
+    else:
+        dom_ms, dom_bytes = k_ms, kb
+        dom_name = "pipe_kernel<HexHelm, MODE 0> (fused local Helmholtz)"
+        traffic, traffic_kernel = ncu_traffic("helmholtz_local", P, n)
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     # assembled apply as a whole against the same roofline
     ab = workload_bytes(P, n)
     a_achieved = ab / (ms * 1e-3) / 1e9
@@ -424,16 +449,23 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": 8 * ng, "ms_per_step": e2e_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, same kernel/config)"
-                     if traffic else None,
-                     "kernel": "pipe_kernel<HexHelm> (fused local Helmholtz, one launch)",
-                     "bytes_per_launch": kb, "launch_ms": k_ms,
-                     "fp64_tflops": helm_flops(P, E) / (k_ms * 1e-3) / 1e12,
+                     "traffic_source": (f"{TRAFFIC_FILE.relative_to(ROOT)} (ncu dram__bytes_read+write, "
+                                        f"{traffic_kernel})") if traffic else None,
+                     "kernel": dom_name, "bytes_per_launch": dom_bytes, "launch_ms": dom_ms,
+                     "share_of_step": dom_ms / ms, "phase_ms": phase_ms,
+                     "frac_nominal_8tbs": achieved / NOMINAL_HBM_GBS,
+                     "fp64_tflops": helm_flops(P, E) / (dom_ms * 1e-3) / 1e12,
+                     "fp64_frac": helm_flops(P, E) / (dom_ms * 1e-3) / 1e12 / FP64_PEAK_TFS,
+                     "local": {"kernel": "pipe_kernel<HexHelm, MODE 0> (block in/out, timed alone)",
+                               "launch_ms": k_ms, "bytes_per_launch": kb,
+                               "achieved": kb / (k_ms * 1e-3) / 1e9,
+                               "frac": kb / (k_ms * 1e-3) / 1e9 / peak},
                      "assembled_achieved": a_achieved, "assembled_frac": a_achieved / peak,
                      "assembled_bytes_per_step": ab},
         "cpu_baseline": cpu,
         "clocks": clk,
-        # split: scatter, fused local Helmholtz, owner sum; owner: gather-fused + owner sum
+        # class: class-range operator + owner sum; split: scatter, operator,
+        # owner sum; owner: gather-fused operator + owner sum
         "gpu_launches": args.steps * (3 if amap.algorithm == "split" else 2),
         "replicas_identical": replicas_identical,
         "parity": parity,

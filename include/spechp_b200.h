@@ -184,7 +184,7 @@ int sphp_amap_destroy(sphp_amap* a);
 #define SPHP_ASSEMBLY_OWNER 0
 #define SPHP_ASSEMBLY_COLOUR 1
 #define SPHP_ASSEMBLY_SPLIT 2
-#define SPHP_ASSEMBLY_CLASS 3
+#define SPHP_ASSEMBLY_CLASS 3  /* periodic maps: class-range gather in the operator + class owner sum */
 int sphp_amap_set_algorithm(sphp_amap* a, int alg);
 int sphp_amap_algorithm(const sphp_amap* a, int* alg);
 int sphp_amap_info(const sphp_amap* a, int64_t* num_elements, int* nmodes,
@@ -209,6 +209,14 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x,
 int sphp_helmholtz_assembled_host(sphp_coll* c, const sphp_amap* a,
                                   const double* x, double* y,
                                   sphp_stream stream);
+/* measurement: one apply (accumulate = 0) with a CUDA event after each of
+ * its launches on `stream`; synchronises and writes the launches'
+ * durations (ms) to ms[0 .. *nphases)  (class: operator, owner sum;
+ * split: scatter, operator, owner sum)                                      */
+int sphp_helmholtz_assembled_phases(sphp_coll* c, const sphp_amap* a,
+                                    const double* x, double* y,
+                                    sphp_stream stream, int max_phases,
+                                    float* ms, int* nphases);
 
 /* GlobalSystem over several per-order Helmholtz batches on explicit maps
  * sharing one numbering (assembly.py:185-215 with per-order element groups,

@@ -92,6 +92,7 @@ _SIGS = {
     "sphp_assemble": (_i, [_p, _p, _p, _p]),
     "sphp_helmholtz_assembled": (_i, [_p, _p, _p, _p, _i, _p]),
     "sphp_helmholtz_assembled_host": (_i, [_p, _p, _p, _p, _p]),
+    "sphp_helmholtz_assembled_phases": (_i, [_p, _p, _p, _p, _p, _i, _p, _p]),
     "sphp_gsys_create": (_i, [_pp, _pp, _i, _i64, _pp]),
     "sphp_gsys_apply": (_i, [_p, _p, _p, _p]),
     "sphp_gsys_destroy": (_i, [_p]),

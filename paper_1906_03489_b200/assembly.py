@@ -16,8 +16,13 @@ assembly algorithms (`AssemblyMap.set_algorithm`):
   "owner"  (default on explicit maps) one kernel gathers x, applies the
            fused elemental operator and writes the local block; a second
            sums every global dof from its contributions in a fixed order;
-  "split"  (default on periodic hex maps) scatter kernel -> fused operator
-           on the local block -> owner-computes sum;
+  "class"  (default on periodic hex maps, but P = 7) the fused operator
+           gathers x by entity-class ranges (16-byte cp.async chunks) and
+           writes a tile-major class block (interiors straight into y); one
+           streaming owner-computes sum reduces it — two launches, no local
+           block; falls back to split where its tiles do not fit;
+  "split"  (default at P = 7) scatter kernel -> fused operator on the local
+           block -> owner-computes sum;
   "colour" one fused gather -> operator -> scatter-add kernel per colour
            class, colours in a fixed order.
 Several per-order batches on explicit "owner" maps (the variable-order
@@ -72,8 +77,8 @@ class AssemblyMap:
 
     @property
     def algorithm(self):
-        """'owner', 'colour' or 'split' (the library default: split for
-        periodic maps the class-range kernels support, owner otherwise)."""
+        """'owner', 'colour', 'split' or 'class' (the library default: class
+        on periodic maps, split there at P = 7, owner on explicit maps)."""
         a = C.c_int()
         _lib.check(_lib.lib.sphp_amap_algorithm(self._h, C.byref(a)), AssemblyError)
         return {_lib.ASSEMBLY_OWNER: "owner", _lib.ASSEMBLY_COLOUR: "colour",
@@ -110,8 +115,9 @@ class AssemblyMap:
 
     def set_algorithm(self, alg):
         """'owner' (gather -> local -> owner-computes sum), 'split' (scatter
-        kernel -> local operator -> owner sum) or 'colour' (fused
-        colour-ordered scatter-add)."""
+        kernel -> local operator -> owner sum), 'colour' (fused
+        colour-ordered scatter-add) or, periodic maps only, 'class'
+        (class-range gather in the operator -> class block -> owner sum)."""
         code = {"owner": _lib.ASSEMBLY_OWNER, "colour": _lib.ASSEMBLY_COLOUR,
                 "split": _lib.ASSEMBLY_SPLIT, "class": _lib.ASSEMBLY_CLASS}[alg]
         _lib.check(_lib.lib.sphp_amap_set_algorithm(self._h, code), AssemblyError)
@@ -219,6 +225,20 @@ class GlobalHelmholtz:
                                                    1 if k else 0, _lib.stream_ptr(stream))
             _lib.check(rc, AssemblyError)
         return out
+
+    def apply_phases(self, x, out, stream=None):
+        """One apply (single batch) with CUDA events between its launches on
+        `stream`: returns the launches' durations in ms (class: operator,
+        owner sum; split: scatter, operator, owner sum).  Synchronises."""
+        if len(self.batches) != 1:
+            raise AssemblyError("apply_phases takes one (collection, map) batch")
+        coll, amap = self.batches[0]
+        ms = (C.c_float * 8)()
+        nph = C.c_int()
+        _lib.check(_lib.lib.sphp_helmholtz_assembled_phases(coll._handle, amap._h, _lib.ptr(x), _lib.ptr(out),
+                                                            _lib.stream_ptr(stream), 8, ms, C.byref(nph)),
+                   AssemblyError)
+        return [float(ms[i]) for i in range(nph.value)]
 
     def apply_host(self, x, out=None, stream=None):
         """y = A^T H A x with HOST vectors (numpy or CPU tensor; pinned for

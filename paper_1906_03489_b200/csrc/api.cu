@@ -1122,8 +1122,12 @@ int sphp_amap_create_hex_periodic(int n, int P, sphp_amap** out) {
   a->E = (int64_t)n * n * n;
   a->num_global = ipow((int64_t)n * P, 3);
   a->ncolours = 8;
-  // the class-range scatter / owner kernels (periodic_ops.cu) need n % 4 == 0
-  a->alg = (P >= 2 && n % 4 == 0) ? SPHP_ASSEMBLY_SPLIT : SPHP_ASSEMBLY_OWNER;
+  // default: class-range assembly (the operator gathers x by entity class,
+  // one streaming owner sum; falls back to split when the mesh does not
+  // divide into its tiles), except at P = 7 where its two-element tile
+  // leaves one CTA per SM and split measures faster (tools/time_class.py:
+  // 3.22 vs 3.54 ms at n = 64; every other order 4-16 % faster)
+  a->alg = P < 2 ? SPHP_ASSEMBLY_OWNER : (P == 7 ? SPHP_ASSEMBLY_SPLIT : SPHP_ASSEMBLY_CLASS);
   if (a->num_global > 2147483645LL) {
     delete a;
     return fail(SPHP_ERR_UNSUPPORTED, "periodic map with more than 2^31-3 global dofs");
@@ -1272,6 +1276,15 @@ int sphp_assemble(const sphp_amap* a, const double* loc, double* g, sphp_stream 
   return amap_assemble_any(a, loc, g, 0, (cudaStream_t)stream);
 }
 
+// phase markers of sphp_helmholtz_assembled_phases: when set (this thread
+// only), the assembled apply records one event on its stream after each of
+// its launches
+thread_local std::vector<cudaEvent_t>* g_phase_marks = nullptr;
+thread_local size_t g_phase_next = 0;
+static void phase_mark(cudaStream_t s) {
+  if (g_phase_marks && g_phase_next < g_phase_marks->size()) cudaEventRecord((*g_phase_marks)[g_phase_next++], s);
+}
+
 static int split_reverse() {
   static const int v = [] {
     const char* e = getenv("SPHP_SPLIT_REVERSE");  // tuning override
@@ -1303,7 +1316,7 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
   OpArgs o = base_args(c);
   o.xg = x;
   o.yg = y;
-  if (a->alg == SPHP_ASSEMBLY_CLASS) {
+  if (a->alg == SPHP_ASSEMBLY_CLASS && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
     // the operator gathers x by entity-class ranges and writes a class-major
     // block (interiors straight into y), then one owner-computes sum over it
     // (two launches, the local block never exists)
@@ -1316,18 +1329,22 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
     o.ne_out = &ne;
     cudaError_t e = sumfac_launch(c, o, s);
     if (e == cudaSuccess) {
+      phase_mark(s);
       CK(class_owner_sum(a->n, a->P, ne, o.zbuf, y, accumulate, !o.direct_interior, s));
+      phase_mark(s);
       return SPHP_OK;
     }
     if (e != cudaErrorNotSupported) return cuda_fail(e, "sphp_helmholtz_assembled");
     // no class-mode tile for this key / mesh: the split algorithm below
   }
+  // (x not 16-byte aligned: the class gather moves 16-byte chunks; split)
   if (a->alg == SPHP_ASSEMBLY_SPLIT || a->alg == SPHP_ASSEMBLY_CLASS) {
     // scatter -> fused local operator -> owner-computes sum (three launches;
     // the fused kernel then runs in its block-input form)
     CK(c->loc_x.ensure(sizeof(double) * c->E * c->t->nm));
     CK(c->loc_y.ensure(sizeof(double) * c->E * c->t->nm));
     CK(amap_scatter(a->dev(), x, c->loc_x.as<double>(), s));
+    phase_mark(s);
     o.in = c->loc_x.as<double>();
     o.out = c->loc_y.as<double>();
     o.mode = AsmMode::LOCAL;
@@ -1338,7 +1355,10 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
     cudaError_t e = sumfac_launch(c, o, s);
     if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no kernel for this key");
     if (e != cudaSuccess) return cuda_fail(e, "sphp_helmholtz_assembled");
-    return amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s, 0);
+    phase_mark(s);
+    const int rc = amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s, 0);
+    phase_mark(s);
+    return rc;
   }
   if (a->alg == SPHP_ASSEMBLY_OWNER) {
     // gather -> fused elemental operator -> local block, then the
@@ -1378,6 +1398,34 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
   return SPHP_OK;
 }
 
+// One assembled apply (accumulate = 0) with an event after each of its
+// launches; waits for it and returns the launches' durations in ms (split:
+// scatter, operator, owner sum; class: operator, owner sum).  Measurement
+// entry for bench.py: the dominant kernel's time on its own stream.
+int sphp_helmholtz_assembled_phases(sphp_coll* c, const sphp_amap* a, const double* x, double* y,
+                                    sphp_stream stream, int max_phases, float* ms, int* nphases) {
+  if (!ms || !nphases || max_phases < 1) return fail(SPHP_ERR_BAD_ARG, "null output");
+  static thread_local std::vector<cudaEvent_t> ev;
+  while ((int)ev.size() < max_phases + 1) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ev.push_back(e);
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<cudaEvent_t> marks(ev.begin() + 1, ev.begin() + 1 + max_phases);
+  CK(cudaEventRecord(ev[0], s));
+  g_phase_marks = &marks;
+  g_phase_next = 0;
+  const int rc = sphp_helmholtz_assembled(c, a, x, y, 0, stream);
+  const size_t np = g_phase_next;
+  g_phase_marks = nullptr;
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < np; ++i) CK(cudaEventElapsedTime(&ms[i], i ? marks[i - 1] : ev[0], marks[i]));
+  *nphases = (int)np;
+  return SPHP_OK;
+}
+
 // Host-buffer apply on a periodic split map, pipelined over K z-slabs: the
 // host->device copy of slab k+1 overlaps the scatter / fused operator /
 // owner sum of slab k, and the device->host copy of finished slabs runs in
@@ -1388,7 +1436,7 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
 // plane, cyclically); owner(k) reads the local block of planes z0-1 .. z1-1,
 // so owner(0) runs after the last slab's operator.
 int assembled_host_pipelined(sphp_coll* c, const sphp_amap* a, const double* x, double* y,
-                             cudaStream_t s, const std::vector<int>& zb) {
+                             cudaStream_t s, const std::vector<int>& zb, bool use_class) {
   const int n = a->n, P = a->P, b = P - 1, K = (int)zb.size() - 1;
   const int64_t N3 = (int64_t)n * n * n, n2 = (int64_t)n * n, nm = c->t->nm;
   // region r: base and dofs per z-plane; regions 1-3 (edges) and 4-6
@@ -1451,23 +1499,43 @@ int assembled_host_pipelined(sphp_coll* c, const sphp_amap* a, const double* x, 
   }
   OpArgs o = base_args(c);
   o.mode = AsmMode::LOCAL;
+  // class-range algorithm: the operator reads x and writes Z + y interiors
+  // slab by slab, the class owner sum takes the place of owner_periodic_v3
+  int ne = 0;
+  if (use_class) {
+    o.mode = AsmMode::PERIODIC_CLASS;
+    o.n = n;
+    o.xg = dx;
+    o.yg = dy;
+    o.zbuf = ly;
+    o.direct_interior = 1;
+    o.ne_out = &ne;
+  }
   // (writing a pinned y directly from the owner sum over PCIe instead of
   // copying it measured slower: 4.8 ms vs 4.0 ms per apply at P=4, n=64)
   auto owner = [&](int k) -> int {
-    CK(owner_periodic_v3(n, P, ly, dy, 0, s, zb[k] * n, zb[k + 1] * n));
+    if (use_class)
+      CK(class_owner_sum(n, P, ne, ly, dy, 0, 0, s, zb[k] * n, zb[k + 1] * n));
+    else
+      CK(owner_periodic_v3(n, P, ly, dy, 0, s, zb[k] * n, zb[k + 1] * n));
     CK(cudaEventRecord(ev_out[k], s));
     return SPHP_OK;
   };
   for (int k = 0; k < K; ++k) {
     CK(cudaStreamWaitEvent(s, ev_in[k], 0));
     CK(cudaStreamWaitEvent(s, ev_in[(k + 1) % K], 0));
-    CK(periodic_scatter_v2(n, P, dx, lx, s, zb[k] * n, zb[k + 1] * n));
     const int64_t e0 = (int64_t)zb[k] * n2;
     o.E = (int64_t)(zb[k + 1] - zb[k]) * n2;
-    o.in = lx + e0 * nm;
-    o.out = ly + e0 * nm;
-    o.geom = c->geom + e0 * c->gstride;
+    if (use_class) {
+      o.e0 = e0;  // absolute element indexing; x, Z, y and geometry are whole-mesh
+    } else {
+      CK(periodic_scatter_v2(n, P, dx, lx, s, zb[k] * n, zb[k + 1] * n));
+      o.in = lx + e0 * nm;
+      o.out = ly + e0 * nm;
+      o.geom = c->geom + e0 * c->gstride;
+    }
     cudaError_t e = sumfac_launch(c, o, s);
+    if (e == cudaErrorNotSupported && use_class && k == 0) return SPHP_ERR_UNSUPPORTED;  // caller: split
     if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no kernel for this key");
     if (e != cudaSuccess) return cuda_fail(e, "sphp_helmholtz_assembled_host");
     if (k > 0) {
@@ -1642,12 +1710,18 @@ int sphp_helmholtz_assembled_host(sphp_coll* c, const sphp_amap* a, const double
   if (!c || !a || !x || !y) return fail(SPHP_ERR_BAD_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
   if (c->op == SPHP_OP_HELMHOLTZ && c->strategy == SPHP_STRATEGY_CUDA_SUMFAC && a->periodic &&
-      a->alg == SPHP_ASSEMBLY_SPLIT && a->P >= 2 && a->n % 4 == 0 && a->E == c->E && a->nm == c->t->nm &&
-      c->t->shape == SPHP_SHAPE_HEX) {
+      (a->alg == SPHP_ASSEMBLY_SPLIT || a->alg == SPHP_ASSEMBLY_CLASS) && a->P >= 2 && a->n % 4 == 0 &&
+      a->E == c->E && a->nm == c->t->nm && c->t->shape == SPHP_SHAPE_HEX) {
     const std::vector<int> zb = host_slabs(a->n);
     if (zb.size() > 2) {
       if (int rc = amap_device(a)) return rc;
-      return assembled_host_pipelined(c, a, x, y, s, zb);
+      // class-range slabs need the mesh to divide into the operator's tiles
+      // (n % 8 covers every order's tile)
+      const bool use_class = a->alg == SPHP_ASSEMBLY_CLASS && a->n % 8 == 0;
+      const int rc = assembled_host_pipelined(c, a, x, y, s, zb, use_class);
+      // no class-mode tile for this key: the same pipeline on split
+      if (rc == SPHP_ERR_UNSUPPORTED && use_class) return assembled_host_pipelined(c, a, x, y, s, zb, false);
+      return rc;
     }
   }
   const size_t b = sizeof(double) * a->num_global;

@@ -42,6 +42,10 @@ static int helm_variant_env() {
 // one input stage and ~74 KB (local) / ~55 KB (gathering modes) per CTA
 // beat double buffering at every order: more resident CTAs hide more latency
 // than a second stage does.  SPHP_HELM_VARIANT=0..4 overrides for tuning.
+#ifndef SPHP_LOCAL_BUDGET_KB
+#define SPHP_LOCAL_BUDGET_KB 74
+#endif
+
 // PERIODIC_CLASS (pipeline MODE 5) needs an even NE dividing n: the largest
 // of 8 / 4 / 2 elements whose tile fits the budget (SPHP_CLASS_BUDGET_KB,
 // default 74 KB: three resident CTAs per SM at P = 4)
@@ -87,7 +91,7 @@ static cudaError_t helm_go(const OpArgs& oa, cudaStream_t s) {
       default: break;
     }
 #endif
-    if (oa.mode == AsmMode::LOCAL) return helm_variant<M, Q, GK, 1, 74 * 1024>(oa, s);
+    if (oa.mode == AsmMode::LOCAL) return helm_variant<M, Q, GK, 1, SPHP_LOCAL_BUDGET_KB * 1024>(oa, s);
   }
   return helm_variant<M, Q, GK, 1, 55 * 1024>(oa, s);
 }

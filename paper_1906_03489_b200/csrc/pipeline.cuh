@@ -22,6 +22,9 @@
 #include "periodic.cuh"
 #include "../../include/spechp_b200.h"
 
+#ifndef SPHP_CLASS_MINB
+#define SPHP_CLASS_MINB 0
+#endif
 namespace sphp {
 
 __host__ __device__ constexpr int even_up(int x) { return (x + 1) & ~1; }
@@ -198,11 +201,11 @@ struct Scaffold {
   // CTAs per SM that shared memory allows (228 KB per SM, 1 KB reserved per
   // CTA)
   static constexpr int SMEM_CTAS = (int)(233472 / (SMEM_BYTES + 1024)) < 1 ? 1 : (int)(233472 / (SMEM_BYTES + 1024));
-  static constexpr int MIN_CTAS = CLS ? (SMEM_CTAS * NT <= 1024 ? SMEM_CTAS : 1024 / NT) : 1;
+  static constexpr int MIN_CTAS = CLS ? SPHP_CLASS_MINB : 1;
 };
 
 template <class Op, int MODE>
-__global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
+__global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_CTAS : 0)) pipe_kernel(const DevArgs a) {
   using S = Scaffold<Op, MODE>;
   using MT = ModeTraits<MODE>;
   static_assert(S::SMEM_BYTES <= 227 * 1024, "one pipeline stage does not fit in shared memory");
@@ -243,21 +246,31 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
   int* cpre = csd + 27;      // 28
   if constexpr (MT::CLASS) {
     const int b = Op::M - 2;
-    if (tid == 0) {
-      int sb = 0, cb = 0, nc = 0;
-      for (int k = 0; k < 27; ++k) {
-        const ClassGeom cg = class_geom(k, a.n, Op::M - 1);
-        const int sz = class_size(k, b), par = (sz & 1) & class_dx(k);
-        csb[k] = sb;
-        ccb[k] = cb;
+    if (tid < 32) {  // lane k: class k, exclusive prefix sums by warp scan
+      const int k = tid;
+      int sz = 0, par = 0, nch = 0;
+      ClassGeom cg{0, 0, 0};
+      if (k < 27) {
+        cg = class_geom(k, a.n, Op::M - 1);
+        sz = class_size(k, b);
+        par = (sz & 1) & class_dx(k);
+        nch = (par + NE * sz + 1) / 2;
+      }
+      int sb = k < 27 ? NE * sz + 2 : 0, cb = sz, nc = nch;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a1 = __shfl_up_sync(0xffffffffu, sb, o), a2 = __shfl_up_sync(0xffffffffu, cb, o),
+                  a3 = __shfl_up_sync(0xffffffffu, nc, o);
+        if (k >= o) sb += a1, cb += a2, nc += a3;
+      }
+      if (k < 27) {
+        csb[k] = sb - (NE * sz + 2);
+        ccb[k] = cb - sz;
         cR[k] = cg.R;
         csd[k] = sz | (cg.d << 16) | (par << 20);
-        cpre[k] = nc;
-        nc += (par + NE * sz + 1) / 2;
-        sb += NE * sz + 2;
-        cb += sz;
+        cpre[k] = nc - nch;
       }
-      cpre[27] = nc;
+      if (k == 26) cpre[27] = nc;
     }
     __syncthreads();
     for (int i = tid; i < IN; i += NT) {
@@ -267,6 +280,19 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
       const int par = (sz & 1) & class_dx(k);
       ptab[i] = (csb[k] + par + off) | (sz << 16);
       qtab[i] = (NE * ccb[k] + off) | (sz << 16);
+    }
+  }
+  // MODE 5: this thread's input chunks c = tid + j * NT (j < CPT) as
+  // class | slot offset << 5, resolved once (the chunk list is static)
+  constexpr int CPT = MT::CLASS ? (NE * IN + 2 * 27 + 2 * NT - 1) / (2 * NT) : 1;
+  int chunk[CPT];
+  if constexpr (MT::CLASS) {
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int c = tid + j * NT;
+      int k = 0;
+      while (k < 26 && cpre[k + 1] <= c) ++k;
+      chunk[j] = c < cpre[27] ? (k | ((2 * (c - cpre[k])) << 5)) : -1;
     }
   }
   constexpr bool PRE = NE * Op::M * Op::M <= NT;
@@ -442,21 +468,20 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
       const int n = a.n, rowi = w0 / n, ex0 = w0 - rowi * n;
       const int ez = rowi / n, ey = rowi - ez * n;
       const bool wrap = ex0 + NE == n;
-      const int nchunk = cpre[27];
-      for (int c = tid; c < nchunk; c += NT) {
-        int k = 0;  // class of chunk c: cpre[k] <= c < cpre[k + 1]
 #pragma unroll
-        for (int h = 16; h > 0; h >>= 1)
-          if (k + h < 27 && cpre[k + h] <= c) k += h;
-        const int d = 2 * (c - cpre[k]);
-        const int sd = csd[k], sz = sd & 0xffff, dx = (sd >> 16) & 1, par = sd >> 20;
+      for (int j = 0; j < CPT; ++j) {
+        if (chunk[j] < 0) continue;
+        const int k = chunk[j] & 31, d = chunk[j] >> 5;
+        // volatile: keeps ptxas from hoisting these per-chunk constants out
+        // of the tile loop (they would stay live through the pointwise stage)
+        const int sd = ld_volatile_s32(csd + k), sz = sd & 0xffff, dx = (sd >> 16) & 1, par = sd >> 20;
         int y = ey + ((sd >> 17) & 1), z = ez + ((sd >> 18) & 1);
         y -= y >= n ? n : 0;
         z -= z >= n ? n : 0;
-        const int rb = cR[k] + sz * n * (y + n * z);  // class region, this row
+        const int rb = ld_volatile_s32(cR + k) + sz * n * (y + n * z);  // class region, this row
         const int plast = par + (NE - 1) * sz;        // slot offset of the last element
         const int src = (wrap && dx && d >= plast) ? rb + (d - plast) : rb + sz * (ex0 + dx) + d - par;
-        cp_async16(in_s + csb[k] + d, a.xg + src);
+        cp_async16(in_s + ld_volatile_s32(csb + k) + d, a.xg + src);
       }
     }
     cp_async_commit();
@@ -593,14 +618,28 @@ __global__ void __launch_bounds__(Op::NT) pipe_kernel(const DevArgs a) {
       // straight into y when the caller does not accumulate
       // the tile's results leave in two bulk stores: classes 0..25
       // (class-major within the tile) to its record of the tile-major block
-      // Z, the interiors straight into y (or after Z when accumulating)
-      if (tid == 0) {
-        constexpr int b = Op::M - 2, ZS = IN - b * b * b;
-        const int64_t wa = a.e0 + w0, N3 = (int64_t)a.n * a.n * a.n;
-        bulk_s2g(a.zbuf + wa * ZS, out_s, (uint32_t)(sizeof(double) * NE * ZS));
-        double* yint = a.direct_interior ? a.yg + N3 * (1 + 3 * b + 3 * b * b) : a.zbuf + N3 * ZS;
-        bulk_s2g(yint + wa * (b * b * b), out_s + NE * ZS, (uint32_t)(sizeof(double) * NE * b * b * b));
-        bulk_commit();
+      // Z, the interiors straight into y (or after Z when accumulating).
+      // Thread stores when a base is not 16-byte aligned (C-ABI callers may
+      // pass offset pointers); keeping that loop in the kernel also keeps
+      // ptxas at ~100 registers (without it: ~150, two CTAs per SM at P=4)
+      constexpr int b = Op::M - 2, ZS = IN - b * b * b, B3 = b * b * b;
+      const int64_t wa = a.e0 + w0, N3 = (int64_t)a.n * a.n * a.n;
+      double* zdst = a.zbuf + wa * ZS;
+      double* ydst = (a.direct_interior ? a.yg + N3 * (1 + 3 * b + 3 * b * b) : a.zbuf + N3 * ZS) + wa * B3;
+      if (((reinterpret_cast<uintptr_t>(zdst) | reinterpret_cast<uintptr_t>(ydst)) & 15) == 0) {
+        if (tid == 0) {
+          bulk_s2g(zdst, out_s, (uint32_t)(sizeof(double) * NE * ZS));
+          bulk_s2g(ydst, out_s + NE * ZS, (uint32_t)(sizeof(double) * NE * B3));
+          bulk_commit();
+        }
+      } else {
+        for (int i = tid; i < NE * IN; i += NT) {
+          if (i < NE * ZS)
+            zdst[i] = out_s[i];
+          else
+            ydst[i - NE * ZS] = out_s[i];
+        }
+        __syncthreads();  // out_s is rewritten by the next tile
       }
     } else if (bulk_out) {
       const int n = r * OUT, body = (n - head) & ~1;

@@ -31,12 +31,13 @@ def oracle_assembled(amap, oe_by_el, coeff_x, lam, G_by_el, wj_by_el):
 
 
 ALGS = ("owner", "colour", "split")
+PERIODIC_ALGS = ALGS + ("class",)
 
 
-@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("alg", PERIODIC_ALGS)
 @pytest.mark.parametrize("P", [2, 3, 4, 5, 6, 7, 8])
 def test_periodic_hex_assembled(sp, P, alg):
-    n = 4
+    n = 8 if alg == "class" else 4  # class tiles are up to 8 elements of a row
     E = n ** 3
     exp = sp.make_hex(P, P + 2)
     batch = sp.ElementBatch.structured(exp, n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE, amp=0.03)
@@ -56,8 +57,8 @@ def test_periodic_hex_assembled(sp, P, alg):
     assert y.tobytes() == y2.tobytes()
 
 
-@pytest.mark.parametrize("alg", ["split", "owner"])
-@pytest.mark.parametrize("n,P", [(8, 2), (12, 3), (16, 4), (8, 5), (4, 8)])
+@pytest.mark.parametrize("alg", ["split", "owner", "class"])
+@pytest.mark.parametrize("n,P", [(8, 2), (12, 3), (16, 4), (8, 5), (4, 8), (16, 6)])
 def test_host_buffer_apply_matches_device(sp, n, P, alg):
     """sphp_helmholtz_assembled_host (slab-pipelined copies on split maps)
     is bitwise the device-resident apply, for numpy and pinned inputs."""
@@ -76,7 +77,7 @@ def test_host_buffer_apply_matches_device(sp, n, P, alg):
         assert yp.numpy().tobytes() == ref.tobytes()
 
 
-@pytest.mark.parametrize("alg", ALGS)
+@pytest.mark.parametrize("alg", PERIODIC_ALGS)
 def test_scatter_assemble_duality(sp, alg):
     """<A x, v> == <x, A^T v> (test_assembly.py:120-129) on the device."""
     n, P = 4, 3
@@ -237,3 +238,59 @@ def test_slab_operator_single_rank_gpu(sp):
     y = op.apply(op.to_local(x)).cpu().numpy()
     assert np.array_equal(part.gids, np.arange(per.num_global))
     assert_parity(y, ref, what="slab operator, one rank")
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("n", [8, 16, 24])
+def test_class_bitwise_equals_split(sp, n, P):
+    """Class-range assembly (operator gathers x by entity class, tile-major
+    class block, streaming owner sum) sums every dof's terms in the split
+    owner sum's order: the two are bitwise equal, on meshes where the row
+    ends (x wrap) fall inside and at the edge of the operator's tiles."""
+    exp = sp.make_hex(P, P + 2)
+    batch = sp.ElementBatch.structured(exp, n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE, amp=0.03)
+    coll = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC)
+    per = sp.AssemblyMap.hex_periodic(n, P)
+    x = torch.as_tensor(np.random.default_rng(n * 10 + P).uniform(-1, 1, per.num_global), device="cuda")
+    ys = {}
+    for alg in ("split", "class", "class"):
+        per.set_algorithm(alg)
+        y = sp.GlobalHelmholtz([(coll, per)], per.num_global).apply(x).cpu().numpy()
+        if alg in ys:
+            assert y.tobytes() == ys[alg].tobytes(), "class path not reproducible"
+        ys[alg] = y
+    assert ys["class"].tobytes() == ys["split"].tobytes()
+
+
+@pytest.mark.parametrize("P", [3, 4])
+def test_class_accumulate_and_batches(sp, P):
+    """accumulate = 1 (a second batch adds into y): the interiors then go
+    through the class block instead of straight into y."""
+    n = 8
+    exp = sp.make_hex(P, P + 2)
+    batch = sp.ElementBatch.structured(exp, n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE, amp=0.03)
+    c1 = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC, lam=1.0)
+    c2 = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC, lam=0.5)
+    per = sp.AssemblyMap.hex_periodic(n, P).set_algorithm("class")
+    x = torch.as_tensor(np.random.default_rng(P).uniform(-1, 1, per.num_global), device="cuda")
+    both = sp.GlobalHelmholtz([(c1, per), (c2, per)], per.num_global).apply(x)
+    y1 = sp.GlobalHelmholtz([(c1, per)], per.num_global).apply(x)
+    y2 = sp.GlobalHelmholtz([(c2, per)], per.num_global).apply(x)
+    assert_parity(both.cpu().numpy(), (y1 + y2).cpu().numpy(), what="class accumulate")
+
+
+def test_class_unaligned_x_falls_back(sp):
+    """x at an 8-byte (not 16-byte) aligned address: the class gather moves
+    16-byte chunks, so the apply takes the split path — same result."""
+    n, P = 8, 4
+    exp = sp.make_hex(P, P + 2)
+    batch = sp.ElementBatch.structured(exp, n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE, amp=0.03)
+    coll = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC)
+    per = sp.AssemblyMap.hex_periodic(n, P)
+    xs = torch.as_tensor(np.random.default_rng(3).uniform(-1, 1, per.num_global + 1), device="cuda")
+    x_odd = xs[1:]
+    assert x_odd.data_ptr() % 16 == 8
+    op = sp.GlobalHelmholtz([(coll, per)], per.num_global)
+    y = op.apply(x_odd).cpu().numpy()
+    y_ref = op.apply(x_odd.clone()).cpu().numpy()
+    assert y.tobytes() == y_ref.tobytes()

@@ -11,7 +11,7 @@ compared with the CPU oracle (tests/helpers.py tolerances: relative L2 <
   cfg4  64^3 deformed periodic hexes, P=2..8: the fused local Helmholtz on
         the whole mesh, 8192 elements checked (first and last 2048 — the
         first and last tiles of every CTA schedule — and 4096 random);
-        the assembled apply (default split algorithm, the benchmarked path)
+        the assembled apply (default class-range algorithm, the benchmarked path)
         checked exactly on the global dofs of 48 sampled elements (their
         values need only the 27-element neighbourhoods); at P=4 the whole
         assembled vector against a chunked oracle
@@ -193,7 +193,7 @@ def test_cfg4_assembled_64_sampled(sp, P):
     E = n ** 3
     batch, coll = _cfg4(sp, P, n)
     amap = sp.AssemblyMap.hex_periodic(n, P)
-    assert amap.algorithm == "split"
+    assert amap.algorithm == ("split" if P == 7 else "class")
     op = sp.GlobalHelmholtz([(coll, amap)], amap.num_global)
     ng = amap.num_global
     x = np.random.default_rng(SEED + 10 * P).uniform(-1, 1, ng)
@@ -211,12 +211,14 @@ def test_cfg4_assembled_64_sampled(sp, P):
     assert_parity(y[dofs], yref[dofs], what=f"cfg4 assembled P{P} 64^3 ({dofs.size} dofs)")
 
 
-def test_cfg4_assembled_64_full_p4(sp):
-    """The headline apply (P=4, 64^3, split) against the whole oracle vector."""
+@pytest.mark.parametrize("alg", ["class", "split"])
+def test_cfg4_assembled_64_full_p4(sp, alg):
+    """The headline apply (P=4, 64^3; class = the default and benchmarked
+    algorithm, split its fallback) against the whole oracle vector."""
     n, P = 64, 4
     E = n ** 3
     batch, coll = _cfg4(sp, P, n)
-    amap = sp.AssemblyMap.hex_periodic(n, P)
+    amap = sp.AssemblyMap.hex_periodic(n, P).set_algorithm(alg)
     op = sp.GlobalHelmholtz([(coll, amap)], amap.num_global)
     ng = amap.num_global
     x = np.random.default_rng(SEED).uniform(-1, 1, ng)
@@ -226,7 +228,7 @@ def test_cfg4_assembled_64_full_p4(sp):
     yl = _pool_apply("helmholtz", "hex", P, P + 2, n, np.arange(E), og.MAP_HEX_SINE, 0.03,
                      _gather(codes, x), chunk=8192)
     yref = _assemble_ref(codes, yl, ng)
-    assert_parity(y, yref, what="cfg4 assembled P4 64^3 (full vector)")
+    assert_parity(y, yref, what=f"cfg4 assembled P4 64^3 (full vector, {alg})")
 
 
 # ---------------------------------------------------------------------------

@@ -126,15 +126,23 @@ def test_explicit_map_from_reference_roundtrip(tag):
 
 
 def test_default_assembly_algorithm():
-    """Periodic maps the class-range kernels support default to split,
-    everything else to owner; set_algorithm round-trips through the C ABI."""
-    assert sp.AssemblyMap.hex_periodic(8, 4).algorithm == "split"
-    assert sp.AssemblyMap.hex_periodic(6, 4).algorithm == "owner"   # n % 4 != 0
+    """Periodic maps default to the class-range algorithm (split at P = 7,
+    where it measures faster; owner without bubbles), explicit maps to
+    owner; set_algorithm round-trips through the C ABI and class-range
+    assembly is refused on explicit maps."""
+    assert sp.AssemblyMap.hex_periodic(8, 4).algorithm == "class"
+    assert sp.AssemblyMap.hex_periodic(6, 4).algorithm == "class"   # runtime fallback: split
+    assert sp.AssemblyMap.hex_periodic(8, 7).algorithm == "split"
     assert sp.AssemblyMap.hex_periodic(8, 1).algorithm == "owner"   # no bubbles
+    per = sp.AssemblyMap.hex_periodic(8, 3)
+    for alg in ("colour", "split", "owner", "class"):
+        assert per.set_algorithm(alg).algorithm == alg
     am = sp.AssemblyMap.explicit(np.array([[0, 1, 2], [2, 3, 0]]), 4)
     assert am.algorithm == "owner"
     for alg in ("colour", "split", "owner"):
         assert am.set_algorithm(alg).algorithm == alg
+    with pytest.raises(sp.AssemblyError, match="periodic"):
+        am.set_algorithm("class")
     with pytest.raises(KeyError):
         am.set_algorithm("atomic")
 
