@@ -544,32 +544,48 @@ struct OwnerGeom {
 // class run; the a = 1 term is u - S, or the previous tile's last element
 // (x wraps to n - 1 at t = 0) when u < S.
 template <int P, int NE, int R>
-__device__ __forceinline__ double owned_sum(const double* const* zr, const double* const* zi, int T, int li) {
+__device__ __forceinline__ void owned_sum2(const double* __restrict__ Z, const int* zr, const int* zi, int T,
+                                           int li, double& acc0, double& acc1) {
+  // outputs li and li + 1 (li even): same region (n S is even), same tile
+  // run (NE S is even), so the index math is shared and 2 NC loads are in
+  // flight per thread
   using G = OwnerGeom<P>;
   constexpr int S = G::S(R), NC = Region<R>::NC, RUN = NE * S, REC = NE * G::ZS;
   const int t = li / RUN, u = li - t * RUN;
-  double v[NC];
+  const int tp = t == 0 ? T - 1 : t - 1;  // tile of the x - 1 neighbour at u < S
+  double v0[NC], v1[NC];
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
     const int bc = Region<R>::b(j) * 2 + Region<R>::c(j);
     if constexpr (R == 7) {
-      v[j] = __ldg(zi[bc] + li);
+      v0[j] = __ldg(Z + zi[bc] + li);
+      v1[j] = __ldg(Z + zi[bc] + li + 1);
     } else {
       const int cls = NE * class_cb(Region<R>::k(j), G::b);
-      int off = t * REC + cls + u;
-      if (Region<R>::a(j)) off = u >= S ? off - S : (t == 0 ? T - 1 : t - 1) * REC + cls + (NE - 1) * S + u;
-      v[j] = __ldg(zr[bc] + off);
+      const int off = zr[bc] + t * REC + cls + u;
+      if (Region<R>::a(j)) {
+        const int wrapd = zr[bc] + tp * REC + cls + (NE - 1) * S;  // + u: last element of the tile before
+        v0[j] = __ldg(Z + (u >= S ? off - S : wrapd + u));
+        v1[j] = __ldg(Z + (u + 1 >= S ? off + 1 - S : wrapd + u + 1));
+      } else {
+        v0[j] = __ldg(Z + off);
+        v1[j] = __ldg(Z + off + 1);
+      }
     }
   }
-  double acc = v[0];
+  acc0 = v0[0];
+  acc1 = v1[0];
 #pragma unroll
-  for (int j = 1; j < NC; ++j) acc += v[j];
-  return acc;
+  for (int j = 1; j < NC; ++j) {
+    acc0 += v0[j];
+    acc1 += v1[j];
+  }
 }
 
 // one CTA per (ey, ez) row at a time: all regions' n * (P^3 [- (P-1)^3])
-// owned dofs of the row as one index space (the region of an output is a
-// few compares), so every thread has work at every order
+// owned dofs of the row as one index space of output pairs (the region of
+// an output is a few compares), so every thread has work at every order.
+// 32-bit offsets from Z: n^3 nm < 2^31 for every map the kernels accept.
 template <int P, int NE>
 __global__ void __launch_bounds__(256, CLASS_OWNER_MINB) class_owner_sum_kernel(int n, const double* __restrict__ Z,
                                                               double* __restrict__ y, int accumulate,
@@ -582,23 +598,22 @@ __global__ void __launch_bounds__(256, CLASS_OWNER_MINB) class_owner_sum_kernel(
     const int ez = row / n, ey = row - ez * n;
     const int ym = ey == 0 ? n - 1 : ey - 1, zm = ez == 0 ? n - 1 : ez - 1;
     const int nr[4] = {ey + n * ez, ey + n * zm, ym + n * ez, ym + n * zm};  // (b, c) = 00, 01, 10, 11
-    const double* zr[4];
-    const double* zi[4];
+    int zr[4], zi[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      zr[q] = Z + (int64_t)nr[q] * n * G::ZS;
-      zi[q] = Z + N3 * G::ZS + (int64_t)nr[q] * n * G::S(7);
+      zr[q] = nr[q] * n * G::ZS;
+      zi[q] = (int)(N3 * G::ZS) + nr[q] * n * G::S(7);
     }
-    for (int i = threadIdx.x; i < per_row; i += blockDim.x) {
+    for (int i = 2 * threadIdx.x; i < per_row; i += 2 * blockDim.x) {
       int r = 0;
 #pragma unroll
       for (int q = 1; q < 8; ++q) r += i >= n * G::start(q) ? 1 : 0;
-      double acc;
+      double a0, a1;
       int64_t g;
 #define REGION(R)                                                \
   case R: {                                                      \
     const int li = i - n * G::start(R);                          \
-    acc = owned_sum<P, NE, R>(zr, zi, T, li);                    \
+    owned_sum2<P, NE, R>(Z, zr, zi, T, li, a0, a1);              \
     g = N3 * G::ybase(R) + (int64_t)row * n * G::S(R) + li;      \
     break;                                                       \
   }
@@ -606,7 +621,8 @@ __global__ void __launch_bounds__(256, CLASS_OWNER_MINB) class_owner_sum_kernel(
         REGION(0) REGION(1) REGION(2) REGION(3) REGION(4) REGION(5) REGION(6) REGION(7)
       }
 #undef REGION
-      y[g] = accumulate ? y[g] + acc : acc;
+      y[g] = accumulate ? y[g] + a0 : a0;
+      y[g + 1] = accumulate ? y[g + 1] + a1 : a1;
     }
   }
 }
