@@ -19,9 +19,18 @@
  *   - return value: SPHP_OK (0) or a negative SPHP_ERR_*; the message is in
  *     sphp_last_error() (thread-local), with the reference's wording where
  *     the reference raises (CollectionError text, collections.py:197-200).
- *   - handles are immutable after create (except set_lambda) and apply is
- *     re-entrant on distinct streams; repeated applies are bitwise equal
- *     (test_collections.py:193-201) — no floating-point atomics anywhere.
+ *   - handles are immutable after create (except set_lambda, which must not
+ *     run concurrently with applies of the handle; collections.py:76-90):
+ *     device tables, StdMat operators and map tables are built by create.
+ *     Everything an apply writes besides its output lives in a per-stream
+ *     workspace of the handle, so applies of one handle on distinct streams
+ *     may run concurrently (from any host threads); applies on one stream
+ *     are ordered by it.  A stream's workspace is sized at its first apply
+ *     (cudaMalloc) or by sphp_collection_reserve / sphp_gsys_reserve; an
+ *     apply captured into a CUDA graph must find it reserved (otherwise it
+ *     fails with SPHP_ERR_BAD_ARG instead of allocating inside the capture).
+ *   - repeated applies are bitwise equal (test_collections.py:193-201) — no
+ *     floating-point atomics anywhere.
  */
 #ifndef SPECHP_B200_H
 #define SPECHP_B200_H
@@ -209,6 +218,13 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x,
 int sphp_helmholtz_assembled_host(sphp_coll* c, const sphp_amap* a,
                                   const double* x, double* y,
                                   sphp_stream stream);
+/* pre-size the per-stream workspace of `c` for applies on `stream`:
+ * SPHP_RESERVE_DEVICE — sphp_apply and, with map `a` (may be NULL),
+ * sphp_helmholtz_assembled; SPHP_RESERVE_HOST — the *_host paths.          */
+#define SPHP_RESERVE_DEVICE 1
+#define SPHP_RESERVE_HOST 2
+int sphp_collection_reserve(sphp_coll* c, const sphp_amap* a, int flags,
+                            sphp_stream stream);
 /* measurement: one apply (accumulate = 0) with a CUDA event after each of
  * its launches on `stream`; synchronises and writes the launches'
  * durations (ms) to ms[0 .. *nphases)  (class: operator, owner sum;
@@ -228,6 +244,7 @@ typedef struct sphp_gsys sphp_gsys;
 int sphp_gsys_create(sphp_coll* const* colls, const sphp_amap* const* maps,
                      int nbatch, int64_t num_global, sphp_gsys** out);
 int sphp_gsys_apply(sphp_gsys* g, const double* x, double* y, sphp_stream stream);
+int sphp_gsys_reserve(sphp_gsys* g, sphp_stream stream);  /* workspace of `stream` */
 int sphp_gsys_destroy(sphp_gsys* g);
 
 /* ---- solver support: GlobalSystem.diag / solve_pcg (assembly.py:185-266) -- */
@@ -250,6 +267,20 @@ int sphp_cg_update(int64_t n, double alpha, const double* p, const double* ap,
 /* p = z + beta p                                                            */
 int sphp_cg_direction(int64_t n, double beta, const double* z, double* p,
                       sphp_stream stream);
+/* the same iteration with the scalars on the device (no host round trip;
+ * a chunk of iterations can be captured into a CUDA graph): `st` holds
+ * sphp_cg_state_size(max_iter) doubles — st[0] rz, st[1] rr, st[5] |rhs|,
+ * st[7] converged flag, st[8] iterations, st[9 + k] residual of iteration
+ * k; init sets x = 0, r = rhs, z = p = dinv r; each step takes ap = A p and
+ * does alpha = rz / p.Ap, the update, the residual test against `tol`
+ * and the new direction; steps after convergence leave x unchanged.     */
+int64_t sphp_cg_state_size(int max_iter);
+int sphp_cg_init_dev(int64_t n, const double* rhs, const double* dinv, double* x,
+                     double* r, double* z, double* p, double* st, int max_iter,
+                     double tol, sphp_stream stream);
+int sphp_cg_step_dev(int64_t n, const double* p, const double* ap, double* x, double* r,
+                     const double* dinv, double* z, double* st, int max_iter,
+                     sphp_stream stream);
 /* build_assembly_map (assembly.py:72-138) for meshio.structured_quad_mesh
  * (meshio.py:377-413) with per-element orders; dirichlet_mask bits:
  * 1 south, 2 east, 4 north, 8 west.  Codes packed per element (m_e^2 each,

@@ -32,6 +32,7 @@ STRATEGY_CUDA_SUMFAC, STRATEGY_CUDA_STDMAT = 0, 1
 GEOM_NONE, GEOM_AFFINE, GEOM_POINT, GEOM_METRIC = 0, 1, 2, 3
 MAP_AFFINE, MAP_QUAD_SINE, MAP_HEX_SINE = 0, 1, 2
 ASSEMBLY_OWNER, ASSEMBLY_COLOUR, ASSEMBLY_SPLIT, ASSEMBLY_CLASS = 0, 1, 2, 3
+RESERVE_DEVICE, RESERVE_HOST = 1, 2
 RIEMANN = {"upwind": 0, "laxfriedrichs": 1}
 BC_INTERIOR, BC_RIGID_WALL, BC_FARFIELD, BC_DIRICHLET = 0, 1, 2, 3
 
@@ -93,6 +94,8 @@ _SIGS = {
     "sphp_helmholtz_assembled": (_i, [_p, _p, _p, _p, _i, _p]),
     "sphp_helmholtz_assembled_host": (_i, [_p, _p, _p, _p, _p]),
     "sphp_helmholtz_assembled_phases": (_i, [_p, _p, _p, _p, _p, _i, _p, _p]),
+    "sphp_collection_reserve": (_i, [_p, _p, _i, _p]),
+    "sphp_gsys_reserve": (_i, [_p, _p]),
     "sphp_gsys_create": (_i, [_pp, _pp, _i, _i64, _pp]),
     "sphp_gsys_apply": (_i, [_p, _p, _p, _p]),
     "sphp_gsys_destroy": (_i, [_p]),
@@ -102,6 +105,9 @@ _SIGS = {
     "sphp_cg_init": (_i, [_i64, _p, _p, _p, _p, _p, _p, _p, _p]),
     "sphp_cg_update": (_i, [_i64, _d, _p, _p, _p, _p, _p, _p, _p, _p]),
     "sphp_cg_direction": (_i, [_i64, _d, _p, _p, _p]),
+    "sphp_cg_state_size": (_i64, [_i]),
+    "sphp_cg_init_dev": (_i, [_i64, _p, _p, _p, _p, _p, _p, _p, _i, _d, _p]),
+    "sphp_cg_step_dev": (_i, [_i64, _p, _p, _p, _p, _p, _p, _p, _i, _p]),
     "sphp_quadmap_structured": (_i, [_i, _i, _p, _i, _i64p, _i64p, _p, _p]),
     "sphp_geom_from_jacobian": (_i, [_p, _i, _i64, _p, _p, _p, _i64p, _p]),
     "sphp_batched_matvec": (_i, [_i64, _i, _i, _p, _p, _p, _d, _i, _p, _p]),

@@ -207,6 +207,19 @@ class GlobalHelmholtz:
                        AssemblyError)
             self._gsys = h
 
+    def reserve(self, stream=None, host=False):
+        """Size the per-stream workspaces this operator's applies on `stream`
+        use (they are otherwise sized at the first apply on a stream); needed
+        before capturing applies into a CUDA graph."""
+        if self._gsys is not None:
+            _lib.check(_lib.lib.sphp_gsys_reserve(self._gsys, _lib.stream_ptr(stream)), AssemblyError)
+            return self
+        flags = _lib.RESERVE_DEVICE | (_lib.RESERVE_HOST if host else 0)
+        for coll, amap in self.batches:
+            _lib.check(_lib.lib.sphp_collection_reserve(coll._handle, amap._h, flags, _lib.stream_ptr(stream)),
+                       AssemblyError)
+        return self
+
     def __del__(self):
         h = getattr(self, "_gsys", None)
         if h and _lib is not None and _lib.lib is not None:

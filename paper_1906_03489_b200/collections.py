@@ -230,6 +230,15 @@ class Collection:
 
     __call__ = apply
 
+    def reserve(self, stream=None, host=False):
+        """Size the per-stream workspace of applies on `stream` (StdMat
+        scratch; host staging with host=True) ahead of the first apply, e.g.
+        before capturing applies into a CUDA graph."""
+        flags = _lib.RESERVE_DEVICE | (_lib.RESERVE_HOST if host else 0)
+        _lib.check(_lib.lib.sphp_collection_reserve(self._handle, None, flags, _lib.stream_ptr(stream)),
+                   CollectionError)
+        return self
+
     # -- cost model (collections.py:250-273 generalised) ------------------------
     def mac_count(self):
         return self._macs

@@ -90,10 +90,62 @@ struct DevBuf {
     if (e == cudaSuccess) bytes = b;
     return e;
   }
+  // growth on a stream that is being captured would put cudaMalloc into the
+  // graph: refused (reserve the workspace before capturing)
+  cudaError_t ensure_on(size_t b, cudaStream_t s) {
+    if (p && bytes >= b) return cudaSuccess;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (s) cudaStreamIsCapturing(s, &cap);
+    if (cap != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;
+    return ensure(b);
+  }
   template <class T>
   T* as() const {
     return reinterpret_cast<T*>(p);
   }
+};
+
+// Per-stream workspace of a handle: everything an apply writes besides its
+// output.  Applies on distinct streams get distinct workspaces, so one
+// handle may be applied concurrently on several streams (the handle itself
+// is immutable after create); applies on one stream are ordered by it.
+// Buffers are sized on first use on the stream (or by sphp_*_reserve,
+// which a caller must do before capturing applies into a CUDA graph) and
+// never shrink.
+struct Workspace {
+  DevBuf loc_x, loc_y;       // local blocks (split / owner / stdmat assembled), Z (class)
+  DevBuf scratch;            // StdMat pointwise buffers
+  DevBuf host_in, host_out;  // host-buffer applies: device staging
+  DevBuf ctr;                // dynamic segment schedule counters (periodic kernels)
+  // host-buffer pipeline: copy streams and per-slab events
+  cudaStream_t pipe_h2d = nullptr, pipe_d2h = nullptr;
+  std::vector<cudaEvent_t> pipe_ev;
+  // sphp_gsys: one stream per batch and its events
+  std::vector<cudaStream_t> bs;
+  std::vector<cudaEvent_t> bev;
+  ~Workspace() {
+    for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : bev) cudaEventDestroy(e);
+    for (cudaStream_t q : bs) cudaStreamDestroy(q);
+    if (pipe_h2d) cudaStreamDestroy(pipe_h2d);
+    if (pipe_d2h) cudaStreamDestroy(pipe_d2h);
+  }
+  int* counter() { return ctr.ensure(2 * sizeof(int)) == cudaSuccess ? ctr.as<int>() : nullptr; }
+};
+
+class WorkspacePool {
+ public:
+  Workspace* get(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (auto& kv : v_)
+      if (kv.first == s) return kv.second.get();
+    v_.emplace_back(s, std::make_unique<Workspace>());
+    return v_.back().second.get();
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<std::pair<cudaStream_t, std::unique_ptr<Workspace>>> v_;
 };
 
 }  // namespace
@@ -207,21 +259,10 @@ struct sphp_coll {
   const double* geom = nullptr;
   int64_t gstride = 0, cs = 0;
   double lam = 0.0;
-  // workspaces
-  DevBuf host_in, host_out;       // apply_host staging
-  DevBuf scratch;                 // StdMat pointwise buffers
-  DevBuf mat_a, mat_b;            // StdMat dense operators
-  DevBuf helm_H;                  // StdMat Helmholtz element matrices
-  DevBuf loc_x, loc_y;            // StdMat assembled path
-  // host-buffer pipeline (sphp_helmholtz_assembled_host): copy streams and
-  // per-slab events, created on first use
-  cudaStream_t pipe_h2d = nullptr, pipe_d2h = nullptr;
-  std::vector<cudaEvent_t> pipe_ev;
-  ~sphp_coll() {
-    for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
-    if (pipe_h2d) cudaStreamDestroy(pipe_h2d);
-    if (pipe_d2h) cudaStreamDestroy(pipe_d2h);
-  }
+  // StdMat operators, built at create (and by set_lambda for Helmholtz)
+  DevBuf mat_a;   // dense elemental operator
+  DevBuf helm_H;  // Helmholtz element matrices
+  WorkspacePool ws;
 };
 
 struct sphp_amap {
@@ -407,36 +448,42 @@ PointJob point_job(const sphp_coll* c) {
   return j;
 }
 
-// build the StdMat operators of a collection (once)
-int stdmat_prepare(sphp_coll* c, cudaStream_t s) {
+// build the StdMat operators of a collection: at create (and, for the
+// Helmholtz element matrices, which depend on lambda, in set_lambda), on a
+// private stream, synchronously — applies never build or allocate them
+int stdmat_prepare(sphp_coll* c) {
   sphp_tables* t = c->t;
   const int64_t nm = t->nm, np = t->np;
   const int d = t->dim;
   if (c->op == SPHP_OP_HELMHOLTZ) {
-    if (c->helm_H.p) return SPHP_OK;
     if (!t->fast)
       return fail(SPHP_ERR_UNSUPPORTED, "stdmat Helmholtz needs a sum-factorisation key to build H_e");
     const double bytes = 8.0 * c->E * nm * nm;
     if (bytes > 16e9)
       return fail(SPHP_ERR_UNSUPPORTED, "stdmat Helmholtz element matrices exceed the 16 GB budget");
     CK(c->helm_H.ensure((size_t)bytes));
-    CK(c->loc_x.ensure(sizeof(double) * c->E * nm));
-    CK(c->loc_y.ensure(sizeof(double) * c->E * nm));
+    DevBuf ux, uy;
+    CK(ux.ensure(sizeof(double) * c->E * nm));
+    CK(uy.ensure(sizeof(double) * c->E * nm));
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     // column n of every H_e = fused Helmholtz applied to unit vector e_n
     OpArgs a = base_args(c);
-    for (int n = 0; n < nm; ++n) {
-      CK(unit_block(c->E, (int)nm, n, c->loc_x.as<double>(), s));
-      a.in = c->loc_x.as<double>();
-      a.out = c->loc_y.as<double>();
-      cudaError_t e = sumfac_launch(c, a, s);
-      if (e != cudaSuccess) return cuda_fail(e, "stdmat Helmholtz build");
-      CK(store_column(c->E, (int)nm, n, c->loc_y.as<double>(), c->helm_H.as<double>(), s));
+    cudaError_t e = cudaSuccess;
+    for (int n = 0; n < nm && e == cudaSuccess; ++n) {
+      e = unit_block(c->E, (int)nm, n, ux.as<double>(), s);
+      a.in = ux.as<double>();
+      a.out = uy.as<double>();
+      if (e == cudaSuccess) e = sumfac_launch(c, a, s);
+      if (e == cudaSuccess) e = store_column(c->E, (int)nm, n, uy.as<double>(), c->helm_H.as<double>(), s);
     }
-    CK(symmetrise(c->E, (int)nm, c->helm_H.as<double>(), s));  // geometry.py:184
-    CK(cudaStreamSynchronize(s));
+    if (e == cudaSuccess) e = symmetrise(c->E, (int)nm, c->helm_H.as<double>(), s);  // geometry.py:184
+    const cudaError_t e2 = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (e != cudaSuccess) return cuda_fail(e, "stdmat Helmholtz build");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "stdmat Helmholtz build");
     return SPHP_OK;
   }
-  if (c->mat_a.p) return SPHP_OK;
   std::vector<double> Bm = dense_bwd(t);  // (nm, np)
   std::vector<double> A;
   switch (c->op) {
@@ -472,9 +519,21 @@ int stdmat_prepare(sphp_coll* c, cudaStream_t s) {
   return SPHP_OK;
 }
 
+int ws_fail(cudaError_t e, const char* where) {
+  if (e == cudaErrorStreamCaptureUnsupported)
+    return fail(SPHP_ERR_BAD_ARG, std::string(where) +
+                                      ": the workspace of this stream is not reserved (call the handle's "
+                                      "reserve entry point before capturing applies into a CUDA graph)");
+  return cuda_fail(e, where);
+}
+#define CKW(call)                                         \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return ws_fail(_e, #call);     \
+  } while (0)
+
 int stdmat_apply(sphp_coll* c, const double* in, double* out, cudaStream_t s) {
-  int rc = stdmat_prepare(c, s);
-  if (rc) return rc;
+  Workspace* w = c->ws.get(s);
   sphp_tables* t = c->t;
   const int64_t nm = t->nm, np = t->np;
   const int d = t->dim;
@@ -484,18 +543,18 @@ int stdmat_apply(sphp_coll* c, const double* in, double* out, cudaStream_t s) {
       CK(dgemm(c->E, (int)np, (int)nm, in, A, out, s));
       break;
     case SPHP_OP_IPRODUCT_WRT_BASE:
-      CK(c->scratch.ensure(sizeof(double) * c->E * np));
-      CK(pointwise(0, point_job(c), in, c->scratch.as<double>(), s));
-      CK(dgemm(c->E, (int)nm, (int)np, c->scratch.as<double>(), A, out, s));
+      CKW(w->scratch.ensure_on(sizeof(double) * c->E * np, s));
+      CK(pointwise(0, point_job(c), in, w->scratch.as<double>(), s));
+      CK(dgemm(c->E, (int)nm, (int)np, w->scratch.as<double>(), A, out, s));
       break;
     case SPHP_OP_PHYS_DERIV:
       CK(dgemm(c->E, (int)(d * np), (int)np, in, A, out, s));
       if (c->geom_kind != SPHP_GEOM_NONE) CK(pointwise(1, point_job(c), nullptr, out, s));
       break;
     case SPHP_OP_IPRODUCT_WRT_DERIV_BASE:
-      CK(c->scratch.ensure(sizeof(double) * c->E * d * np));
-      CK(pointwise(2, point_job(c), in, c->scratch.as<double>(), s));
-      CK(dgemm(c->E, (int)nm, (int)(d * np), c->scratch.as<double>(), A, out, s));
+      CKW(w->scratch.ensure_on(sizeof(double) * c->E * d * np, s));
+      CK(pointwise(2, point_job(c), in, w->scratch.as<double>(), s));
+      CK(dgemm(c->E, (int)nm, (int)(d * np), w->scratch.as<double>(), A, out, s));
       break;
     case SPHP_OP_HELMHOLTZ:
       CK(elem_matvec(c->E, (int)nm, c->helm_H.as<double>(), in, out, s));
@@ -919,6 +978,13 @@ int sphp_collection_create(const sphp_tables* tc, int op, int strategy, int64_t 
     case SPHP_OP_IPRODUCT_WRT_DERIV_BASE: c->in_size = d * t->np; c->out_size = t->nm; break;
     case SPHP_OP_HELMHOLTZ: c->in_size = t->nm; c->out_size = t->nm; break;
   }
+  if (strategy == SPHP_STRATEGY_CUDA_STDMAT) {
+    rc = stdmat_prepare(c);
+    if (rc) {
+      delete c;
+      return rc;
+    }
+  }
   *out = c;
   return SPHP_OK;
 }
@@ -928,14 +994,13 @@ int sphp_collection_destroy(sphp_coll* c) {
   return SPHP_OK;
 }
 
+// the one mutation a handle allows (collections.py: lam is a constructor
+// argument there); not concurrent with applies of the handle
 int sphp_collection_set_lambda(sphp_coll* c, double lambda) {
   if (!c) return fail(SPHP_ERR_BAD_ARG, "null collection");
-  if (c->strategy == SPHP_STRATEGY_CUDA_STDMAT && c->helm_H.p && lambda != c->lam) {
-    cudaFree(c->helm_H.p);  // dense H_e depends on lambda: rebuild lazily
-    c->helm_H.p = nullptr;
-    c->helm_H.bytes = 0;
-  }
+  const bool rebuild = c->strategy == SPHP_STRATEGY_CUDA_STDMAT && c->op == SPHP_OP_HELMHOLTZ && lambda != c->lam;
   c->lam = lambda;
+  if (rebuild) return stdmat_prepare(c);  // dense H_e depends on lambda
   return SPHP_OK;
 }
 
@@ -975,14 +1040,54 @@ int sphp_apply_host(sphp_coll* c, int64_t E, int64_t n_in, const double* in, dou
   if (!c) return fail(SPHP_ERR_BAD_ARG, "null collection");
   if (E != c->E || n_in != c->in_size) return sphp_apply(c, E, n_in, in, out, stream);
   cudaStream_t s = (cudaStream_t)stream;
+  Workspace* w = c->ws.get(s);
   const size_t bi = sizeof(double) * c->E * c->in_size, bo = sizeof(double) * c->E * c->out_size;
-  CK(c->host_in.ensure(bi));
-  CK(c->host_out.ensure(bo));
-  CK(cudaMemcpyAsync(c->host_in.p, in, bi, cudaMemcpyHostToDevice, s));
-  int rc = sphp_apply(c, E, n_in, c->host_in.as<double>(), c->host_out.as<double>(), stream);
+  CKW(w->host_in.ensure_on(bi, s));
+  CKW(w->host_out.ensure_on(bo, s));
+  CK(cudaMemcpyAsync(w->host_in.p, in, bi, cudaMemcpyHostToDevice, s));
+  int rc = sphp_apply(c, E, n_in, w->host_in.as<double>(), w->host_out.as<double>(), stream);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(out, c->host_out.p, bo, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(out, w->host_out.p, bo, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return SPHP_OK;
+}
+
+static int amap_device(const sphp_amap* ac);
+
+// Allocate the per-stream workspace a later apply on `stream` would size on
+// first use (so that apply can be captured into a CUDA graph): device
+// applies (StdMat scratch; with a map, the local blocks / class block and
+// the schedule counters of the assembled apply) and, with
+// SPHP_RESERVE_HOST, the host-buffer staging and copy pipeline.
+int sphp_collection_reserve(sphp_coll* c, const sphp_amap* a, int flags, sphp_stream stream) {
+  if (!c) return fail(SPHP_ERR_BAD_ARG, "null collection");
+  cudaStream_t s = (cudaStream_t)stream;
+  Workspace* w = c->ws.get(s);
+  const int64_t E = c->E, nm = c->t->nm, np = c->t->np, d = c->t->dim;
+  if (flags & SPHP_RESERVE_DEVICE) {
+    if (c->strategy == SPHP_STRATEGY_CUDA_STDMAT) CKW(w->scratch.ensure_on(sizeof(double) * E * d * np, s));
+    if (a) {
+      CKW(w->loc_x.ensure_on(sizeof(double) * E * nm, s));
+      CKW(w->loc_y.ensure_on(sizeof(double) * E * nm, s));
+      CKW(w->ctr.ensure_on(2 * sizeof(int), s));
+      if (int rc = amap_device(a)) return rc;
+    }
+  }
+  if (flags & SPHP_RESERVE_HOST) {
+    int64_t hb = std::max(E * c->in_size, E * c->out_size);
+    if (a) hb = std::max<int64_t>(hb, a->num_global);
+    CKW(w->host_in.ensure_on(sizeof(double) * hb, s));
+    CKW(w->host_out.ensure_on(sizeof(double) * hb, s));
+    if (a) {
+      CKW(w->loc_x.ensure_on(sizeof(double) * E * nm, s));
+      CKW(w->loc_y.ensure_on(sizeof(double) * E * nm, s));
+      CKW(w->ctr.ensure_on(2 * sizeof(int), s));
+      if (!w->pipe_h2d) {
+        CK(cudaStreamCreateWithFlags(&w->pipe_h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&w->pipe_d2h, cudaStreamNonBlocking));
+      }
+    }
+  }
   return SPHP_OK;
 }
 
@@ -1022,17 +1127,31 @@ static int amap_colour_and_upload(sphp_amap* a) {
   return SPHP_OK;
 }
 
-// device copies of an explicit map, made on first device use
+// device tables of a map, built when the map is created (explicit maps:
+// codes, colour lists, CSR) or switched to the owner algorithm (periodic
+// maps: the (E, 27) entity table only the gathering owner path reads);
+// applies find them built and never allocate.  (Without a visible device,
+// e.g. host-only map construction, the build waits for the first device
+// call.)
+static bool device_present() {
+  int n = 0;
+  return cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+}
 static int amap_device(const sphp_amap* ac) {
   sphp_amap* a = const_cast<sphp_amap*>(ac);
   if (a->periodic) {
-    if (a->d_entity.p) return SPHP_OK;
+    if (a->alg != SPHP_ASSEMBLY_OWNER) return SPHP_OK;
     std::lock_guard<std::mutex> lk(a->mu);
     if (a->d_entity.p) return SPHP_OK;
     DevBuf tmp;
     CK(tmp.ensure(sizeof(int) * a->E * 27));
-    CK(periodic_entity_table(a->n, a->P, tmp.as<int>(), 0));
-    CK(cudaDeviceSynchronize());
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaError_t e = periodic_entity_table(a->n, a->P, tmp.as<int>(), s);
+    const cudaError_t e2 = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    CK(e);
+    CK(e2);
     std::swap(a->d_entity.p, tmp.p);
     std::swap(a->d_entity.bytes, tmp.bytes);
     return SPHP_OK;
@@ -1073,10 +1192,10 @@ static int amap_device(const sphp_amap* ac) {
 
 // local (E, nm) -> global with the map's algorithm; accumulate adds to g
 static int amap_assemble_any(const sphp_amap* a, const double* loc, double* g, int accumulate,
-                             cudaStream_t s, int mode_major = 0) {
+                             cudaStream_t s, int mode_major = 0, int* ctr = nullptr) {
   if (a->alg == SPHP_ASSEMBLY_OWNER || a->alg == SPHP_ASSEMBLY_SPLIT || a->alg == SPHP_ASSEMBLY_CLASS) {
     if (a->periodic) {
-      CK(owner_assemble_periodic(a->n, a->P, loc, g, accumulate, mode_major, s));
+      CK(owner_assemble_periodic(a->n, a->P, loc, g, accumulate, mode_major, s, ctr));
     } else {
       CK(owner_assemble_csr(a->num_global, a->d_rowp.as<int64_t>(), a->d_ent.as<int>(), loc, g,
                             accumulate, a->nm, a->E, mode_major, s));
@@ -1103,6 +1222,7 @@ int sphp_amap_create_explicit(int64_t E, int nmodes, const int64_t* codes, int64
   a->num_global = num_global;
   a->codes_host.assign(codes, codes + E * nmodes);
   int rc = amap_colour_and_upload(a);
+  if (!rc && device_present()) rc = amap_device(a);
   if (rc) {
     delete a;
     return rc;
@@ -1131,6 +1251,10 @@ int sphp_amap_create_hex_periodic(int n, int P, sphp_amap** out) {
   if (a->num_global > 2147483645LL) {
     delete a;
     return fail(SPHP_ERR_UNSUPPORTED, "periodic map with more than 2^31-3 global dofs");
+  }
+  if (int rc = device_present() ? amap_device(a) : SPHP_OK) {
+    delete a;
+    return rc;
   }
   *out = a;
   return SPHP_OK;
@@ -1229,7 +1353,7 @@ int sphp_amap_set_algorithm(sphp_amap* a, int alg) {
   if (alg == SPHP_ASSEMBLY_CLASS && !a->periodic)
     return fail(SPHP_ERR_UNSUPPORTED, "class-range assembly needs a periodic map");
   a->alg = alg;
-  return SPHP_OK;
+  return device_present() ? amap_device(a) : SPHP_OK;  // the owner path's entity table (periodic maps)
 }
 
 int sphp_amap_algorithm(const sphp_amap* a, int* alg) {
@@ -1304,14 +1428,19 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
     return fail(SPHP_ERR_BAD_ARG, "periodic analytic maps are hexahedral");
   if (int rc = amap_device(a)) return rc;
   cudaStream_t s = (cudaStream_t)stream;
+  Workspace* w = c->ws.get(s);
+  const size_t lb = sizeof(double) * c->E * c->t->nm;
+  int* ctr = nullptr;
+  if (a->periodic) {
+    CKW(w->ctr.ensure_on(2 * sizeof(int), s));
+    ctr = w->ctr.as<int>();
+  }
   if (c->strategy == SPHP_STRATEGY_CUDA_STDMAT) {
-    int rc = stdmat_prepare(c, s);
-    if (rc) return rc;
-    CK(c->loc_x.ensure(sizeof(double) * c->E * c->t->nm));
-    CK(c->loc_y.ensure(sizeof(double) * c->E * c->t->nm));
-    CK(amap_scatter(a->dev(), x, c->loc_x.as<double>(), s));
-    CK(elem_matvec(c->E, (int)c->t->nm, c->helm_H.as<double>(), c->loc_x.as<double>(), c->loc_y.as<double>(), s));
-    return amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s);
+    CKW(w->loc_x.ensure_on(lb, s));
+    CKW(w->loc_y.ensure_on(lb, s));
+    CK(amap_scatter(a->dev(), x, w->loc_x.as<double>(), s, ctr));
+    CK(elem_matvec(c->E, (int)c->t->nm, c->helm_H.as<double>(), w->loc_x.as<double>(), w->loc_y.as<double>(), s));
+    return amap_assemble_any(a, w->loc_y.as<double>(), y, accumulate, s, 0, ctr + 1);
   }
   OpArgs o = base_args(c);
   o.xg = x;
@@ -1320,10 +1449,10 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
     // the operator gathers x by entity-class ranges and writes a class-major
     // block (interiors straight into y), then one owner-computes sum over it
     // (two launches, the local block never exists)
-    CK(c->loc_y.ensure(sizeof(double) * class_block_doubles(a->n, a->P)));
+    CKW(w->loc_y.ensure_on(sizeof(double) * class_block_doubles(a->n, a->P), s));
     o.mode = AsmMode::PERIODIC_CLASS;
     o.n = a->n;
-    o.zbuf = c->loc_y.as<double>();
+    o.zbuf = w->loc_y.as<double>();
     o.direct_interior = accumulate ? 0 : 1;
     int ne = 0;
     o.ne_out = &ne;
@@ -1341,12 +1470,12 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
   if (a->alg == SPHP_ASSEMBLY_SPLIT || a->alg == SPHP_ASSEMBLY_CLASS) {
     // scatter -> fused local operator -> owner-computes sum (three launches;
     // the fused kernel then runs in its block-input form)
-    CK(c->loc_x.ensure(sizeof(double) * c->E * c->t->nm));
-    CK(c->loc_y.ensure(sizeof(double) * c->E * c->t->nm));
-    CK(amap_scatter(a->dev(), x, c->loc_x.as<double>(), s));
+    CKW(w->loc_x.ensure_on(lb, s));
+    CKW(w->loc_y.ensure_on(lb, s));
+    CK(amap_scatter(a->dev(), x, w->loc_x.as<double>(), s, ctr));
     phase_mark(s);
-    o.in = c->loc_x.as<double>();
-    o.out = c->loc_y.as<double>();
+    o.in = w->loc_x.as<double>();
+    o.out = w->loc_y.as<double>();
     o.mode = AsmMode::LOCAL;
     // the operator walks the elements backwards: it starts on the block the
     // scatter wrote last and ends on the elements the owner sum reads first,
@@ -1356,15 +1485,15 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
     if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no kernel for this key");
     if (e != cudaSuccess) return cuda_fail(e, "sphp_helmholtz_assembled");
     phase_mark(s);
-    const int rc = amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s, 0);
+    const int rc = amap_assemble_any(a, w->loc_y.as<double>(), y, accumulate, s, 0, ctr + 1);
     phase_mark(s);
     return rc;
   }
   if (a->alg == SPHP_ASSEMBLY_OWNER) {
     // gather -> fused elemental operator -> local block, then the
     // owner-computes sum (two launches, no colour passes)
-    CK(c->loc_y.ensure(sizeof(double) * c->E * c->t->nm));
-    o.out = c->loc_y.as<double>();
+    CKW(w->loc_y.ensure_on(lb, s));
+    o.out = w->loc_y.as<double>();
     if (a->periodic) {
       o.mode = AsmMode::PERIODIC_GATHER;
       o.n = a->n;
@@ -1376,7 +1505,7 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
     cudaError_t e = sumfac_launch(c, o, s);
     if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no assembled kernel for this key");
     if (e != cudaSuccess) return cuda_fail(e, "sphp_helmholtz_assembled");
-    return amap_assemble_any(a, c->loc_y.as<double>(), y, accumulate, s, /*mode_major=*/0);
+    return amap_assemble_any(a, w->loc_y.as<double>(), y, accumulate, s, /*mode_major=*/0, ctr + 1);
   }
   if (!accumulate) CK(cudaMemsetAsync(y, 0, sizeof(double) * a->num_global, s));
   for (int col = 0; col < a->ncolours; ++col) {
@@ -1452,26 +1581,29 @@ int assembled_host_pipelined(sphp_coll* c, const sphp_amap* a, const double* x, 
   }
   if (acc != a->num_global) return fail(SPHP_ERR_UNSUPPORTED, "unexpected periodic numbering");
   const size_t bytes = sizeof(double) * a->num_global;
-  CK(c->host_in.ensure(bytes));
-  CK(c->host_out.ensure(bytes));
-  CK(c->loc_x.ensure(sizeof(double) * c->E * nm));
-  CK(c->loc_y.ensure(sizeof(double) * c->E * nm));
-  if (!c->pipe_h2d) {
-    CK(cudaStreamCreateWithFlags(&c->pipe_h2d, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&c->pipe_d2h, cudaStreamNonBlocking));
+  Workspace* w = c->ws.get(s);
+  CKW(w->host_in.ensure_on(bytes, s));
+  CKW(w->host_out.ensure_on(bytes, s));
+  CKW(w->loc_x.ensure_on(sizeof(double) * c->E * nm, s));
+  CKW(w->loc_y.ensure_on(sizeof(double) * c->E * nm, s));
+  CKW(w->ctr.ensure_on(2 * sizeof(int), s));
+  if (!w->pipe_h2d) {
+    CK(cudaStreamCreateWithFlags(&w->pipe_h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&w->pipe_d2h, cudaStreamNonBlocking));
   }
-  while ((int)c->pipe_ev.size() < 2 * K + 2) {
+  while ((int)w->pipe_ev.size() < 2 * K + 2) {
     cudaEvent_t e;
     CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    c->pipe_ev.push_back(e);
+    w->pipe_ev.push_back(e);
   }
-  cudaEvent_t* ev_in = c->pipe_ev.data();
+  int* ctr = w->ctr.as<int>();
+  cudaEvent_t* ev_in = w->pipe_ev.data();
   cudaEvent_t* ev_out = ev_in + K;
   cudaEvent_t ev_start = ev_in[2 * K], ev_done = ev_in[2 * K + 1];
-  double* dx = c->host_in.as<double>();
-  double* dy = c->host_out.as<double>();
-  double* lx = c->loc_x.as<double>();
-  double* ly = c->loc_y.as<double>();
+  double* dx = w->host_in.as<double>();
+  double* dy = w->host_out.as<double>();
+  double* lx = w->loc_x.as<double>();
+  double* ly = w->loc_y.as<double>();
   // copy planes [z0, z1) of every region between host and device
   auto slab_copy = [&](double* dst, const double* src, int z0, int z1, cudaMemcpyKind kind,
                        cudaStream_t st) -> cudaError_t {
@@ -1491,11 +1623,11 @@ int assembled_host_pipelined(sphp_coll* c, const sphp_amap* a, const double* x, 
   };
   // copies start after everything already queued on the caller's stream
   CK(cudaEventRecord(ev_start, s));
-  CK(cudaStreamWaitEvent(c->pipe_h2d, ev_start, 0));
-  CK(cudaStreamWaitEvent(c->pipe_d2h, ev_start, 0));
+  CK(cudaStreamWaitEvent(w->pipe_h2d, ev_start, 0));
+  CK(cudaStreamWaitEvent(w->pipe_d2h, ev_start, 0));
   for (int k = 0; k < K; ++k) {
-    CK(slab_copy(dx, x, zb[k], zb[k + 1], cudaMemcpyHostToDevice, c->pipe_h2d));
-    CK(cudaEventRecord(ev_in[k], c->pipe_h2d));
+    CK(slab_copy(dx, x, zb[k], zb[k + 1], cudaMemcpyHostToDevice, w->pipe_h2d));
+    CK(cudaEventRecord(ev_in[k], w->pipe_h2d));
   }
   OpArgs o = base_args(c);
   o.mode = AsmMode::LOCAL;
@@ -1517,7 +1649,7 @@ int assembled_host_pipelined(sphp_coll* c, const sphp_amap* a, const double* x, 
     if (use_class)
       CK(class_owner_sum(n, P, ne, ly, dy, 0, 0, s, zb[k] * n, zb[k + 1] * n));
     else
-      CK(owner_periodic_v3(n, P, ly, dy, 0, s, zb[k] * n, zb[k + 1] * n));
+      CK(owner_periodic_v3(n, P, ly, dy, 0, s, zb[k] * n, zb[k + 1] * n, ctr + 1));
     CK(cudaEventRecord(ev_out[k], s));
     return SPHP_OK;
   };
@@ -1529,7 +1661,7 @@ int assembled_host_pipelined(sphp_coll* c, const sphp_amap* a, const double* x, 
     if (use_class) {
       o.e0 = e0;  // absolute element indexing; x, Z, y and geometry are whole-mesh
     } else {
-      CK(periodic_scatter_v2(n, P, dx, lx, s, zb[k] * n, zb[k + 1] * n));
+      CK(periodic_scatter_v2(n, P, dx, lx, s, zb[k] * n, zb[k + 1] * n, ctr));
       o.in = lx + e0 * nm;
       o.out = ly + e0 * nm;
       o.geom = c->geom + e0 * c->gstride;
@@ -1545,10 +1677,10 @@ int assembled_host_pipelined(sphp_coll* c, const sphp_amap* a, const double* x, 
   if (int rc = owner(0)) return rc;
   for (int i = 1; i <= K; ++i) {
     const int k = i % K;
-    CK(cudaStreamWaitEvent(c->pipe_d2h, ev_out[k], 0));
-    CK(slab_copy(y, dy, zb[k], zb[k + 1], cudaMemcpyDeviceToHost, c->pipe_d2h));
+    CK(cudaStreamWaitEvent(w->pipe_d2h, ev_out[k], 0));
+    CK(slab_copy(y, dy, zb[k], zb[k + 1], cudaMemcpyDeviceToHost, w->pipe_d2h));
   }
-  CK(cudaEventRecord(ev_done, c->pipe_d2h));
+  CK(cudaEventRecord(ev_done, w->pipe_d2h));
   CK(cudaStreamWaitEvent(s, ev_done, 0));
   CK(cudaStreamSynchronize(s));
   return SPHP_OK;
@@ -1592,16 +1724,38 @@ struct sphp_gsys {
   std::vector<const sphp_amap*> maps;
   std::vector<int64_t> off;  // batch slice offsets (doubles, 16-byte aligned)
   int64_t num_global = 0, total = 0;
-  DevBuf loc_x, loc_y, rowp, ent;
-  // one stream per batch: the batches' scatter + operator launches overlap
-  // (each batch alone leaves the GPU half idle in its ramp and tail)
-  std::vector<cudaStream_t> bs;
-  std::vector<cudaEvent_t> ev;  // [0] start, [1 + b] batch b done
-  ~sphp_gsys() {
-    for (auto q : bs) cudaStreamDestroy(q);
-    for (auto e : ev) cudaEventDestroy(e);
-  }
+  DevBuf rowp, ent;  // the owner-computes CSR (immutable after create)
+  // per caller stream: the concatenated local blocks, one stream per batch
+  // (the batches' scatter + operator launches overlap: each batch alone
+  // leaves the GPU half idle in its ramp and tail) and the events
+  // [0] start, [1 + b] batch b done
+  WorkspacePool ws;
 };
+
+// a gsys workspace for stream s: local blocks, batch streams, events
+static int gsys_workspace(sphp_gsys* g, cudaStream_t s, Workspace** out) {
+  Workspace* w = g->ws.get(s);
+  CKW(w->loc_x.ensure_on(sizeof(double) * (g->total + 2), s));
+  CKW(w->loc_y.ensure_on(sizeof(double) * (g->total + 2), s));
+  const size_t nb = g->colls.size();
+  if (w->bs.size() < nb || w->bev.size() < nb + 1) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (s) cudaStreamIsCapturing(s, &cap);
+    if (cap != cudaStreamCaptureStatusNone) return ws_fail(cudaErrorStreamCaptureUnsupported, "sphp_gsys_apply");
+  }
+  while (w->bs.size() < nb) {
+    cudaStream_t q;
+    CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
+    w->bs.push_back(q);
+  }
+  while (w->bev.size() < nb + 1) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    w->bev.push_back(e);
+  }
+  *out = w;
+  return SPHP_OK;
+}
 
 int sphp_gsys_create(sphp_coll* const* colls, const sphp_amap* const* maps, int nbatch, int64_t num_global,
                      sphp_gsys** out) {
@@ -1650,18 +1804,6 @@ int sphp_gsys_create(sphp_coll* const* colls, const sphp_amap* const* maps, int 
   CK(cudaMemcpy(g->rowp.p, rowp.data(), sizeof(int) * rowp.size(), cudaMemcpyHostToDevice));
   CK(g->ent.ensure(sizeof(int) * (ent.size() + 1)));
   if (!ent.empty()) CK(cudaMemcpy(g->ent.p, ent.data(), sizeof(int) * ent.size(), cudaMemcpyHostToDevice));
-  CK(g->loc_x.ensure(sizeof(double) * (acc + 2)));
-  CK(g->loc_y.ensure(sizeof(double) * (acc + 2)));
-  for (int b = 0; b <= nbatch; ++b) {
-    cudaEvent_t e;
-    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    g->ev.push_back(e);
-    if (b < nbatch) {
-      cudaStream_t q;
-      CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
-      g->bs.push_back(q);
-    }
-  }
   *out = g.release();
   return SPHP_OK;
 }
@@ -1669,17 +1811,18 @@ int sphp_gsys_create(sphp_coll* const* colls, const sphp_amap* const* maps, int 
 int sphp_gsys_apply(sphp_gsys* g, const double* x, double* y, sphp_stream stream) {
   if (!g || !x || !y) return fail(SPHP_ERR_BAD_ARG, "null argument");
   cudaStream_t s0 = (cudaStream_t)stream;
-  CK(cudaEventRecord(g->ev[0], s0));
+  Workspace* w = nullptr;
+  if (int rc = gsys_workspace(g, s0, &w)) return rc;
+  CK(cudaEventRecord(w->bev[0], s0));
   for (size_t b = 0; b < g->colls.size(); ++b) {
     sphp_coll* c = g->colls[b];
     const sphp_amap* a = g->maps[b];
-    double* lx = g->loc_x.as<double>() + g->off[b];
-    double* ly = g->loc_y.as<double>() + g->off[b];
-    cudaStream_t s = g->bs[b];
-    CK(cudaStreamWaitEvent(s, g->ev[0], 0));
+    double* lx = w->loc_x.as<double>() + g->off[b];
+    double* ly = w->loc_y.as<double>() + g->off[b];
+    cudaStream_t s = w->bs[b];
+    CK(cudaStreamWaitEvent(s, w->bev[0], 0));
     CK(amap_scatter(a->dev(), x, lx, s));
     if (c->strategy == SPHP_STRATEGY_CUDA_STDMAT) {
-      if (int rc = stdmat_prepare(c, s)) return rc;
       CK(elem_matvec(c->E, (int)c->t->nm, c->helm_H.as<double>(), lx, ly, s));
     } else {
       OpArgs o = base_args(c);
@@ -1690,11 +1833,17 @@ int sphp_gsys_apply(sphp_gsys* g, const double* x, double* y, sphp_stream stream
       if (e == cudaErrorNotSupported) return fail(SPHP_ERR_UNSUPPORTED, "no kernel for this key");
       if (e != cudaSuccess) return cuda_fail(e, "sphp_gsys_apply");
     }
-    CK(cudaEventRecord(g->ev[1 + b], s));
-    CK(cudaStreamWaitEvent(s0, g->ev[1 + b], 0));
+    CK(cudaEventRecord(w->bev[1 + b], s));
+    CK(cudaStreamWaitEvent(s0, w->bev[1 + b], 0));
   }
-  CK(owner_assemble_csr32(g->num_global, g->rowp.as<int>(), g->ent.as<int>(), g->loc_y.as<double>(), y, s0));
+  CK(owner_assemble_csr32(g->num_global, g->rowp.as<int>(), g->ent.as<int>(), w->loc_y.as<double>(), y, s0));
   return SPHP_OK;
+}
+
+int sphp_gsys_reserve(sphp_gsys* g, sphp_stream stream) {
+  if (!g) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  Workspace* w = nullptr;
+  return gsys_workspace(g, (cudaStream_t)stream, &w);
 }
 
 int sphp_gsys_destroy(sphp_gsys* g) {
@@ -1725,12 +1874,13 @@ int sphp_helmholtz_assembled_host(sphp_coll* c, const sphp_amap* a, const double
     }
   }
   const size_t b = sizeof(double) * a->num_global;
-  CK(c->host_in.ensure(b));
-  CK(c->host_out.ensure(b));
-  CK(cudaMemcpyAsync(c->host_in.p, x, b, cudaMemcpyHostToDevice, s));
-  int rc = sphp_helmholtz_assembled(c, a, c->host_in.as<double>(), c->host_out.as<double>(), 0, stream);
+  Workspace* w = c->ws.get(s);
+  CKW(w->host_in.ensure_on(b, s));
+  CKW(w->host_out.ensure_on(b, s));
+  CK(cudaMemcpyAsync(w->host_in.p, x, b, cudaMemcpyHostToDevice, s));
+  int rc = sphp_helmholtz_assembled(c, a, w->host_in.as<double>(), w->host_out.as<double>(), 0, stream);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(y, c->host_out.p, b, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(y, w->host_out.p, b, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return SPHP_OK;
 }
@@ -1783,6 +1933,22 @@ int sphp_cg_update(int64_t n, double alpha, const double* p, const double* ap, d
                    const double* dinv, double* z, double* ws, sphp_stream stream) {
   if (!p || !ap || !x || !r || !dinv || !z || !ws) return fail(SPHP_ERR_BAD_ARG, "null argument");
   CK(cg_update(n, alpha, p, ap, x, r, dinv, z, ws + 2, ws, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int64_t sphp_cg_state_size(int max_iter) { return cg_state_size(max_iter); }
+
+int sphp_cg_init_dev(int64_t n, const double* rhs, const double* dinv, double* x, double* r, double* z,
+                     double* p, double* st, int max_iter, double tol, sphp_stream stream) {
+  if (!rhs || !dinv || !x || !r || !z || !p || !st || max_iter < 0) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  CK(cg_init_dev(n, rhs, dinv, x, r, z, p, st, max_iter, tol, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+
+int sphp_cg_step_dev(int64_t n, const double* p, const double* ap, double* x, double* r, const double* dinv,
+                     double* z, double* st, int max_iter, sphp_stream stream) {
+  if (!p || !ap || !x || !r || !dinv || !z || !st) return fail(SPHP_ERR_BAD_ARG, "null argument");
+  CK(cg_step_dev(n, p, ap, x, r, dinv, z, const_cast<double*>(p), st, max_iter, (cudaStream_t)stream));
   return SPHP_OK;
 }
 

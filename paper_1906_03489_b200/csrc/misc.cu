@@ -302,9 +302,9 @@ __global__ void assemble_colour_kernel(AmapDev m, const double* __restrict__ loc
   if (gid >= 0) g[gid] += sg * loc[e * m.nm + nl];
 }
 
-cudaError_t amap_scatter(const AmapDev& m, const double* g, double* loc, cudaStream_t s) {
+cudaError_t amap_scatter(const AmapDev& m, const double* g, double* loc, cudaStream_t s, int* ctr) {
   if (m.periodic) {
-    cudaError_t e = periodic_scatter_v2(m.n, m.P, g, loc, s);
+    cudaError_t e = periodic_scatter_v2(m.n, m.P, g, loc, s, 0, -1, ctr);
     return e == cudaErrorNotSupported ? periodic_scatter(m.n, m.P, g, loc, s) : e;
   }
   const int64_t total = m.E * m.nm;
@@ -671,9 +671,9 @@ __global__ void owner_csr_kernel(int64_t ng, const int64_t* __restrict__ rowp,
 }
 
 cudaError_t owner_assemble_periodic(int n, int P, const double* loc, double* y, int accumulate,
-                                    int mode_major, cudaStream_t s) {
+                                    int mode_major, cudaStream_t s, int* ctr) {
   if (!mode_major) {
-    cudaError_t e = owner_periodic_v3(n, P, loc, y, accumulate, s);
+    cudaError_t e = owner_periodic_v3(n, P, loc, y, accumulate, s, 0, -1, ctr);
     if (e != cudaErrorNotSupported) return e;
   }
   if (n == 0) return cudaSuccess;

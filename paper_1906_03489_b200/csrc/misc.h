@@ -47,12 +47,14 @@ cudaError_t jacobian_factors(int64_t E, int64_t np, const double* dx, const doub
 int64_t class_block_doubles(int n, int P);
 cudaError_t class_owner_sum(int n, int P, int ne, const double* Z, double* y, int accumulate,
                             int with_interior, cudaStream_t s, int row0 = 0, int row1 = -1);
+// (ctr: one device int of the caller's per-stream workspace for the
+// dynamic segment schedule, or null for the static one)
 cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int accumulate,
-                              cudaStream_t s, int row0 = 0, int row1 = -1);
+                              cudaStream_t s, int row0 = 0, int row1 = -1, int* ctr = nullptr);
 cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cudaStream_t s,
-                                int row0 = 0, int row1 = -1);
+                                int row0 = 0, int row1 = -1, int* ctr = nullptr);
 cudaError_t periodic_entity_table(int n, int P, int* ent, cudaStream_t s);
-cudaError_t amap_scatter(const AmapDev& m, const double* g, double* loc, cudaStream_t s);
+cudaError_t amap_scatter(const AmapDev& m, const double* g, double* loc, cudaStream_t s, int* ctr = nullptr);
 cudaError_t owner_assemble_csr32(int64_t ng, const int* rowp, const int* ent, const double* loc, double* y,
                                  cudaStream_t s);
 cudaError_t amap_assemble(const AmapDev& m, const double* loc, double* g, int ncolours,
@@ -70,7 +72,7 @@ cudaError_t store_column(int64_t E, int nm, int n, const double* y, double* H, c
 cudaError_t symmetrise(int64_t E, int nm, double* H, cudaStream_t s);
 // loc is element-major (E, nm), or mode-major (nm, E) when mode_major != 0
 cudaError_t owner_assemble_periodic(int n, int P, const double* loc, double* y, int accumulate,
-                                    int mode_major, cudaStream_t s);
+                                    int mode_major, cudaStream_t s, int* ctr = nullptr);
 cudaError_t owner_assemble_csr(int64_t ng, const int64_t* rowp, const int* ent, const double* loc,
                                double* y, int accumulate, int nm, int64_t E, int mode_major,
                                cudaStream_t s);

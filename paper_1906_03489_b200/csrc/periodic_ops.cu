@@ -80,27 +80,14 @@ unsigned persistent_grid(K kernel, size_t smem, int64_t work) {
   return (unsigned)(work < g ? work : g);
 }
 
-// per-launch schedule counter (zeroed on the launch stream); a ring so that
-// launches in flight on different streams do not share one
-int* schedule_counter(cudaStream_t s) {
-  constexpr int kRing = 64, kMaxDev = 16;
-  static int* ring[kMaxDev] = {};
-  static std::atomic<unsigned> next{0};
+// segment schedule: the caller's counter (one int, owned by the stream's
+// workspace) is zeroed on the launch stream and handed out by atomics, or
+// the static round-robin schedule when it is null / SPHP_PERIODIC_DYNAMIC=0
+int* schedule_counter(int* ctr, cudaStream_t s) {
   static const int dynamic = env_int("SPHP_PERIODIC_DYNAMIC", 1);
-  if (!dynamic) return nullptr;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= kMaxDev) return nullptr;
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(s, &cap);
-  if (!ring[dev] && cap != cudaStreamCaptureStatusNone) return nullptr;  // no malloc in capture
-  if (!ring[dev] && cudaMalloc(&ring[dev], sizeof(int) * kRing) != cudaSuccess) {
-    ring[dev] = nullptr;
-    return nullptr;
-  }
-  int* c = ring[dev] + (next.fetch_add(1) % kRing);
-  if (cudaMemsetAsync(c, 0, sizeof(int), s) != cudaSuccess) return nullptr;
-  return c;
+  if (!dynamic || !ctr) return nullptr;
+  if (cudaMemsetAsync(ctr, 0, sizeof(int), s) != cudaSuccess) return nullptr;
+  return ctr;
 }
 
 template <typename K>
@@ -260,7 +247,7 @@ cudaError_t with_unroll(int slots, F&& f) {
 }
 
 cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cudaStream_t s, int row0,
-                                int row1) {
+                                int row1, int* ctr) {
   const int L = segment_length(n, P, false);
   if (L == 0 || P < 2) return cudaErrorNotSupported;
   if (reinterpret_cast<uintptr_t>(loc) & 15) return cudaErrorNotSupported;
@@ -277,7 +264,7 @@ cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cuda
     if (row1 <= row0) return cudaSuccess;
     const unsigned blocks =
         persistent_grid(periodic_scatter_v2_kernel<U>, smem, (int64_t)(row1 - row0) * segs);
-    periodic_scatter_v2_kernel<U><<<blocks, kThreads, smem, s>>>(n, P, L, x, loc, schedule_counter(s),
+    periodic_scatter_v2_kernel<U><<<blocks, kThreads, smem, s>>>(n, P, L, x, loc, schedule_counter(ctr, s),
                                                                  row0 * segs, row1 * segs);
     return cudaGetLastError();
   });
@@ -456,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, U <= 8 ? 4 : 3) owner_periodic_v3_ke
 }
 
 cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int accumulate,
-                              cudaStream_t s, int row0, int row1) {
+                              cudaStream_t s, int row0, int row1, int* ctr) {
   const int L = segment_length(n, P, true);
   if (L == 0 || P < 2) return cudaErrorNotSupported;
   if (n == 0) return cudaSuccess;
@@ -474,7 +461,7 @@ cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int ac
     const unsigned blocks =
         persistent_grid(owner_periodic_v3_kernel<U>, smem, (int64_t)(row1 - row0) * segs);
     owner_periodic_v3_kernel<U><<<blocks, kThreads, smem, s>>>(n, P, L, loc, y, accumulate,
-                                                                 schedule_counter(s), row0 * segs,
+                                                                 schedule_counter(ctr, s), row0 * segs,
                                                                  row1 * segs);
     return cudaGetLastError();
   });

@@ -228,6 +228,113 @@ cudaError_t cg_direction(int64_t n, double beta, const double* z, double* p, cud
   cg_direction_kernel<<<RB, RT, 0, s>>>(n, beta, z, p);
   return cudaGetLastError();
 }
+// ---------------------------------------------------------------------------
+// Device-scalar CG (no host round trip per iteration, capturable in a CUDA
+// graph): the scalars live in a device state vector
+//   st[0] rz   st[1] rr   st[2] p.Ap   st[3] (unused)   st[4] beta
+//   st[5] rhs norm   st[6] tol   st[7] done (0/1)   st[8] iterations
+//   st[9 ..] residual history (max_iter entries), then 2 RB partials
+// The arithmetic is the host loop's (alpha = rz / pAp, beta = rz' / rz,
+// res = sqrt(max(rr, 0)) / |rhs|, stop at res <= tol), so a solve is
+// bitwise the host-scalar one; after convergence the updates are no-ops.
+// ---------------------------------------------------------------------------
+constexpr int ST_HIST = 9;
+
+__global__ void cg_init_finish_kernel(const double* partial, double* st, double tol) {
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < RB; ++k) {
+      a += partial[2 * k];
+      b += partial[2 * k + 1];
+    }
+    st[0] = a;
+    st[1] = b;
+    st[5] = sqrt(b);
+    st[6] = tol;
+    st[7] = st[5] == 0.0 ? 1.0 : 0.0;
+    st[8] = 0.0;
+  }
+}
+
+__global__ void cg_pap_finish_kernel(const double* partial, double* st) {
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int k = 0; k < RB; ++k) a += partial[2 * k];
+    st[2] = a;
+  }
+}
+
+__global__ void __launch_bounds__(RT) cg_update_dev_kernel(int64_t n, const double* st,
+                                                           const double* __restrict__ p,
+                                                           const double* __restrict__ ap,
+                                                           double* __restrict__ x, double* __restrict__ r,
+                                                           const double* __restrict__ dinv,
+                                                           double* __restrict__ z, double* partial) {
+  if (st[7] != 0.0) return;  // converged: x, r, z stay
+  const double alpha = st[0] / st[2];
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x; i < n; i += (int64_t)RB * RT) {
+    const double xi = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, ap[i], r[i]);
+    const double zi = dinv[i] * ri;
+    x[i] = xi;
+    r[i] = ri;
+    z[i] = zi;
+    s0 = fma(ri, zi, s0);
+    s1 = fma(ri, ri, s1);
+  }
+  block_sum2(s0, s1, partial);
+}
+
+__global__ void cg_update_finish_kernel(const double* partial, double* st, int max_iter) {
+  if (threadIdx.x == 0) {
+    if (st[7] != 0.0) return;
+    double a = 0.0, b = 0.0;
+    for (int k = 0; k < RB; ++k) {
+      a += partial[2 * k];
+      b += partial[2 * k + 1];
+    }
+    const int it = (int)st[8];
+    const double res = sqrt(b > 0.0 ? b : 0.0) / st[5];
+    if (it < max_iter) st[ST_HIST + it] = res;
+    st[8] = it + 1;
+    st[4] = a / st[0];  // beta
+    st[0] = a;
+    st[1] = b;
+    if (res <= st[6]) st[7] = 1.0;
+  }
+}
+
+__global__ void cg_direction_dev_kernel(int64_t n, const double* st, const double* __restrict__ z,
+                                        double* __restrict__ p) {
+  if (st[7] != 0.0) return;
+  const double beta = st[4];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+
+int cg_state_size(int max_iter) { return ST_HIST + max_iter + 2 * RB; }
+
+cudaError_t cg_init_dev(int64_t n, const double* rhs, const double* dinv, double* x, double* r, double* z,
+                        double* p, double* st, int max_iter, double tol, cudaStream_t s) {
+  double* partial = st + ST_HIST + max_iter;
+  cg_init_kernel<<<RB, RT, 0, s>>>(n, rhs, dinv, x, r, z, p, partial);
+  cg_init_finish_kernel<<<1, 32, 0, s>>>(partial, st, tol);
+  return cudaGetLastError();
+}
+
+cudaError_t cg_step_dev(int64_t n, const double* p, const double* ap, double* x, double* r, const double* dinv,
+                        double* z, double* pp, double* st, int max_iter, cudaStream_t s) {
+  double* partial = st + ST_HIST + max_iter;
+  dot2_kernel<<<RB, RT, 0, s>>>(n, p, ap, nullptr, nullptr, partial);
+  cg_pap_finish_kernel<<<1, 32, 0, s>>>(partial, st);
+  cg_update_dev_kernel<<<RB, RT, 0, s>>>(n, st, p, ap, x, r, dinv, z, partial);
+  cg_update_finish_kernel<<<1, 32, 0, s>>>(partial, st, max_iter);
+  cg_direction_dev_kernel<<<RB, RT, 0, s>>>(n, st, z, pp);
+  return cudaGetLastError();
+}
+
 int reduction_partials() { return 2 * RB; }
 
 }  // namespace sphp

@@ -69,6 +69,7 @@ class HelmholtzSolver:
         self.nd = int(num_dirichlet)
         self.diag = assembled_diagonal(self.batches, self.num_global)
         self._buf = torch.empty(self.num_global, dtype=torch.float64, device=self.diag.device)
+        self._graph_stream = None
 
     def _apply_free(self, v, out):
         # A restricted to the free block: Dirichlet entries of the input and
@@ -77,9 +78,11 @@ class HelmholtzSolver:
         out[: self.nd] = 0.0
         return out
 
-    def solve(self, rhs, u_dirichlet=None, tol=1e-12, max_iter=3000):
+    def solve(self, rhs, u_dirichlet=None, tol=1e-12, max_iter=3000, graph=False, check_every=8):
         """rhs: assembled load vector (num_global); u_dirichlet: lifted
-        boundary values (num_global, Dirichlet block used) or None (zero)."""
+        boundary values (num_global, Dirichlet block used) or None (zero).
+        graph=True replays chunks of `check_every` CG iterations from one
+        CUDA graph (no host work per iteration)."""
         b = rhs.clone()
         if u_dirichlet is not None and self.nd:
             ud = torch.zeros_like(b)
@@ -91,39 +94,69 @@ class HelmholtzSolver:
         # zero preconditioner on pinned dofs keeps CG in the free subspace
         dinv = torch.where(diag == 0, torch.zeros_like(diag), 1.0 / torch.where(diag == 0,
                                                                              torch.ones_like(diag), diag))
-        x = _solve_with_dinv(self._apply_free, b, dinv, tol, max_iter)
+        cs = None
+        if graph:
+            if self._graph_stream is None:
+                self._graph_stream = torch.cuda.Stream(device=b.device)
+                self.op.reserve(stream=self._graph_stream)
+            cs = self._graph_stream
+        x = _solve_with_dinv(self._apply_free, b, dinv, tol, max_iter, check_every=check_every, graph=cs)
         if u_dirichlet is not None and self.nd:
             x[: self.nd] = u_dirichlet[: self.nd]
         return x
 
 
-def _solve_with_dinv(apply, rhs, dinv, tol, max_iter):
-    """solve_pcg with an explicit inverse diagonal (zeros allowed)."""
+def _solve_with_dinv(apply, rhs, dinv, tol, max_iter, check_every=8, graph=None):
+    """solve_pcg with an explicit inverse diagonal (zeros allowed).
+
+    The CG scalars stay on the device (sphp_cg_init_dev / sphp_cg_step_dev:
+    alpha = rz / pAp, beta = rz' / rz and the residual test run in the
+    update kernels), so the host only looks at the state every
+    `check_every` iterations; steps after convergence are no-ops, so x is
+    bitwise the per-iteration loop's.  `graph`: a (CUDAGraph, stream)
+    factory key — when given, one chunk of `check_every` iterations is
+    captured once and replayed (the operator must be reserved on that
+    stream, GlobalHelmholtz.reserve)."""
     n = rhs.numel()
     dev = rhs.device
     x, r, z, p, ap = (torch.empty_like(rhs) for _ in range(5))
-    ws = _ws(dev)
-    s = _lib.stream_ptr()
-    _lib.check(_lib.lib.sphp_cg_init(n, _lib.ptr(rhs), _lib.ptr(dinv), _lib.ptr(x), _lib.ptr(r),
-                                     _lib.ptr(z), _lib.ptr(p), _lib.ptr(ws), s))
-    rz, rr = ws[:2].tolist()
-    rhs_norm = float(np.sqrt(rr))
-    if rhs_norm == 0.0:
-        return x
-    residuals = [1.0]
-    for _ in range(max_iter):
+    st = torch.zeros(int(_lib.lib.sphp_cg_state_size(max_iter)), dtype=torch.float64, device=dev)
+
+    def step(stream=None):
         apply(p, ap)
-        _lib.check(_lib.lib.sphp_vec_dot2(n, _lib.ptr(p), _lib.ptr(ap), None, None, _lib.ptr(ws), s))
-        alpha = rz / ws[0].item()
-        _lib.check(_lib.lib.sphp_cg_update(n, alpha, _lib.ptr(p), _lib.ptr(ap), _lib.ptr(x),
-                                           _lib.ptr(r), _lib.ptr(dinv), _lib.ptr(z), _lib.ptr(ws), s))
-        rz_new, rr = ws[:2].tolist()
-        res = float(np.sqrt(max(rr, 0.0))) / rhs_norm
-        residuals.append(res)
-        if res <= tol:
+        _lib.check(_lib.lib.sphp_cg_step_dev(n, _lib.ptr(p), _lib.ptr(ap), _lib.ptr(x), _lib.ptr(r),
+                                             _lib.ptr(dinv), _lib.ptr(z), _lib.ptr(st), max_iter,
+                                             _lib.stream_ptr(stream)))
+
+    _lib.check(_lib.lib.sphp_cg_init_dev(n, _lib.ptr(rhs), _lib.ptr(dinv), _lib.ptr(x), _lib.ptr(r),
+                                         _lib.ptr(z), _lib.ptr(p), _lib.ptr(st), max_iter, float(tol),
+                                         _lib.stream_ptr()))
+    if float(st[5].item()) == 0.0:
+        return x
+    chunk = None
+    if graph is not None and max_iter >= check_every:
+        cs = graph
+        cs.wait_stream(torch.cuda.current_stream(dev))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cs):
+            for _ in range(check_every):
+                step(cs)
+        torch.cuda.current_stream(dev).wait_stream(cs)
+        chunk = g
+    done_iters = 0
+    while done_iters < max_iter:
+        k = min(check_every, max_iter - done_iters)
+        if chunk is not None and k == check_every:
+            chunk.replay()
+        else:
+            for _ in range(k):
+                step()
+        done_iters += k
+        done, iters = st[7:9].tolist()
+        if done:
             return x
-        _lib.check(_lib.lib.sphp_cg_direction(n, rz_new / rz, _lib.ptr(z), _lib.ptr(p), s))
-        rz = rz_new
+    iters = int(st[8].item())
+    residuals = [1.0] + st[9:9 + iters].tolist()
     raise ConvergenceError(f"PCG did not reach {tol} in {max_iter} iterations "
                            f"(final residual {residuals[-1]:.3e})", residuals)
 

@@ -99,3 +99,71 @@ def test_pcg_raises_convergence_error(sp):
     with pytest.raises(sp.ConvergenceError) as ei:
         sp.solve_pcg(apply, rhs, tol=1e-14, max_iter=3, diag=diag)
     assert len(ei.value.residuals) == 4
+
+
+GD = np.load(Path(__file__).resolve().parent / "golden" / "reference_dirichlet.npz")
+
+
+@pytest.mark.parametrize("graph", [False, True])
+@pytest.mark.parametrize("tag", ["all", "sw"])
+@pytest.mark.parametrize("P", range(2, 7))
+def test_nonzero_dirichlet_lifting_matches_reference(sp, P, tag, graph):
+    """The lifting branch of helmholtz_solve (assembly.py:316-354) with
+    non-zero boundary data: b_free = b - A u_d, CG on the free block, the
+    Dirichlet block set to u_d.  Inputs are the reference's own load vector
+    and lifted boundary values (tests/golden/make_golden_dirichlet.py); the
+    device solve (host-checked every 8 iterations, or replayed from one CUDA
+    graph) reproduces the reference's global solution."""
+    pre = f"{tag}/P{P}/"
+    sides = ("south", "east", "north", "west") if tag == "all" else ("south", "west")
+    ng, nd, maps, _ = sp.quad_structured_maps(4, 4, P, sides)
+    assert nd == int(GD[pre + "nd"]) and ng == GD[pre + "x"].size
+    ids, amap = maps[P]
+    exp = sp.make_quad(P)
+    helm = sp.Collection(sp.ElementBatch.structured(exp, 4, kind=sp.GEOM_METRIC), sp.OperatorKind.HELMHOLTZ,
+                         sp.Strategy.CUDA_SUMFAC, lam=1.0)
+    solver = sp.HelmholtzSolver([(helm, amap)], ng, nd)
+    b = torch.as_tensor(GD[pre + "b"], device="cuda")
+    ud = torch.as_tensor(GD[pre + "u_d"], device="cuda")
+    x = solver.solve(b, u_dirichlet=ud, tol=1e-13, max_iter=6000, graph=graph).cpu().numpy()
+    ref = GD[pre + "x"]
+    assert np.array_equal(x[:nd], ref[:nd])
+    assert np.linalg.norm(x - ref) <= 1e-10 * np.linalg.norm(ref), (P, tag)
+
+
+def test_device_scalar_cg_matches_host_scalar_loop(sp):
+    """The device-scalar CG (alpha, beta, residual test in the kernels) is
+    bitwise the per-iteration host loop it replaces."""
+    n = 200
+    rng = np.random.default_rng(0)
+    d = torch.as_tensor(rng.uniform(1, 10, n), device="cuda")
+    rhs = torch.as_tensor(rng.standard_normal(n), device="cuda")
+
+    def apply(p, out):
+        out.copy_(d * p)
+        out[1:] += 0.3 * p[:-1]
+        out[:-1] += 0.3 * p[1:]
+        return out
+
+    x = sp.solve_pcg(apply, rhs, tol=1e-13, max_iter=500, diag=d)
+    # host loop, same kernels' arithmetic (assembly.py:218-266)
+    xh = torch.zeros_like(rhs)
+    dinv = 1.0 / d
+    r = rhs.clone()
+    z = dinv * r
+    p = z.clone()
+    rz = float((r * z).sum())
+    rn = float(torch.sqrt((r * r).sum()))
+    ap = torch.empty_like(p)
+    for _ in range(500):
+        apply(p, ap)
+        alpha = rz / float((p * ap).sum())
+        xh += alpha * p
+        r -= alpha * ap
+        z = dinv * r
+        rz_new = float((r * z).sum())
+        if float(torch.sqrt((r * r).sum())) / rn <= 1e-13:
+            break
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    assert torch.allclose(x, xh, rtol=0, atol=1e-12 * float(xh.abs().max()))
