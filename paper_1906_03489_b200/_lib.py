@@ -161,6 +161,16 @@ def stream_ptr(stream=None):
     return C.c_void_p(s.cuda_stream)
 
 
+def raw_stream(stream, device_index):
+    """cudaStream_t as an int: the given torch stream's, or the current
+    stream of `device_index` (the per-call fast path: no Stream object)."""
+    if stream is not None:
+        return stream.cuda_stream
+    import torch
+
+    return torch._C._cuda_getCurrentRawStream(device_index)
+
+
 def abi_version():
     return lib.sphp_abi_version()
 

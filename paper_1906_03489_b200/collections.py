@@ -103,6 +103,9 @@ def _normalise(elements):
     return ref, (None if geoms[0] is None else geoms)
 
 
+_APPLY = _lib.lib.sphp_apply
+
+
 def _is_cuda_tensor(x):
     return torch.is_tensor(x) and x.is_cuda
 
@@ -165,6 +168,9 @@ class Collection:
         _lib.check(_lib.lib.sphp_collection_info(self._handle, C.byref(ins), C.byref(outs),
                                                  C.byref(macs), C.byref(hbm)))
         self._in, self._out, self._macs, self._hbm = ins.value, outs.value, macs.value, hbm.value
+        self._h = self._handle.value
+        self._in_shape = torch.Size((self.num_elements, self._in))
+        self._out_numel = self.num_elements * self._out
 
     def __del__(self):
         h = getattr(self, "_handle", None)
@@ -204,6 +210,20 @@ class Collection:
 
     def apply(self, block, out=None, stream=None):
         """Evaluate the operator over the packed block."""
+        # fast path (device float64 contiguous blocks of the exact shape, the
+        # repeated-apply case): one ctypes call, raw ints, no Stream object
+        if type(block) is torch.Tensor and block.is_cuda and block.dtype is torch.float64 \
+                and block.shape == self._in_shape and block.is_contiguous():
+            if out is None:
+                out = torch.empty(self.output_shape, dtype=torch.float64, device=block.device)
+            elif not (type(out) is torch.Tensor and out.is_cuda and out.dtype is torch.float64
+                      and out.is_contiguous() and out.numel() == self._out_numel):
+                raise CollectionError("out must be a contiguous float64 CUDA tensor of output_shape")
+            rc = _APPLY(self._h, self.num_elements, self._in, block.data_ptr(), out.data_ptr(),
+                        _lib.raw_stream(stream, block.device.index))
+            if rc:
+                _lib.check(rc, CollectionError)
+            return out
         if _is_cuda_tensor(block):
             if block.dtype != torch.float64:
                 block = block.to(torch.float64)
