@@ -251,30 +251,138 @@ def parity_sample(P, n, x, y, c, yl, seed=SEED):
 
 
 # ---------------------------------------------------------------------------
+class FullMeshPort:
+    """The reference algorithm (GlobalSystem.apply: scatter -> elemental
+    Helmholtz -> assemble, assembly.py:177-182, with collections.py's
+    sum-factorised elemental operator restated for hex by oracle/) on the
+    FULL n^3 mesh, chunked over elements (geometry of all chunks prepared
+    once: 3.2 GB at P = 4, n = 64).  One apply = every chunk's gather,
+    operator and np.add.at assembly."""
+
+    def __init__(self, P, n, chunk=8192, seed=SEED):
+        from oracle import assembly as oa
+        from oracle import geometry as og
+        from oracle import ops as oo
+
+        self.oo = oo
+        self.oe = oo.Expansion("hex", P, P + 2)
+        E = n ** 3
+        _, _, codes = oa.hex_periodic_codes(n, P)
+        self.codes = codes.reshape(E, -1)
+        self.ng = (n * P) ** 3
+        self.x = np.random.default_rng(seed).uniform(-1, 1, self.ng)
+        self.chunks = []
+        for c0 in range(0, E, chunk):
+            ids = np.arange(c0, min(E, c0 + chunk))
+            _, _, inv, wj = og.factors(self.oe, n, ids, og.MAP_HEX_SINE, AMP)
+            self.chunks.append((ids, oo.metric_from_inv(wj, inv), wj))
+        self.local_dofs = E * (P + 1) ** 3
+
+    def apply(self):
+        y = np.zeros(self.ng)
+        for ids, G, wj in self.chunks:
+            cod = self.codes[ids]
+            yl = self.oo.helmholtz(self.oe, self.x[cod], 1.0, G, wj)
+            np.add.at(y, cod.ravel(), yl.ravel())
+        return y
+
+
+def reference_2d(seconds_budget=150.0):
+    """The reference ITSELF (baseline/_ref, installed from /root/reference;
+    pure Python/numpy) on the 2D BASELINE configs, in its own protocol:
+    autotune (collections.py:285-313: median of trials over every strategy)
+    per operator on cfg1 (32x32 affine quads, P=4, Q=6 GLL) and the
+    assembled matrix-free GlobalSystem.apply (assembly.py:177-182) of the
+    Helmholtz operator on 256x256 quads, P=6, Q=8 (cfg2's size; the
+    reference's geometry cannot express cfg2's curved map, so the mesh is
+    affine).  None when baseline/_ref is absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "spechp").is_dir():
+        return None
+    sys.path.insert(0, str(ref))
+    from spechp.assembly import build_assembly_map, build_global_system
+    from spechp.collections import OperatorKind, autotune
+    from spechp.meshio import structured_quad_mesh
+    from spechp.region import build_elements
+
+    out = {"source": "baseline/_ref (pip install --no-index --no-deps of /root/reference/pkg)"}
+    t_start = time.perf_counter()
+    mesh = structured_quad_mesh(32, 32)
+    els = build_elements(mesh, orders=4, num_points=6)
+    cfg1 = {}
+    for op in (OperatorKind.BWD_TRANS, OperatorKind.IPRODUCT_WRT_BASE, OperatorKind.PHYS_DERIV):
+        pick, rep = autotune(els, op, trials=5, warmups=2)
+        cfg1[op.value] = {"pick": pick.value,
+                          "median_s": {k: v.get("median_s") for k, v in rep.items() if isinstance(v, dict)}}
+    out["cfg1_autotune"] = cfg1
+    if time.perf_counter() - t_start < seconds_budget:
+        t0 = time.perf_counter()
+        mesh = structured_quad_mesh(256, 256)
+        els = build_elements(mesh, orders=6, num_points=8)
+        amap = build_assembly_map(mesh, els, ())
+        system = build_global_system(els, amap, "helmholtz", 1.0)
+        setup = time.perf_counter() - t0
+        x = np.random.default_rng(SEED).uniform(-1, 1, amap.num_global)
+        system.apply(x)
+        times = []
+        for _ in range(3):
+            t1 = time.perf_counter()
+            system.apply(x)
+            times.append(time.perf_counter() - t1)
+        t = statistics.median(times)
+        out["cfg2_global_apply"] = {"s": t, "global_dofs": int(amap.num_global),
+                                    "local_dofs": int(len(els) * 49),
+                                    "global_dof_s": amap.num_global / t, "local_dof_s": len(els) * 49 / t,
+                                    "matrix_free": system.matrix is None, "setup_s": setup,
+                                    "mesh": "256x256 affine quads P=6 Q=8 (cfg2 size, affine map)"}
+    return out
+
+
 def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm on the host cores (tier
+    rules: the CPU restatement in oracle/, BLAS threads = all cores), on the
+    FULL 64^3 cfg4 mesh (chunked), one assembled apply per step; plus the
+    reference itself (baseline/_ref) on the 2D configs."""
     if rank != 0:
         return
-    n_s = 12 if args.P <= 4 else 8
-    times = []
-    # each step = one bounded sample (assembled apply on an n_s^3 sub-mesh)
-    from oracle import assembly as oa  # noqa: F401
-    for i in range(args.warmup + args.steps):
-        v, runs, el, cores, E = cpu_port_assembled(args.P, n_s, 0.0)
-        if i >= args.warmup:
-            times.append(el / runs)
-    t = statistics.median(times)
-    value = n_s ** 3 * (args.P + 1) ** 3 / t
-    sample = f"assembled apply on a {n_s}^3 periodic sub-mesh (same map, P={args.P}), one per step"
+    from threadpoolctl import threadpool_limits
+
+    cores = os.cpu_count() or 1
+    with threadpool_limits(limits=cores):
+        port = FullMeshPort(args.P, args.n)
+        t0 = time.perf_counter()
+        port.apply()  # first (untimed) apply also sizes the step budget
+        first = time.perf_counter() - t0
+        warm = max(0, args.warmup - 1)
+        # each step is one full apply; keep the whole run within ~3 minutes
+        steps = max(3, min(args.steps, int(150.0 / max(first, 1e-3)) - warm))
+        for _ in range(warm):
+            port.apply()
+        times = []
+        for _ in range(steps):
+            t1 = time.perf_counter()
+            port.apply()
+            times.append(time.perf_counter() - t1)
+        t = statistics.median(times)
+        value = port.local_dofs / t
+        r2d = None
+        try:
+            r2d = reference_2d()
+        except Exception as exc:  # the 2D extra must not sink the line
+            r2d = {"error": repr(exc)}
+    sample = (f"full {args.n}^3 mesh, one assembled apply per step (median of {steps}), "
+              f"chunks of 8192 elements, numpy + BLAS threads = {cores}")
     line = {
         "metric": metric_name(args.P, args.n), "value": value, "unit": "DoF/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded, SPECHP_SEED)",
-        "config": {"workload": f"cfg4 hex Helmholtz P={args.P} n={args.n} (sampled {n_s}^3)",
+        "config": {"workload": f"cfg4 hex Helmholtz P={args.P} n={args.n} (full mesh)",
                    "P": args.P, "Q": args.P + 2, "n": args.n, "lambda": 1.0},
         "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_2d": r2d,
     }
     print(json.dumps(line), flush=True)
 
@@ -425,11 +533,16 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        from threadpoolctl import threadpool_limits
+
         n_s = 12 if P <= 4 else 8
-        v, runs, el, cores, Es = cpu_port_assembled(P, n_s, args.cpu_seconds)
+        with threadpool_limits(limits=os.cpu_count() or 1):
+            v, runs, el, cores, Es = cpu_port_assembled(P, n_s, args.cpu_seconds)
         cpu = {"value": v, "unit": "DoF/s", "cores": cores, "kind": "port",
                "sample": f"{runs} assembled applies on a {n_s}^3 periodic sub-mesh ({Es} elements, "
-                         f"same map, P={P}) in {el:.1f} s, numpy with BLAS threads = all cores"}
+                         f"same map, P={P}) in {el:.1f} s, numpy + BLAS threads = {cores} (threadpoolctl); "
+                         f"the rate is quoted per local DoF, i.e. extrapolated to the {n}^3 mesh — "
+                         "bench.py --impl reference times the full mesh (chunked)"}
 
     if rank != 0:
         return
