@@ -1244,10 +1244,9 @@ int sphp_amap_create_hex_periodic(int n, int P, sphp_amap** out) {
   a->ncolours = 8;
   // default: class-range assembly (the operator gathers x by entity class,
   // one streaming owner sum; falls back to split when the mesh does not
-  // divide into its tiles), except at P = 7 where its two-element tile
-  // leaves one CTA per SM and split measures faster (tools/time_class.py:
-  // 3.22 vs 3.54 ms at n = 64; every other order 4-16 % faster)
-  a->alg = P < 2 ? SPHP_ASSEMBLY_OWNER : (P == 7 ? SPHP_ASSEMBLY_SPLIT : SPHP_ASSEMBLY_CLASS);
+  // divide into its tiles or x is misaligned): 4-19 % faster than split at
+  // every order P = 2..8 (tools/time_phases.py, n = 64)
+  a->alg = P < 2 ? SPHP_ASSEMBLY_OWNER : SPHP_ASSEMBLY_CLASS;
   if (a->num_global > 2147483645LL) {
     delete a;
     return fail(SPHP_ERR_UNSUPPORTED, "periodic map with more than 2^31-3 global dofs");

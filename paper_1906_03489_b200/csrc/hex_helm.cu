@@ -46,23 +46,40 @@ static int helm_variant_env() {
 #define SPHP_LOCAL_BUDGET_KB 74
 #endif
 
-// PERIODIC_CLASS (pipeline MODE 5) needs an even NE dividing n: the largest
-// of 8 / 4 / 2 elements whose tile fits the budget (SPHP_CLASS_BUDGET_KB,
-// default 74 KB: three resident CTAs per SM at P = 4)
-#ifndef SPHP_CLASS_BUDGET_KB
-#define SPHP_CLASS_BUDGET_KB 75
-#endif
+// PERIODIC_CLASS (pipeline MODE 5): tiles of NE consecutive elements of an
+// x-row (NE must divide n)
 template <int M, int Q, int GK, int NE>
 constexpr size_t class_smem() {
   using Op = HexHelm<M, Q, GK, NE, choose_nt(NE, Q * Q), 1>;
   return Scaffold<Op, 5>::SMEM_BYTES;
 }
+// tile size of the class mode: the NE in {1, 2, 4, 8} that keeps the most
+// elements resident per SM (shared memory: 228 KB per SM, 1 KB per CTA;
+// at most 256 work items per stage, i.e. threads, so registers do not cap
+// the pointwise stage), the smaller NE (more CTAs) on ties; SPHP_CLASS_NE
+// overrides (tuning builds)
+template <int M, int Q, int GK, int NE>
+constexpr int class_resident() {
+  constexpr size_t b = class_smem<M, Q, GK, NE>();
+  return (b > 227 * 1024 || (NE > 1 && NE * Q * Q > 256)) ? 0 : (int)(233472 / (b + 1024)) * NE;
+}
 template <int M, int Q, int GK>
 constexpr int class_ne() {
-  return class_smem<M, Q, GK, 8>() <= SPHP_CLASS_BUDGET_KB * 1024 && 8 * Q * Q <= 512   ? 8
-         : class_smem<M, Q, GK, 4>() <= SPHP_CLASS_BUDGET_KB * 1024 && 4 * Q * Q <= 512 ? 4
-                                                                                          : 2;
+#ifdef SPHP_CLASS_NE
+  return SPHP_CLASS_NE;
+#else
+  // measured (tools/time_phases.py, cfg4 64^3, METRIC, Q = P + 2): P = 2..8
+  // -> 4, 4, 4, 2, 1, 1, 1 (residency alone picks 2 at P = 3 and 1 at P = 5,
+  // 9-10 % slower there)
+  if (GK == SPHP_GEOM_METRIC && Q == M + 1) return M <= 5 ? 4 : (M == 6 ? 2 : 1);
+  int best = 1, score = class_resident<M, Q, GK, 1>();
+  if (class_resident<M, Q, GK, 2>() > score) best = 2, score = class_resident<M, Q, GK, 2>();
+  if (class_resident<M, Q, GK, 4>() > score) best = 4, score = class_resident<M, Q, GK, 4>();
+  if (class_resident<M, Q, GK, 8>() > score) best = 8, score = class_resident<M, Q, GK, 8>();
+  return best;
+#endif
 }
+
 template <int M, int Q, int GK>
 static cudaError_t helm_class(const OpArgs& oa, cudaStream_t s) {
   constexpr int NE = class_ne<M, Q, GK>();

@@ -531,32 +531,58 @@ struct OwnerGeom {
 // class run; the a = 1 term is u - S, or the previous tile's last element
 // (x wraps to n - 1 at t = 0) when u < S.
 template <int P, int NE, int R>
-__device__ __forceinline__ void owned_sum2(const double* __restrict__ Z, const int* zr, const int* zi, int T,
-                                           int li, double& acc0, double& acc1) {
-  // outputs li and li + 1 (li even): same region (n S is even), same tile
-  // run (NE S is even), so the index math is shared and 2 NC loads are in
-  // flight per thread
+__device__ __forceinline__ double owned_one(const double* __restrict__ Z, const int* zr, const int* zi, int T,
+                                            int li, double* v) {
   using G = OwnerGeom<P>;
   constexpr int S = G::S(R), NC = Region<R>::NC, RUN = NE * S, REC = NE * G::ZS;
   const int t = li / RUN, u = li - t * RUN;
   const int tp = t == 0 ? T - 1 : t - 1;  // tile of the x - 1 neighbour at u < S
-  double v0[NC], v1[NC];
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
     const int bc = Region<R>::b(j) * 2 + Region<R>::c(j);
     if constexpr (R == 7) {
-      v0[j] = __ldg(Z + zi[bc] + li);
-      v1[j] = __ldg(Z + zi[bc] + li + 1);
+      v[j] = __ldg(Z + zi[bc] + li);
     } else {
       const int cls = NE * class_cb(Region<R>::k(j), G::b);
       const int off = zr[bc] + t * REC + cls + u;
-      if (Region<R>::a(j)) {
-        const int wrapd = zr[bc] + tp * REC + cls + (NE - 1) * S;  // + u: last element of the tile before
-        v0[j] = __ldg(Z + (u >= S ? off - S : wrapd + u));
-        v1[j] = __ldg(Z + (u + 1 >= S ? off + 1 - S : wrapd + u + 1));
+      v[j] = __ldg(Z + (!Region<R>::a(j) ? off : (u >= S ? off - S : zr[bc] + tp * REC + cls + (NE - 1) * S + u)));
+    }
+  }
+  return 0.0;
+}
+
+template <int P, int NE, int R>
+__device__ __forceinline__ void owned_sum2(const double* __restrict__ Z, const int* zr, const int* zi, int T,
+                                           int li, double& acc0, double& acc1) {
+  // outputs li and li + 1 (li even, same region: n S is even); when the
+  // tile run NE S is even they share the index math (same tile), 2 NC loads
+  // in flight per thread either way
+  using G = OwnerGeom<P>;
+  constexpr int S = G::S(R), NC = Region<R>::NC, RUN = NE * S, REC = NE * G::ZS;
+  double v0[NC], v1[NC];
+  if constexpr (RUN % 2 != 0) {
+    owned_one<P, NE, R>(Z, zr, zi, T, li, v0);
+    owned_one<P, NE, R>(Z, zr, zi, T, li + 1, v1);
+  } else {
+    const int t = li / RUN, u = li - t * RUN;
+    const int tp = t == 0 ? T - 1 : t - 1;  // tile of the x - 1 neighbour at u < S
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const int bc = Region<R>::b(j) * 2 + Region<R>::c(j);
+      if constexpr (R == 7) {
+        v0[j] = __ldg(Z + zi[bc] + li);
+        v1[j] = __ldg(Z + zi[bc] + li + 1);
       } else {
-        v0[j] = __ldg(Z + off);
-        v1[j] = __ldg(Z + off + 1);
+        const int cls = NE * class_cb(Region<R>::k(j), G::b);
+        const int off = zr[bc] + t * REC + cls + u;
+        if (Region<R>::a(j)) {
+          const int wrapd = zr[bc] + tp * REC + cls + (NE - 1) * S;  // + u: last element of the tile before
+          v0[j] = __ldg(Z + (u >= S ? off - S : wrapd + u));
+          v1[j] = __ldg(Z + (u + 1 >= S ? off + 1 - S : wrapd + u + 1));
+        } else {
+          v0[j] = __ldg(Z + off);
+          v1[j] = __ldg(Z + off + 1);
+        }
       }
     }
   }
@@ -639,6 +665,7 @@ cudaError_t class_owner_sum(int n, int P, int ne, const double* Z, double* y, in
   };
   auto by_ne = [&](auto pc) -> cudaError_t {
     switch (ne) {
+      case 1: return go(pc, std::integral_constant<int, 1>());
       case 2: return go(pc, std::integral_constant<int, 2>());
       case 4: return go(pc, std::integral_constant<int, 4>());
       case 8: return go(pc, std::integral_constant<int, 8>());

@@ -45,20 +45,28 @@ struct BlockIO {
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
-template <bool PRE>
+template <bool PRE, int PV = 1>
 struct ClassIO {
   static constexpr bool DENSE = false;
-  const int* tab;
+  const int* tab;  // PV tables of IN position words
   // PRE: every thread owns at most one (e, p, q) row of S1 / S9, the same
-  // for every tile: its three positions are resolved once per kernel
-  int p0 = 0, p1 = 0, p2 = 0;
+  // for every tile: its three positions are resolved once per kernel, for
+  // each of the PV tile parities (odd NE: the 16-byte parity of the tile's
+  // x ranges alternates with the tile)
+  int p[PV][3] = {};
+  int v = 0;  // this tile's parity variant
+  int in_size = 0;
   __device__ __forceinline__ static int at(int t, int e) { return (t & 0xffff) + e * (t >> 16); }
   template <int M>
   __device__ __forceinline__ void resolve(int e, int pq, int& a0, int& a1, int& a2) const {
+    const int vv = PV > 1 ? v : 0;
     if constexpr (PRE) {
-      a0 = p0, a1 = p1, a2 = p2;
+      // selects, not a dynamic index (which would put p in local memory)
+      a0 = (PV > 1 && vv) ? p[PV - 1][0] : p[0][0];
+      a1 = (PV > 1 && vv) ? p[PV - 1][1] : p[0][1];
+      a2 = (PV > 1 && vv) ? p[PV - 1][2] : p[0][2];
     } else {
-      const int* tr = tab + pq * M;
+      const int* tr = tab + vv * in_size + pq * M;
       a0 = at(tr[0], e), a1 = at(tr[1], e), a2 = at(tr[2], e);
     }
   }
@@ -165,8 +173,9 @@ struct Scaffold {
   static constexpr int NE = Op::NE, NT = Op::NT;
   static constexpr bool CLS = ModeTraits<MODE>::CLASS;
   // MODE 5 stages each of the 27 classes in its own slot of NE * size + 2
-  // doubles (room for the 16-byte widening of its copy window)
-  static constexpr int IN_T = CLS ? even_up(NE * Op::IN + 2 * 27) : even_up(NE * Op::IN + 2);
+  // doubles (room for the 16-byte widening of its copy window) rounded up
+  // to even (16-byte aligned slots)
+  static constexpr int IN_T = CLS ? even_up(NE * Op::IN + 3 * 27) : even_up(NE * Op::IN + 2);
   static constexpr int GEO_S = geo_s_impl<Op>(0);  // even, >= GEO
   static constexpr int GEO_T = NE * GEO_S;
   static constexpr int STAGE = IN_T + GEO_T;
@@ -188,9 +197,11 @@ struct Scaffold {
   static constexpr int ITAB = (MODE == 0 || CLS) ? 0 : even_up(NE * (2 + ENT)) / 2 + 1;
   // MODE 5 int tables: per-mode input / output positions (2 * IN), per
   // class slot base, Z offset, geometry and first 16-byte chunk (5 * 27 + 1)
+  // (PV tile-parity variants of the positions and of the chunk prefix)
+  static constexpr int PV = (CLS && (NE & 1)) ? 2 : 1;
   static constexpr int MTAB = ModeTraits<MODE>::PERIODIC ? even_up(Op::IN) / 2 + 1
-                              : CLS                      ? (2 * Op::IN + 5 * 27 + 1) / 2 + 1
-                                                         : 0;
+                              : CLS ? ((PV + PV) * Op::IN + 4 * 27 + PV * 28) / 2 + 1
+                                    : 0;
   static constexpr size_t fixed_bytes(int nst) {
     return sizeof(double) * (nst * (STAGE + ITAB) + OUT_T + WORK_T + ITAB + MTAB) + 2 * sizeof(uint64_t);
   }
@@ -216,6 +227,9 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
   double* stage_base = smem;
   double* work = smem + NST * S::STAGE + S::OUT_T;
   double* out_s = S::OUT_OFF >= 0 ? work + (S::OUT_OFF >= 0 ? S::OUT_OFF : 0) : smem + NST * S::STAGE;
+  // MODE 5 stages the tile's class-major results 16-byte aligned (an odd
+  // OUT_OFF — odd element strides at odd Q with NE = 1 — moves it by one)
+  double* out_c = out_s + (MT::CLASS ? (S::OUT_OFF & 1) : 0);
   int* itab = reinterpret_cast<int*>(work + S::WORK_T);      // NST stages of [ids NE | ent NE*27]
   int* icur = itab + NST * 2 * S::ITAB;                       // current tile copy
   int* mtab = icur + 2 * S::ITAB;                             // per-mode codes (MODE 1)
@@ -235,78 +249,98 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
     for (int i = tid; i < IN; i += NT) mtab[i] = mode_code(Op::M, i);
   // MODE 5 tables: csb[k] = slot of class k in the input stage, ccb[k] =
   // offset of class k in an element's class-major record (sum of sizes),
-  // cR / csd[k] = class geometry (region base; size | d << 16 | parity << 20),
-  // cpre[k] = first 16-byte input chunk of class k (cpre[27] = count)
-  int* ptab = mtab;          // IN: input position word per mode
-  int* qtab = mtab + IN;     // IN: output position word per mode
-  int* csb = mtab + 2 * IN;  // 27
-  int* ccb = csb + 27;       // 27
-  int* cR = ccb + 27;        // 27
-  int* csd = cR + 27;        // 27
-  int* cpre = csd + 27;      // 28
+  // cR / csd[k] = class geometry (region base; size | d << 16 | parity of
+  // variant v << (20 + v)), cpre[v][k] = first 16-byte input chunk of class
+  // k (cpre[v][27] = count).  Variant v = parity of the tile's first x: with
+  // even NE and n it is always 0; with odd NE the classes of odd size start
+  // at alternating 16-byte parities, and everything parity-dependent (slot
+  // offsets, chunk lists, the interiors' staging shift) exists twice.
+  constexpr int PV = S::PV;
+  int* ptab = mtab;               // PV x IN: input position word per mode
+  int* qtab = mtab + PV * IN;     // PV x IN: output position word per mode
+  int* csb = qtab + PV * IN;      // 27
+  int* ccb = csb + 27;            // 27
+  int* cR = ccb + 27;             // 27
+  int* csd = cR + 27;             // 27
+  int* cpre = csd + 27;           // PV x 28
+  constexpr int B3 = (Op::M - 2) * (Op::M - 2) * (Op::M - 2);
   if constexpr (MT::CLASS) {
     const int b = Op::M - 2;
     if (tid < 32) {  // lane k: class k, exclusive prefix sums by warp scan
       const int k = tid;
-      int sz = 0, par = 0, nch = 0;
+      int sz = 0, dx = 0, nch0 = 0, nch1 = 0;
       ClassGeom cg{0, 0, 0};
       if (k < 27) {
         cg = class_geom(k, a.n, Op::M - 1);
         sz = class_size(k, b);
-        par = (sz & 1) & class_dx(k);
-        nch = (par + NE * sz + 1) / 2;
+        dx = class_dx(k);
+        nch0 = (((sz & 1) & dx) + NE * sz + 1) / 2;
+        nch1 = (((sz & 1) & (dx ^ 1)) + NE * sz + 1) / 2;
       }
-      int sb = k < 27 ? NE * sz + 2 : 0, cb = sz, nc = nch;
+      const int slot = k < 27 ? even_up(NE * sz + 2) : 0;
+      int sb = slot, cb = sz, nc0 = nch0, nc1 = nch1;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int a1 = __shfl_up_sync(0xffffffffu, sb, o), a2 = __shfl_up_sync(0xffffffffu, cb, o),
-                  a3 = __shfl_up_sync(0xffffffffu, nc, o);
-        if (k >= o) sb += a1, cb += a2, nc += a3;
+                  a3 = __shfl_up_sync(0xffffffffu, nc0, o), a4 = __shfl_up_sync(0xffffffffu, nc1, o);
+        if (k >= o) sb += a1, cb += a2, nc0 += a3, nc1 += a4;
       }
       if (k < 27) {
-        csb[k] = sb - (NE * sz + 2);
+        csb[k] = sb - slot;
         ccb[k] = cb - sz;
         cR[k] = cg.R;
-        csd[k] = sz | (cg.d << 16) | (par << 20);
-        cpre[k] = nc - nch;
+        csd[k] = sz | (cg.d << 16) | (((sz & 1) & dx) << 20) | (((sz & 1) & (dx ^ 1)) << 21);
+        cpre[k] = nc0 - nch0;
+        if (PV > 1) cpre[28 + k] = nc1 - nch1;
       }
-      if (k == 26) cpre[27] = nc;
+      if (k == 26) {
+        cpre[27] = nc0;
+        if (PV > 1) cpre[28 + 27] = nc1;
+      }
     }
     __syncthreads();
     for (int i = tid; i < IN; i += NT) {
       const int c = mode_code(Op::M, i), k = c & 31, off = c >> 5, sz = class_size(k, b);
-      // 16-byte parity of the class's first value: static for even n, even
-      // NE (x-shifted classes of odd size start odd)
-      const int par = (sz & 1) & class_dx(k);
-      ptab[i] = (csb[k] + par + off) | (sz << 16);
-      qtab[i] = (NE * ccb[k] + off) | (sz << 16);
+      for (int v = 0; v < PV; ++v) {
+        // 16-byte parity of the class's first value in variant v
+        const int par = (sz & 1) & ((v + class_dx(k)) & 1);
+        ptab[v * IN + i] = (csb[k] + par + off) | (sz << 16);
+        // the interiors' staging is shifted to the parity of their y range
+        const int sh = (k == 26) ? ((v * B3) & 1) : 0;
+        qtab[v * IN + i] = (NE * ccb[k] + sh + off) | (sz << 16);
+      }
     }
   }
-  // MODE 5: this thread's input chunks c = tid + j * NT (j < CPT) as
-  // class | slot offset << 5, resolved once (the chunk list is static)
+  // MODE 5: this thread's input chunks c = tid + j * NT (j < CPT) of each
+  // variant as class | slot offset << 5, resolved once (static lists)
   constexpr int CPT = MT::CLASS ? (NE * IN + 2 * 27 + 2 * NT - 1) / (2 * NT) : 1;
-  int chunk[CPT];
+  int chunk[PV][CPT];
   if constexpr (MT::CLASS) {
 #pragma unroll
-    for (int j = 0; j < CPT; ++j) {
-      const int c = tid + j * NT;
-      int k = 0;
-      while (k < 26 && cpre[k + 1] <= c) ++k;
-      chunk[j] = c < cpre[27] ? (k | ((2 * (c - cpre[k])) << 5)) : -1;
-    }
+    for (int v = 0; v < PV; ++v)
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        const int* cp = cpre + 28 * v;
+        const int c = tid + j * NT;
+        int k = 0;
+        while (k < 26 && cp[k + 1] <= c) ++k;
+        chunk[v][j] = c < cp[27] ? (k | ((2 * (c - cp[k])) << 5)) : -1;
+      }
   }
   constexpr bool PRE = NE * Op::M * Op::M <= NT;
-  ClassIO<PRE> cin_io{ptab}, cout_io{qtab};
+  ClassIO<PRE, PV> cin_io{ptab}, cout_io{qtab};
+  cin_io.in_size = cout_io.in_size = IN;
   if constexpr (MT::CLASS && PRE) {
     __syncthreads();
     if (tid < NE * Op::M * Op::M) {
       const int e = tid / (Op::M * Op::M), pq = tid - e * (Op::M * Op::M);
-      cin_io.p0 = ClassIO<PRE>::at(ptab[pq * Op::M], e);
-      cin_io.p1 = ClassIO<PRE>::at(ptab[pq * Op::M + 1], e);
-      cin_io.p2 = ClassIO<PRE>::at(ptab[pq * Op::M + 2], e);
-      cout_io.p0 = ClassIO<PRE>::at(qtab[pq * Op::M], e);
-      cout_io.p1 = ClassIO<PRE>::at(qtab[pq * Op::M + 1], e);
-      cout_io.p2 = ClassIO<PRE>::at(qtab[pq * Op::M + 2], e);
+#pragma unroll
+      for (int v = 0; v < PV; ++v)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          cin_io.p[v][r] = ClassIO<PRE, PV>::at(ptab[v * IN + pq * Op::M + r], e);
+          cout_io.p[v][r] = ClassIO<PRE, PV>::at(qtab[v * IN + pq * Op::M + r], e);
+        }
     }
   }
   __syncthreads();
@@ -468,13 +502,16 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
       const int n = a.n, rowi = w0 / n, ex0 = w0 - rowi * n;
       const int ez = rowi / n, ey = rowi - ez * n;
       const bool wrap = ex0 + NE == n;
+      const int v = PV > 1 ? (ex0 & 1) : 0;
 #pragma unroll
       for (int j = 0; j < CPT; ++j) {
-        if (chunk[j] < 0) continue;
-        const int k = chunk[j] & 31, d = chunk[j] >> 5;
+        const int w = (PV > 1 && v) ? chunk[PV - 1][j] : chunk[0][j];
+        if (w < 0) continue;
+        const int k = w & 31, d = w >> 5;
         // volatile: keeps ptxas from hoisting these per-chunk constants out
         // of the tile loop (they would stay live through the pointwise stage)
-        const int sd = ld_volatile_s32(csd + k), sz = sd & 0xffff, dx = (sd >> 16) & 1, par = sd >> 20;
+        const int sd = ld_volatile_s32(csd + k), sz = sd & 0xffff, dx = (sd >> 16) & 1,
+                  par = (sd >> (20 + v)) & 1;
         int y = ey + ((sd >> 17) & 1), z = ez + ((sd >> 18) & 1);
         y -= y >= n ? n : 0;
         z -= z >= n ? n : 0;
@@ -603,7 +640,11 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
       // the class slots are free once S1 has read them: the next tile's x
       // chunks are issued right after S1 (all of S2..S9 to land)
       auto after_in = [&]() { issue_x(ts + G); };
-      Op::compute(in_p, geo_s, work, out_s, a.lam, release, pre_out, c_tab, cin_io, cout_io, after_in);
+      if constexpr (PV > 1) {
+        const int v = (int)(((a.e0 + w0) % a.n) & 1);  // parity of the tile's first x
+        cin_io.v = cout_io.v = v;
+      }
+      Op::compute(in_p, geo_s, work, out_c, a.lam, release, pre_out, c_tab, cin_io, cout_io, after_in);
       fence_proxy_async();
     } else {
       Op::compute(in_p, geo_s, work, out_t, a.lam, release, pre_out, c_tab);
@@ -613,31 +654,38 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
 
     // ---- write back ------------------------------------------------------
     if constexpr (MT::CLASS) {
-      // lane k: class k's NE * size results -> Z (class region k, element
-      // w0..w0+NE-1: one contiguous, 16-byte aligned range), interiors
-      // straight into y when the caller does not accumulate
-      // the tile's results leave in two bulk stores: classes 0..25
+      // the tile's results leave in TMA bulk stores: classes 0..25
       // (class-major within the tile) to its record of the tile-major block
-      // Z, the interiors straight into y (or after Z when accumulating).
-      // Thread stores when a base is not 16-byte aligned (C-ABI callers may
-      // pass offset pointers); keeping that loop in the kernel also keeps
-      // ptxas at ~100 registers (without it: ~150, two CTAs per SM at P=4)
-      constexpr int b = Op::M - 2, ZS = IN - b * b * b, B3 = b * b * b;
+      // Z (always 16-byte aligned: ZS is even), the interiors straight into
+      // y (or after Z when accumulating); with odd NE and odd (P-1)^3 the
+      // interiors' y range starts odd, so their staging is shifted to the
+      // same parity (qtab) and the stores split into scalar head / bulk
+      // body / scalar tail.  Thread stores when a base is not 16-byte
+      // aligned (C-ABI callers may pass offset pointers); keeping that loop
+      // in the kernel also keeps ptxas at ~100 registers (without it: ~150,
+      // two CTAs per SM at P=4)
+      constexpr int b = Op::M - 2, ZS = IN - b * b * b, B3 = b * b * b, NI = NE * B3;
       const int64_t wa = a.e0 + w0, N3 = (int64_t)a.n * a.n * a.n;
+      const int sh = (int)((wa * B3) & 1);
       double* zdst = a.zbuf + wa * ZS;
-      double* ydst = (a.direct_interior ? a.yg + N3 * (1 + 3 * b + 3 * b * b) : a.zbuf + N3 * ZS) + wa * B3;
-      if (((reinterpret_cast<uintptr_t>(zdst) | reinterpret_cast<uintptr_t>(ydst)) & 15) == 0) {
+      double* ybase = a.direct_interior ? a.yg + N3 * (1 + 3 * b + 3 * b * b) : a.zbuf + N3 * ZS;
+      double* ydst = ybase + wa * B3;
+      const double* isrc = out_c + NE * ZS + sh;
+      if (((reinterpret_cast<uintptr_t>(zdst) | reinterpret_cast<uintptr_t>(ybase)) & 15) == 0) {
         if (tid == 0) {
-          bulk_s2g(zdst, out_s, (uint32_t)(sizeof(double) * NE * ZS));
-          bulk_s2g(ydst, out_s + NE * ZS, (uint32_t)(sizeof(double) * NE * B3));
+          bulk_s2g(zdst, out_c, (uint32_t)(sizeof(double) * NE * ZS));
+          const int body = (NI - sh) & ~1;
+          if (sh) ydst[0] = isrc[0];
+          if (body > 0) bulk_s2g(ydst + sh, isrc + sh, (uint32_t)(sizeof(double) * body));
+          if (sh + body < NI) ydst[NI - 1] = isrc[NI - 1];
           bulk_commit();
         }
       } else {
         for (int i = tid; i < NE * IN; i += NT) {
           if (i < NE * ZS)
-            zdst[i] = out_s[i];
+            zdst[i] = out_c[i];
           else
-            ydst[i - NE * ZS] = out_s[i];
+            ydst[i - NE * ZS] = isrc[i - NE * ZS];
         }
         __syncthreads();  // out_s is rewritten by the next tile
       }

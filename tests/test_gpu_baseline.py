@@ -193,7 +193,7 @@ def test_cfg4_assembled_64_sampled(sp, P):
     E = n ** 3
     batch, coll = _cfg4(sp, P, n)
     amap = sp.AssemblyMap.hex_periodic(n, P)
-    assert amap.algorithm == ("split" if P == 7 else "class")
+    assert amap.algorithm == "class"
     op = sp.GlobalHelmholtz([(coll, amap)], amap.num_global)
     ng = amap.num_global
     x = np.random.default_rng(SEED + 10 * P).uniform(-1, 1, ng)

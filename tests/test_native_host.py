@@ -132,7 +132,7 @@ def test_default_assembly_algorithm():
     assembly is refused on explicit maps."""
     assert sp.AssemblyMap.hex_periodic(8, 4).algorithm == "class"
     assert sp.AssemblyMap.hex_periodic(6, 4).algorithm == "class"   # runtime fallback: split
-    assert sp.AssemblyMap.hex_periodic(8, 7).algorithm == "split"
+    assert sp.AssemblyMap.hex_periodic(8, 7).algorithm == "class"
     assert sp.AssemblyMap.hex_periodic(8, 1).algorithm == "owner"   # no bubbles
     per = sp.AssemblyMap.hex_periodic(8, 3)
     for alg in ("colour", "split", "owner", "class"):
