@@ -655,8 +655,10 @@ cudaError_t class_owner_sum(int n, int P, int ne, const double* Z, double* y, in
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t blocks = row1 - row0;
-  if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+  // one wave of CTAs with the same number of rows each (no tail)
+  const int64_t rows = row1 - row0, cap = (int64_t)sms * 8;
+  const int64_t per = (rows + cap - 1) / cap;
+  const int64_t blocks = (rows + per - 1) / per;
   auto go = [&](auto pc, auto nc) -> cudaError_t {
     constexpr int PP = decltype(pc)::value, NE = decltype(nc)::value;
     class_owner_sum_kernel<PP, NE><<<(unsigned)blocks, 256, 0, s>>>(n, Z, y, accumulate, with_interior ? 8 : 7,
