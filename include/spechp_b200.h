@@ -178,6 +178,17 @@ int sphp_amap_create_hex_periodic(int n, int P, sphp_amap** out);
  * back to back (element e at offsets[e], offsets has n^3+1 entries).       */
 int sphp_hexmap_variable(int n, const int* orders, int64_t* num_global,
                          int64_t* offsets, int64_t* codes);
+/* rows [e0, e1) (element id ex + n (ey + n ez)) of the uniform-order
+ * periodic map's codes, (e1 - e0, (P+1)^3) int64: a rank's slab of the
+ * sharded operator without building the whole n^3 table                  */
+int sphp_hexmap_periodic_codes(int n, int P, int64_t e0, int64_t e1, int64_t* codes);
+/* the sharded operator's interface exchange (distributed.py): pack
+ * dst[i] = src[idx[i]]; combine y[idx[i]] = lo[i] + hi[i] (the lower
+ * rank's partial sum first, so both sides hold identical bits)            */
+int sphp_index_gather(int64_t n, const int64_t* idx, const double* src, double* dst,
+                      sphp_stream stream);
+int sphp_index_sum2(int64_t n, const int64_t* idx, const double* lo, const double* hi,
+                    double* y, sphp_stream stream);
 int sphp_amap_destroy(sphp_amap* a);
 /* assembly algorithm of sphp_assemble / sphp_helmholtz_assembled, both
  * deterministic (bitwise reproducible) and atomic-free.  Default: SPLIT for

@@ -89,6 +89,9 @@ _SIGS = {
     "sphp_amap_algorithm": (_i, [_p, _p]),
     "sphp_amap_info": (_i, [_p, _i64p, _ip, _i64p, _ip]),
     "sphp_amap_codes": (_i, [_p, _p]),
+    "sphp_hexmap_periodic_codes": (_i, [_i, _i, _i64, _i64, _p]),
+    "sphp_index_gather": (_i, [_i64, _p, _p, _p, _p]),
+    "sphp_index_sum2": (_i, [_i64, _p, _p, _p, _p, _p]),
     "sphp_scatter": (_i, [_p, _p, _p, _p]),
     "sphp_assemble": (_i, [_p, _p, _p, _p]),
     "sphp_helmholtz_assembled": (_i, [_p, _p, _p, _p, _i, _p]),

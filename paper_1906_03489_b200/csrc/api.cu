@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "misc.h"
+#include "periodic.cuh"
 #include "solver.h"
 #include "tables.h"
 
@@ -1341,6 +1342,40 @@ int sphp_hexmap_variable(int n, const int* orders, int64_t* num_global, int64_t*
       }
   if (offsets) offsets[N3] = off;
   *num_global = gid;
+  return SPHP_OK;
+}
+
+// rows [e0, e1) of the periodic structured hex map (the analytic numbering
+// of sphp_amap_create_hex_periodic, = sphp_hexmap_variable at uniform
+// order): per-slab maps for the sharded operator without the n^3 table
+int sphp_hexmap_periodic_codes(int n, int P, int64_t e0, int64_t e1, int64_t* codes) {
+  if (n < 1 || P < 1 || e0 < 0 || e1 < e0 || e1 > (int64_t)n * n * n || !codes)
+    return fail(SPHP_ERR_BAD_ARG, "bad arguments");
+  if (ipow((int64_t)n * P, 3) > 2147483645LL) return fail(SPHP_ERR_UNSUPPORTED, "more than 2^31-3 global dofs");
+  const int M = P + 1, nm = M * M * M;
+  std::vector<int> mc(nm);
+  for (int i = 0; i < nm; ++i) mc[i] = mode_code(M, i);
+  for (int64_t e = e0; e < e1; ++e) {
+    const int ex = (int)(e % n), ey = (int)((e / n) % n), ez = (int)(e / ((int64_t)n * n));
+    int base[27];
+    for (int k = 0; k < 27; ++k) base[k] = entity_base(n, P, ex, ey, ez, k);
+    int64_t* row = codes + (e - e0) * nm;
+    for (int i = 0; i < nm; ++i) row[i] = base[mc[i] & 31] + (mc[i] >> 5);
+  }
+  return SPHP_OK;
+}
+
+// the sharded operator's interface exchange: dst[i] = src[idx[i]] (pack),
+// y[idx[i]] = lo[i] + hi[i] (combine the two copies in rank order)
+int sphp_index_gather(int64_t n, const int64_t* idx, const double* src, double* dst, sphp_stream stream) {
+  if (n < 0 || (n > 0 && (!idx || !src || !dst))) return fail(SPHP_ERR_BAD_ARG, "bad arguments");
+  CK(index_gather(n, idx, src, dst, (cudaStream_t)stream));
+  return SPHP_OK;
+}
+int sphp_index_sum2(int64_t n, const int64_t* idx, const double* lo, const double* hi, double* y,
+                    sphp_stream stream) {
+  if (n < 0 || (n > 0 && (!idx || !lo || !hi || !y))) return fail(SPHP_ERR_BAD_ARG, "bad arguments");
+  CK(index_sum2(n, idx, lo, hi, y, (cudaStream_t)stream));
   return SPHP_OK;
 }
 

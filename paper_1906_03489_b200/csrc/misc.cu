@@ -770,4 +770,33 @@ cudaError_t periodic_entity_table(int n, int P, int* ent, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// sharded operator's interface exchange (distributed.py): pack the
+// interface entries into a send buffer, and combine the two copies in rank
+// order (lo + hi: identical bits on both sides of the interface)
+__global__ void index_gather_kernel(int64_t n, const int64_t* __restrict__ idx, const double* __restrict__ src,
+                                    double* __restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+__global__ void index_sum2_kernel(int64_t n, const int64_t* __restrict__ idx, const double* __restrict__ lo,
+                                  const double* __restrict__ hi, double* __restrict__ y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[idx[i]] = lo[i] + hi[i];
+}
+static unsigned grid_for(int64_t n) {
+  const int64_t b = (n + 255) / 256;
+  return (unsigned)(b < 1 ? 1 : (b > 65535 ? 65535 : b));
+}
+cudaError_t index_gather(int64_t n, const int64_t* idx, const double* src, double* dst, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  index_gather_kernel<<<grid_for(n), 256, 0, s>>>(n, idx, src, dst);
+  return cudaGetLastError();
+}
+cudaError_t index_sum2(int64_t n, const int64_t* idx, const double* lo, const double* hi, double* y,
+                       cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  index_sum2_kernel<<<grid_for(n), 256, 0, s>>>(n, idx, lo, hi, y);
+  return cudaGetLastError();
+}
+
 }  // namespace sphp

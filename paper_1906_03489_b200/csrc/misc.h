@@ -54,6 +54,9 @@ cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int ac
 cudaError_t periodic_scatter_v2(int n, int P, const double* x, double* loc, cudaStream_t s,
                                 int row0 = 0, int row1 = -1, int* ctr = nullptr);
 cudaError_t periodic_entity_table(int n, int P, int* ent, cudaStream_t s);
+cudaError_t index_gather(int64_t n, const int64_t* idx, const double* src, double* dst, cudaStream_t s);
+cudaError_t index_sum2(int64_t n, const int64_t* idx, const double* lo, const double* hi, double* y,
+                       cudaStream_t s);
 cudaError_t amap_scatter(const AmapDev& m, const double* g, double* loc, cudaStream_t s, int* ctr = nullptr);
 cudaError_t owner_assemble_csr32(int64_t ng, const int* rowp, const int* ent, const double* loc, double* y,
                                  cudaStream_t s);

@@ -13,7 +13,7 @@ namespace sphp {
 // once per CTA, the 27 entity bases once per element, so a gather/scatter
 // index costs one shared load and one add.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int mode_code(int M, int nl) {
+__host__ __device__ __forceinline__ int mode_code(int M, int nl) {
   const int b = M - 2;  // bubbles per edge (P - 1)
   const int p = nl / (M * M), q = (nl / M) % M, r = nl % M;
   const int idx[3] = {p, q, r};
@@ -89,7 +89,7 @@ __host__ __device__ __forceinline__ int class_gid(const ClassGeom& g, int n, int
   z -= z >= n ? n : 0;
   return g.R + g.s * (x + n * (y + n * z));
 }
-__device__ __forceinline__ int entity_base(int n, int P, int ex, int ey, int ez, int k) {
+__host__ __device__ __forceinline__ int entity_base(int n, int P, int ex, int ey, int ez, int k) {
   const int N3 = n * n * n, b = P - 1;
   auto wrap = [n](int i) { return i >= n ? i - n : i; };
   auto vid = [&](int i, int j, int l) { return wrap(i) + n * (wrap(j) + n * wrap(l)); };

@@ -9,6 +9,9 @@ interface planes are swapped with the neighbouring ranks (point-to-point,
 NCCL over NVLink on GPUs, gloo on CPUs) and added in rank order, so both
 copies of an interface dof are bitwise identical and independent of which
 rank computed them.  0.5 MB per neighbour at P=4, n=64 (one z-plane of dofs).
+Each rank builds only its slab's rows of the map (the periodic numbering in
+closed form, sphp_hexmap_periodic_codes) and its neighbours' adjacent
+element layers; the exchange's pack / combine run as our kernels.
 
 Dot products for CG count every dof once (owned = lowest rank touching it)
 and are all-reduced.
@@ -19,32 +22,48 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .assembly import hex_variable_codes
+from . import _lib
+
+
+def slab_codes(n, P, e0, e1):
+    """Rows [e0, e1) of the periodic map's codes (sphp_hexmap_periodic_codes:
+    the analytic numbering, no n^3 table)."""
+    nm = (P + 1) ** 3
+    out = np.empty((e1 - e0, nm), dtype=np.int64)
+    _lib.check(_lib.lib.sphp_hexmap_periodic_codes(int(n), int(P), int(e0), int(e1), _lib.ptr(out)))
+    return out
 
 
 class SlabPartition:
-    """Rank `rank`'s z-slab of the periodic n^3 grid with order P."""
+    """Rank `rank`'s z-slab of the periodic n^3 grid with order P.  Only the
+    slab's own rows of the map are built, plus the one element layer of each
+    neighbour that touches it (its interface planes)."""
 
     def __init__(self, n, P, rank, world):
         if n % world or n // world < 2:
             raise ValueError(f"need n divisible by world with >= 2 layers per rank (n={n}, world={world})")
         self.n, self.P, self.rank, self.world = n, P, rank, world
         nz = n // world
+        n2 = n * n
         self.z0, self.z1 = rank * nz, (rank + 1) * nz
-        self.e0, self.e1 = self.z0 * n * n, self.z1 * n * n
-        ng, off, codes = hex_variable_codes(n, np.full(n ** 3, P, dtype=np.int32))
-        nm = (P + 1) ** 3
-        self.num_global_total = ng
-        allc = codes.reshape(n ** 3, nm)
-        mine = allc[self.e0:self.e1]
+        self.e0, self.e1 = self.z0 * n2, self.z1 * n2
+        self.num_global_total = (n * P) ** 3
+        mine = slab_codes(n, P, self.e0, self.e1)
         self.gids = np.unique(mine)                       # local -> global, sorted
         self.local_codes = np.searchsorted(self.gids, mine).astype(np.int64)
         self.num_local = self.gids.size
-        # interface dofs shared with each neighbour rank (ring), sorted by gid
+        # interface dofs shared with each neighbour rank (ring), sorted by
+        # gid: the neighbour's element layer adjacent to this slab (below:
+        # its top layer z0 - 1; above: its bottom layer z1)
+        below, above = (rank - 1) % world, (rank + 1) % world
+        layers = {}
+        for nb, z in ((below, (self.z0 - 1) % n), (above, self.z1 % n)):
+            if nb == rank:
+                continue
+            layers.setdefault(nb, []).append(slab_codes(n, P, z * n2, (z + 1) * n2))
         self.shared = {}
-        for nb in {(rank - 1) % world, (rank + 1) % world} - {rank}:
-            lo, hi = nb * nz * n * n, (nb + 1) * nz * n * n
-            theirs = np.unique(allc[lo:hi])
+        for nb, rows in layers.items():
+            theirs = np.unique(np.concatenate([r.ravel() for r in rows]))
             common = np.intersect1d(self.gids, theirs, assume_unique=True)
             self.shared[nb] = np.searchsorted(self.gids, common)
         # ownership for reductions: lowest rank touching the dof
@@ -68,7 +87,7 @@ class DistributedHelmholtz:
         self._owned = torch.as_tensor(part.owned, device=device)
 
     @classmethod
-    def from_gpu(cls, part: SlabPartition, lam=1.0, amp=0.03, device=None):
+    def from_gpu(cls, part: SlabPartition, lam=1.0, amp=0.03, device=None, algorithm="split"):
         from . import (GEOM_METRIC, MAP_HEX_SINE, AssemblyMap, Collection, ElementBatch,
                        GlobalHelmholtz, OperatorKind, Strategy, make_hex)
         from .geometry import structured_geometry
@@ -79,7 +98,9 @@ class DistributedHelmholtz:
                                 num_elements=part.e1 - part.e0, device=dev)
         coll = Collection(ElementBatch(exp, part.e1 - part.e0, g, GEOM_METRIC), OperatorKind.HELMHOLTZ,
                           Strategy.CUDA_SUMFAC, lam=lam)
-        amap = AssemblyMap.explicit(part.local_codes, part.num_local)
+        # split: explicit scatter -> fused operator on the local block ->
+        # CSR owner sum (faster than the gathering owner path on slabs)
+        amap = AssemblyMap.explicit(part.local_codes, part.num_local).set_algorithm(algorithm)
         op = GlobalHelmholtz([(coll, amap)], part.num_local)
         obj = cls(part, lambda x, y: op.apply(x, y), dev)
         obj._keep = (exp, g, coll, amap, op)
@@ -94,12 +115,20 @@ class DistributedHelmholtz:
 
     def exchange_add(self, y_local):
         """The one exchange step: swap interface partial sums with each
-        neighbour, add in rank order (identical bits on both sides)."""
+        neighbour, add in rank order (identical bits on both sides).  On the
+        GPU the pack and the combine are our kernels (sphp_index_gather /
+        sphp_index_sum2) and the swap is NCCL point-to-point over NVLink."""
         if not self._idx:
             return y_local
+        cuda = y_local.is_cuda
         ops, bufs = [], {}
         for nb, idx in sorted(self._idx.items()):
-            send = y_local.index_select(0, idx).contiguous()
+            send = torch.empty(idx.numel(), dtype=y_local.dtype, device=y_local.device)
+            if cuda:
+                _lib.check(_lib.lib.sphp_index_gather(idx.numel(), _lib.ptr(idx), _lib.ptr(y_local), _lib.ptr(send),
+                                                      _lib.stream_ptr()))
+            else:
+                torch.index_select(y_local, 0, idx, out=send)
             recv = torch.empty_like(send)
             bufs[nb] = (idx, send, recv)
             ops.append(dist.P2POp(dist.isend, send, nb))
@@ -108,7 +137,11 @@ class DistributedHelmholtz:
             req.wait()
         for nb, (idx, send, recv) in sorted(bufs.items()):
             lo, hi = (recv, send) if nb < self.part.rank else (send, recv)
-            y_local.index_copy_(0, idx, lo + hi)
+            if cuda:
+                _lib.check(_lib.lib.sphp_index_sum2(idx.numel(), _lib.ptr(idx), _lib.ptr(lo), _lib.ptr(hi),
+                                                    _lib.ptr(y_local), _lib.stream_ptr()))
+            else:
+                y_local.index_copy_(0, idx, lo + hi)
         return y_local
 
     def dot(self, a, b):
