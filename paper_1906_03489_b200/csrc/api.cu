@@ -459,9 +459,18 @@ int stdmat_prepare(sphp_coll* c) {
   if (c->op == SPHP_OP_HELMHOLTZ) {
     if (!t->fast)
       return fail(SPHP_ERR_UNSUPPORTED, "stdmat Helmholtz needs a sum-factorisation key to build H_e");
+    // dense element matrices: up to half the free device memory (B200: 180
+    // GB HBM3e; e.g. the cfg5 P = 6 / P = 7 batches, 21 / 46 GB)
     const double bytes = 8.0 * c->E * nm * nm;
-    if (bytes > 16e9)
-      return fail(SPHP_ERR_UNSUPPORTED, "stdmat Helmholtz element matrices exceed the 16 GB budget");
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    if (bytes > 0.5 * (double)free_b) {
+      char buf[160];
+      std::snprintf(buf, sizeof(buf),
+                    "stdmat Helmholtz element matrices (%.1f GB) exceed half the free device memory (%.1f GB)",
+                    bytes / 1e9, free_b / 1e9);
+      return fail(SPHP_ERR_UNSUPPORTED, buf);
+    }
     CK(c->helm_H.ensure((size_t)bytes));
     DevBuf ux, uy;
     CK(ux.ensure(sizeof(double) * c->E * nm));
