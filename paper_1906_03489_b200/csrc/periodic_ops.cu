@@ -481,8 +481,11 @@ cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int ac
 // summed in increasing (a, b, c) order, as owner_periodic_v3 does, so both
 // give bitwise-identical results.
 // ---------------------------------------------------------------------------
+#ifndef CLASS_OWNER_NT
+#define CLASS_OWNER_NT 128
+#endif
 #ifndef CLASS_OWNER_MINB
-#define CLASS_OWNER_MINB 8
+#define CLASS_OWNER_MINB (2048 / CLASS_OWNER_NT)
 #endif
 namespace {
 
@@ -600,7 +603,7 @@ __device__ __forceinline__ void owned_sum2(const double* __restrict__ Z, const i
 // an output is a few compares), so every thread has work at every order.
 // 32-bit offsets from Z: n^3 nm < 2^31 for every map the kernels accept.
 template <int P, int NE>
-__global__ void __launch_bounds__(256, CLASS_OWNER_MINB) class_owner_sum_kernel(int n, const double* __restrict__ Z,
+__global__ void __launch_bounds__(CLASS_OWNER_NT, CLASS_OWNER_MINB) class_owner_sum_kernel(int n, const double* __restrict__ Z,
                                                               double* __restrict__ y, int accumulate,
                                                               int nreg, int row0, int row1) {
   using G = OwnerGeom<P>;
@@ -656,12 +659,12 @@ cudaError_t class_owner_sum(int n, int P, int ne, const double* Z, double* y, in
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // one wave of CTAs with the same number of rows each (no tail)
-  const int64_t rows = row1 - row0, cap = (int64_t)sms * 8;
+  const int64_t rows = row1 - row0, cap = (int64_t)sms * (2048 / CLASS_OWNER_NT);
   const int64_t per = (rows + cap - 1) / cap;
   const int64_t blocks = (rows + per - 1) / per;
   auto go = [&](auto pc, auto nc) -> cudaError_t {
     constexpr int PP = decltype(pc)::value, NE = decltype(nc)::value;
-    class_owner_sum_kernel<PP, NE><<<(unsigned)blocks, 256, 0, s>>>(n, Z, y, accumulate, with_interior ? 8 : 7,
+    class_owner_sum_kernel<PP, NE><<<(unsigned)blocks, CLASS_OWNER_NT, 0, s>>>(n, Z, y, accumulate, with_interior ? 8 : 7,
                                                                     row0, row1);
     return cudaGetLastError();
   };
