@@ -48,10 +48,15 @@ static int helm_variant_env() {
 
 // PERIODIC_CLASS (pipeline MODE 5): tiles of NE consecutive elements of an
 // x-row (NE must divide n)
+// MODE 6 (geometry from global memory, L2-prefetched) at P = 2 / METRIC
+template <int M, int Q, int GK>
+constexpr int class_mode() {
+  return (GK == SPHP_GEOM_METRIC && M == 3 && Q == 4) ? 6 : 5;
+}
 template <int M, int Q, int GK, int NE>
 constexpr size_t class_smem() {
   using Op = HexHelm<M, Q, GK, NE, choose_nt(NE, Q * Q), 1>;
-  return Scaffold<Op, 5>::SMEM_BYTES;
+  return Scaffold<Op, class_mode<M, Q, GK>()>::SMEM_BYTES;
 }
 // tile size of the class mode: the NE in {1, 2, 4, 8} that keeps the most
 // elements resident per SM (shared memory: 228 KB per SM, 1 KB per CTA;
@@ -90,7 +95,7 @@ static cudaError_t helm_class(const OpArgs& oa, cudaStream_t s) {
     using Op = HexHelm<M, Q, GK, NE, NT, 1>;
     if (M < 3 || oa.n % NE != 0 || oa.n % 2 != 0 || oa.E % NE != 0) return cudaErrorNotSupported;
     if (oa.ne_out) *oa.ne_out = NE;
-    return launch_pipe<Op, 5>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
+    return launch_pipe<Op, class_mode<M, Q, GK>()>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
   }
 }
 

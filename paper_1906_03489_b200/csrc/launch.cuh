@@ -80,6 +80,7 @@ cudaError_t launch_pipe(const OpArgs& oa, int64_t gstride, int64_t goff, cudaStr
   a.e0 = oa.e0;
   a.zbuf = oa.zbuf;
   a.direct_interior = oa.direct_interior;
+  if (Sc::GDIR && (gstride != Op::GEO || goff != 0)) return cudaErrorNotSupported;
   const int64_t count = (MODE == 0 || MODE >= 3) ? oa.E : oa.nlist;
   if (count <= 0) return cudaSuccess;
   const int64_t ntiles = (count + Op::NE - 1) / Op::NE;
@@ -119,7 +120,7 @@ cudaError_t launch_mode(const OpArgs& oa, int64_t gstride, int64_t goff, cudaStr
     case AsmMode::EXPLICIT_GATHER:
       return launch_pipe<Op, 4>(oa, gstride, goff, s);
     case AsmMode::PERIODIC_CLASS:
-      return cudaErrorNotSupported;  // Helmholtz only (hex_helm.cu: helm_class)
+      return cudaErrorNotSupported;  // Helmholtz only (hex_helm.cu: helm_class, MODE 5 / 6)
   }
   return cudaErrorInvalidValue;
 }

@@ -128,6 +128,7 @@ struct DevArgs {
 // MODE 2: explicit map, colour class: gather in, scatter-add out.
 // MODE 3: periodic hex, all elements in order: gather in, local block out.
 // MODE 4: explicit map, all elements in order: gather in, local block out.
+// MODE 6: MODE 5 with the geometry read from global memory (L2 prefetch).
 // MODE 5: periodic hex, all elements in order, by entity class: the tile's
 //         27 class ranges of x arrive by TMA bulk copies into a class-
 //         staged input, results leave by 27 bulk stores into the class-major
@@ -141,7 +142,8 @@ struct ModeTraits {
   static constexpr bool EXPLICIT = MODE == 2 || MODE == 4;
   static constexpr bool SCATTER = MODE == 1 || MODE == 2;
   static constexpr bool CONTIG = MODE == 0 || MODE >= 3;
-  static constexpr bool CLASS = MODE == 5;
+  static constexpr bool CLASS = MODE == 5 || MODE == 6;
+  static constexpr bool GDIR = MODE == 6;  // class, geometry read from global memory
 };
 // ---------------------------------------------------------------------------
 // preferred number of input stages: Op::NSTP when the Op declares it, else 1
@@ -177,7 +179,13 @@ struct Scaffold {
   // to even (16-byte aligned slots)
   static constexpr int IN_T = CLS ? even_up(NE * Op::IN + 3 * 27) : even_up(NE * Op::IN + 2);
   static constexpr int GEO_S = geo_s_impl<Op>(0);  // even, >= GEO
-  static constexpr int GEO_T = NE * GEO_S;
+  // MODE 6 = MODE 5 reading the geometry straight from global memory in the
+  // pointwise stage (prefetched into L2 one tile ahead) instead of staging
+  // it: no shared-memory copy, more resident CTAs.  Only wins where the
+  // tile's compute is short enough for L2 latency (P = 2: 0.209 -> 0.198
+  // ms; P = 3..8 lose 10-35 %, tools/time_phases.py)
+  static constexpr bool GDIR = ModeTraits<MODE>::GDIR;
+  static constexpr int GEO_T = GDIR ? 0 : NE * GEO_S;
   static constexpr int STAGE = IN_T + GEO_T;
   static constexpr int OUT_OFF = out_off_impl<Op>(0);
   // block-input (MODE 0) ops stream the output block back with one TMA bulk
@@ -528,6 +536,10 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
     if (ts >= ntiles || GEO == 0) return;
     double* geo_s = stage_base + s * S::STAGE + S::IN_T;
     const int64_t w0 = a.e0 + (int64_t)ts * NE;
+    if constexpr (S::GDIR) {
+      bulk_prefetch_l2(a.geom + w0 * a.gstride, (uint32_t)(sizeof(double) * NE * GEO));
+      return;
+    }
     mbar_expect_tx(&bar[s], (uint32_t)(sizeof(double) * NE * GEO));
     if (a.gstride == GEO && a.goff == 0 && GEO_S == GEO) {
       bulk_g2s(geo_s, a.geom + w0 * a.gstride, (uint32_t)(sizeof(double) * NE * GEO), &bar[s]);
@@ -565,8 +577,10 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
     const double* in_p = in_s;
     if constexpr (MT::CLASS) {
       cp_async_wait<0>();
-      mbar_wait(&bar[s], (phase >> s) & 1);
-      phase ^= (1u << s);
+      if constexpr (!S::GDIR) {
+        mbar_wait(&bar[s], (phase >> s) & 1);
+        phase ^= (1u << s);
+      }
       // the previous tile's bulk stores must have read the output buffer
       if (tid == 0) bulk_wait_read0();
     } else if (MODE == 0) {
@@ -644,7 +658,8 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
         const int v = (int)(((a.e0 + w0) % a.n) & 1);  // parity of the tile's first x
         cin_io.v = cout_io.v = v;
       }
-      Op::compute(in_p, geo_s, work, out_c, a.lam, release, pre_out, c_tab, cin_io, cout_io, after_in);
+      const double* geo_p = S::GDIR ? a.geom + (a.e0 + w0) * a.gstride : geo_s;
+      Op::compute(in_p, geo_p, work, out_c, a.lam, release, pre_out, c_tab, cin_io, cout_io, after_in);
       fence_proxy_async();
     } else {
       Op::compute(in_p, geo_s, work, out_t, a.lam, release, pre_out, c_tab);
