@@ -1738,6 +1738,22 @@ std::vector<int> host_slabs(int n) {
     const char* v = getenv("SPHP_HOST_SLABS");
     return v && *v ? atoi(v) : 8;
   }();
+  // tuning override: explicit slab plane counts "1,1,2,8,..." summing to n
+  static const std::vector<int> list = [] {
+    std::vector<int> l;
+    const char* v = getenv("SPHP_HOST_SLAB_LIST");
+    while (v && *v) {
+      l.push_back(atoi(v));
+      v = strchr(v, ',');
+      if (v) ++v;
+    }
+    return l;
+  }();
+  if (!list.empty()) {
+    std::vector<int> zb{0};
+    for (int c : list) zb.push_back(zb.back() + c);
+    if (zb.back() == n) return zb;
+  }
   std::vector<int> zb{0};
   if (mid <= 0 || n < 8) return zb;
   const int head[] = {1, 1, 2}, tail[] = {2, 1, 1};

@@ -38,8 +38,11 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
         step()
     e1.record()
     torch.cuda.synchronize()
-    print(f"slabs={os.environ.get('SPHP_HOST_SLABS', 'default')}: e2e {e0.elapsed_time(e1) / 10:.3f} ms", flush=True)
+    print(f"slabs={os.environ.get('SPHP_HOST_SLAB_LIST', os.environ.get('SPHP_HOST_SLABS', 'default'))}: "
+          f"e2e {e0.elapsed_time(e1) / 10:.3f} ms", flush=True)
 else:
-    for s in ("8", "4", "2", "16", "0"):
-        env = dict(os.environ, SPHP_HOST_SLABS=s)
+    lists = sys.argv[1:] or ["", "1,1,2,4,8,8,8,8,8,4,2,1,1", "1,1,2,4,8,8,8,8,8,8,4,2,1,1"[:0] or
+                             "1,2,4,8,8,8,8,8,8,4,2,1,1,1", "2,2,4,8,8,8,8,8,8,4,2,1,1", "1,1,2,4,6,6,6,6,6,6,6,6,4,2,1,1"]
+    for s in lists:
+        env = dict(os.environ, SPHP_HOST_SLAB_LIST=s)
         subprocess.run([sys.executable, __file__, "child"], env=env)
