@@ -41,6 +41,7 @@ struct QuadHelm {
   // buffer fewer per CTA -> more resident CTAs; the kernel is latency bound)
   static constexpr int OUT_OFF = NE * SW;
   using T = Tab<M, Q>;
+  using X = EO<M, Q>;
 
   template <class R, class W>
   __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
@@ -54,21 +55,16 @@ struct QuadHelm {
       eo_interp<M, Q, 1, 1>(tab, cin + e * M2 + p * M, W0 + e * SW + p * QK);
     }
     __syncthreads();
-    SPHP_FOR_ITEMS(NE * Q, w) {  // p -> i, u and d0
+    SPHP_FOR_ITEMS(NE * Q, w) {  // p -> i, u and d0 (even-odd form)
       const int e = w % NE, j = w / NE;
-      double x[M];
+      double x[M], u[Q], d[Q];
 #pragma unroll
       for (int p = 0; p < M; ++p) x[p] = W0[e * SW + p * QK + j];
+      X::interp_and_deriv(tab, x, u, d);
 #pragma unroll
       for (int i = 0; i < Q; ++i) {
-        double a = 0.0, b = 0.0;
-#pragma unroll
-        for (int p = 0; p < M; ++p) {
-          a = fma(tab[T::B + p * Q + i], x[p], a);
-          b = fma(tab[T::BD + p * Q + i], x[p], b);
-        }
-        W1[e * SW + i * QK + j] = a;
-        W2[e * SW + i * QK + j] = b;
+        W1[e * SW + i * QK + j] = u[i];
+        W2[e * SW + i * QK + j] = d[i];
       }
     }
     __syncthreads();
@@ -88,13 +84,7 @@ struct QuadHelm {
         adet = det;
       }
       double d1v[Q];
-#pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        double acc = 0.0;
-#pragma unroll
-        for (int l = 0; l < Q; ++l) acc = fma(tab[T::D + j * Q + l], u[l], acc);
-        d1v[j] = acc;
-      }
+      X::template deriv<false, false>(tab, u, d1v);
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
         const double d1 = d1v[j];
@@ -117,34 +107,23 @@ struct QuadHelm {
         f1[j] = G01 * d0 + G11 * d1;
         u[j] = lam * wj * u[j];
       }
+      X::template deriv<true, true>(tab, f1, u);  // t = mass + D1^T f1
 #pragma unroll
-      for (int j = 0; j < Q; ++j) {
-        double t = u[j];
-#pragma unroll
-        for (int l = 0; l < Q; ++l) t = fma(tab[T::D + l * Q + j], f1[l], t);
-        W1[base + j] = t;
-      }
+      for (int j = 0; j < Q; ++j) W1[base + j] = u[j];
     }
     __syncthreads();
     release();
     SPHP_FOR_ITEMS(NE * Q, w) {  // i -> p : B t + Bd f0
       const int e = w % NE, j = w / NE;
-      double t[Q], f0[Q];
+      double t[Q], f0[Q], c[M];
 #pragma unroll
       for (int i = 0; i < Q; ++i) {
         t[i] = W1[e * SW + i * QK + j];
         f0[i] = W2[e * SW + i * QK + j];
       }
+      X::project2(tab, t, f0, c);
 #pragma unroll
-      for (int p = 0; p < M; ++p) {
-        double acc = 0.0;
-#pragma unroll
-        for (int i = 0; i < Q; ++i) {
-          acc = fma(tab[T::B + p * Q + i], t[i], acc);
-          acc = fma(tab[T::BD + p * Q + i], f0[i], acc);
-        }
-        W0[e * SW + p * QK + j] = acc;
-      }
+      for (int p = 0; p < M; ++p) W0[e * SW + p * QK + j] = c[p];
     }
     pre_out();
     __syncthreads();
