@@ -16,13 +16,13 @@ assembly algorithms (`AssemblyMap.set_algorithm`):
   "owner"  (default on explicit maps) one kernel gathers x, applies the
            fused elemental operator and writes the local block; a second
            sums every global dof from its contributions in a fixed order;
-  "class"  (default on periodic hex maps, but P = 7) the fused operator
+  "class"  (default on periodic hex maps, every order) the fused operator
            gathers x by entity-class ranges (16-byte cp.async chunks) and
            writes a tile-major class block (interiors straight into y); one
            streaming owner-computes sum reduces it — two launches, no local
            block; falls back to split where its tiles do not fit;
-  "split"  (default at P = 7) scatter kernel -> fused operator on the local
-           block -> owner-computes sum;
+  "split"  scatter kernel -> fused operator on the local block ->
+           owner-computes sum (the fallback of "class");
   "colour" one fused gather -> operator -> scatter-add kernel per colour
            class, colours in a fixed order.
 Several per-order batches on explicit "owner" maps (the variable-order
@@ -166,21 +166,73 @@ def hex_variable_maps(n, orders):
     return ng, out
 
 
-def scatter(amap: AssemblyMap, x, out=None, stream=None):
-    """Global -> local (E, nm), pinned modes -> 0 (assembly.py:150-160)."""
+def _device_input(x, numel, name):
+    """(tensor, was_host): x as a contiguous float64 CUDA tensor of `numel`
+    values.  Host inputs (numpy arrays / CPU tensors, what the reference's
+    assembly.py takes) are copied to the current device; the returned tensor
+    must stay referenced until the launch that reads it has been issued."""
+    was_host = not (torch.is_tensor(x) and x.is_cuda)
+    if was_host:
+        t = torch.as_tensor(np.ascontiguousarray(np.asarray(x, dtype=np.float64)) if not torch.is_tensor(x)
+                            else x.to(torch.float64).contiguous())
+        t = t.to(device=torch.device("cuda", torch.cuda.current_device()))
+    else:
+        t = x if x.dtype == torch.float64 else x.to(torch.float64)
+        t = t.contiguous()
+    if t.numel() != numel:
+        raise AssemblyError(f"{name} has {t.numel()} values, expected {numel}")
+    return t, was_host
+
+
+def _device_output(out, numel, device, shape):
     if out is None:
-        out = torch.empty((amap.num_elements, amap.nmodes), dtype=torch.float64, device=x.device)
-    _lib.check(_lib.lib.sphp_scatter(amap._h, _lib.ptr(x), _lib.ptr(out), _lib.stream_ptr(stream)))
+        return torch.empty(shape, dtype=torch.float64, device=device)
+    if not (torch.is_tensor(out) and out.is_cuda and out.dtype == torch.float64 and out.is_contiguous()
+            and out.numel() == numel and out.device == device):
+        raise AssemblyError(f"out must be a contiguous float64 CUDA tensor of {numel} values on {device}")
     return out
+
+
+def _overlaps(a, b):
+    a0, b0 = a.data_ptr(), b.data_ptr()
+    return a0 < b0 + 8 * b.numel() and b0 < a0 + 8 * a.numel()
+
+
+def scatter(amap: AssemblyMap, x, out=None, stream=None):
+    """Global -> local (E, nm), pinned modes -> 0 (assembly.py:150-160).
+    Host x -> host result; device x -> device result."""
+    xd, host = _device_input(x, amap.num_global, "x")
+    out_d = _device_output(None if host else out, amap.num_elements * amap.nmodes, xd.device,
+                           (amap.num_elements, amap.nmodes))
+    if _overlaps(xd, out_d):
+        raise AssemblyError("x and out must not alias")
+    _lib.check(_lib.lib.sphp_scatter(amap._h, _lib.ptr(xd), _lib.ptr(out_d), _lib.stream_ptr(stream)),
+               AssemblyError)
+    return _to_caller(out_d, out, host)
 
 
 def assemble(amap: AssemblyMap, local, out=None, stream=None):
-    """Local (E, nm) -> global, signed, deterministic (assembly.py:141-147)."""
-    if out is None:
-        out = torch.empty(amap.num_global, dtype=torch.float64, device=local.device)
-    _lib.check(_lib.lib.sphp_assemble(amap._h, _lib.ptr(local.contiguous()), _lib.ptr(out),
-                                      _lib.stream_ptr(stream)))
-    return out
+    """Local (E, nm) -> global, signed, deterministic (assembly.py:141-147).
+    Host local -> host result; device local -> device result."""
+    ld, host = _device_input(local, amap.num_elements * amap.nmodes, "local")
+    out_d = _device_output(None if host else out, amap.num_global, ld.device, (amap.num_global,))
+    if _overlaps(ld, out_d):
+        raise AssemblyError("local and out must not alias")
+    _lib.check(_lib.lib.sphp_assemble(amap._h, _lib.ptr(ld), _lib.ptr(out_d), _lib.stream_ptr(stream)),
+               AssemblyError)
+    return _to_caller(out_d, out, host)
+
+
+def _to_caller(out_d, out, host):
+    """Device result -> what the caller passed: the device tensor, or (host
+    input) a numpy array / the caller's host `out` filled in."""
+    if not host:
+        return out_d
+    res = out_d.cpu().numpy()
+    if out is not None:
+        out[...] = res if not torch.is_tensor(out) else torch.as_tensor(res)
+        return out
+    return res
 
 
 class GlobalHelmholtz:
@@ -227,17 +279,23 @@ class GlobalHelmholtz:
             self._gsys = None
 
     def apply(self, x, out=None, stream=None):
-        if out is None:
-            out = torch.empty(self.num_global, dtype=torch.float64, device=x.device)
+        """y = A^T H A x.  Device x (contiguous float64 CUDA tensor) -> device
+        y; host x (numpy / CPU tensor, the reference's GlobalSystem.apply
+        argument) -> host y.  x and out must not alias (every algorithm
+        reads x while writing y)."""
+        xd, host = _device_input(x, self.num_global, "x")
+        out_d = _device_output(None if host else out, self.num_global, xd.device, (self.num_global,))
+        if _overlaps(xd, out_d):
+            raise AssemblyError("x and out must not alias")
         if self._gsys is not None:
-            _lib.check(_lib.lib.sphp_gsys_apply(self._gsys, _lib.ptr(x), _lib.ptr(out),
+            _lib.check(_lib.lib.sphp_gsys_apply(self._gsys, _lib.ptr(xd), _lib.ptr(out_d),
                                                 _lib.stream_ptr(stream)), AssemblyError)
-            return out
+            return _to_caller(out_d, out, host)
         for k, (coll, amap) in enumerate(self.batches):
-            rc = _lib.lib.sphp_helmholtz_assembled(coll._handle, amap._h, _lib.ptr(x), _lib.ptr(out),
+            rc = _lib.lib.sphp_helmholtz_assembled(coll._handle, amap._h, _lib.ptr(xd), _lib.ptr(out_d),
                                                    1 if k else 0, _lib.stream_ptr(stream))
             _lib.check(rc, AssemblyError)
-        return out
+        return _to_caller(out_d, out, host)
 
     def apply_phases(self, x, out, stream=None):
         """One apply (single batch) with CUDA events between its launches on
@@ -246,6 +304,12 @@ class GlobalHelmholtz:
         if len(self.batches) != 1:
             raise AssemblyError("apply_phases takes one (collection, map) batch")
         coll, amap = self.batches[0]
+        if not (torch.is_tensor(x) and x.is_cuda):
+            raise AssemblyError("apply_phases takes device vectors")
+        x, _ = _device_input(x, self.num_global, "x")
+        out = _device_output(out, self.num_global, x.device, (self.num_global,))
+        if _overlaps(x, out):
+            raise AssemblyError("x and out must not alias")
         ms = (C.c_float * 8)()
         nph = C.c_int()
         _lib.check(_lib.lib.sphp_helmholtz_assembled_phases(coll._handle, amap._h, _lib.ptr(x), _lib.ptr(out),

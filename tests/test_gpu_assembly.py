@@ -294,3 +294,37 @@ def test_class_unaligned_x_falls_back(sp):
     y = op.apply(x_odd).cpu().numpy()
     y_ref = op.apply(x_odd.clone()).cpu().numpy()
     assert y.tobytes() == y_ref.tobytes()
+
+
+def test_assembly_api_host_inputs_and_validation(sp):
+    """The reference's assembly.py takes numpy vectors: host x -> host y,
+    equal to the device apply; wrong sizes, non-float64 CUDA `out` and
+    aliased x/out are rejected before any launch (no sticky CUDA error)."""
+    n, P = 4, 3
+    exp = sp.make_hex(P, P + 2)
+    batch = sp.ElementBatch.structured(exp, n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE, amp=0.03)
+    coll = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC)
+    amap = sp.AssemblyMap.hex_periodic(n, P)
+    op = sp.GlobalHelmholtz([(coll, amap)], amap.num_global)
+    x = np.random.default_rng(5).uniform(-1, 1, amap.num_global)
+    xd = torch.as_tensor(x, device="cuda")
+    y_dev = op.apply(xd).cpu().numpy()
+    y_host = op.apply(x)
+    assert isinstance(y_host, np.ndarray) and y_host.tobytes() == y_dev.tobytes()
+    out = np.empty_like(x)
+    assert op.apply(x, out=out) is out and out.tobytes() == y_dev.tobytes()
+    # scatter / assemble with host inputs equal their device results
+    loc_h = sp.scatter(amap, x)
+    assert isinstance(loc_h, np.ndarray) and loc_h.tobytes() == sp.scatter(amap, xd).cpu().numpy().tobytes()
+    g_h = sp.assemble(amap, loc_h)
+    assert g_h.tobytes() == sp.assemble(amap, torch.as_tensor(loc_h, device="cuda")).cpu().numpy().tobytes()
+    with pytest.raises(sp.AssemblyError):
+        op.apply(xd[:-1])
+    with pytest.raises(sp.AssemblyError):
+        op.apply(xd, out=torch.empty(amap.num_global, dtype=torch.float32, device="cuda"))
+    with pytest.raises(sp.AssemblyError):
+        op.apply(xd, out=xd)
+    with pytest.raises(sp.AssemblyError):
+        sp.assemble(amap, np.zeros(3))
+    # the context is still healthy
+    assert op.apply(xd).cpu().numpy().tobytes() == y_dev.tobytes()
