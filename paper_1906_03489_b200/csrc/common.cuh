@@ -151,8 +151,26 @@ __device__ __forceinline__ void cp_async_wait() {
 // 8 banks apart.  Every producer (geometry kernels) and consumer (the
 // Helmholtz kernels, the Jacobi diagonal) goes through this function.
 // ---------------------------------------------------------------------------
+#ifndef SPHP_KMAJOR_QMASK
+#define SPHP_KMAJOR_QMASK (1 << 9)  // bit Q: hex METRIC components of Q stored k-major
+#endif
+// k-major METRIC points, (k*Q + i)*Q + j: the K-row Helmholtz reads its
+// (i, j) rows one k at a time with lanes on consecutive (i, j), i.e. one
+// coalesced 32-point run per k, which lets its local operator read the
+// geometry straight from global memory (pipeline MODE 7) instead of staging
+// 7 Q^3 doubles per element in shared memory.  Measured (cfg4, local):
+// Q = 9 (P = 7) 2.409 -> 2.298 ms; Q = 5, 7 unchanged; Q = 6, 10 lose their
+// 128-bit row reads (P = 4 0.613 -> 0.635, P = 8 3.26 -> 3.57 ms with the
+// global reads, 3.30 staged); the class operator with global geometry
+// (MODE 6) loses 7-20 % at every Q >= 5 (profiles/r02_kmajor.log)
+__host__ __device__ constexpr bool metric_kmajor(int Q) { return Q < 32 && ((SPHP_KMAJOR_QMASK >> Q) & 1); }
 __host__ __device__ __forceinline__ int metric_slot(int dim, int Q, int pt) {
-  if (dim != 3 || Q != 8) return pt;
+  if (dim != 3) return pt;
+  if (metric_kmajor(Q)) {
+    const int ij = pt / Q, k = pt - ij * Q;
+    return k * Q * Q + ij;
+  }
+  if (Q != 8) return pt;
   const int i = pt >> 6, j = (pt >> 3) & 7, k = pt & 7;
   return (j << 6) | (i << 3) | k;
 }

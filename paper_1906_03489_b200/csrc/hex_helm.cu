@@ -17,6 +17,13 @@ SPHP_DECLARE_TABLE_BANK(hex_helm2)
 
 namespace sphp {
 
+// Op::GDIR_LOCAL when the plan declares it: its local operator reads the
+// geometry from global memory (pipeline MODE 7)
+template <class Op>
+constexpr auto gdir_local_impl(int) -> decltype(Op::GDIR_LOCAL, bool()) { return Op::GDIR_LOCAL; }
+template <class Op>
+constexpr bool gdir_local_impl(...) { return false; }
+
 // tile-shape variants: (input stages, shared-memory budget per CTA)
 template <int M, int Q, int GK, int NSTP, int BUDGET>
 static cudaError_t helm_variant(const OpArgs& oa, cudaStream_t s) {
@@ -24,6 +31,11 @@ static cudaError_t helm_variant(const OpArgs& oa, cudaStream_t s) {
   constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(NSTP), Q * Q, BUDGET);
   constexpr int NT = choose_nt(NE, Q * Q);
   using Op = HexHelm<M, Q, GK, NE, NT, NSTP>;
+  if constexpr (gdir_local_impl<Op>(0)) {
+    // full tiles only (the compute reads every element of a tile)
+    if (oa.mode == AsmMode::LOCAL && oa.E % NE == 0)
+      return launch_pipe<Op, 7>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
+  }
   return launch_mode<Op>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
 }
 
@@ -49,9 +61,12 @@ static int helm_variant_env() {
 // PERIODIC_CLASS (pipeline MODE 5): tiles of NE consecutive elements of an
 // x-row (NE must divide n)
 // MODE 6 (geometry from global memory, L2-prefetched) at P = 2 / METRIC
+#ifndef SPHP_CLASS_GDIR
+#define SPHP_CLASS_GDIR 0  // tuning: 1 = class mode of k-major METRIC orders reads global geometry too
+#endif
 template <int M, int Q, int GK>
 constexpr int class_mode() {
-  return (GK == SPHP_GEOM_METRIC && M == 3 && Q == 4) ? 6 : 5;
+  return (GK == SPHP_GEOM_METRIC && ((M == 3 && Q == 4) || (SPHP_CLASS_GDIR && metric_kmajor(Q)))) ? 6 : 5;
 }
 template <int M, int Q, int GK, int NE>
 constexpr size_t class_smem() {

@@ -14,6 +14,9 @@
 #ifndef SPHP_Q7_EFAST
 #define SPHP_Q7_EFAST 1  // tuning: 0 = rotated j-pencils at Q = 7 instead
 #endif
+#ifndef SPHP_GDIR_LOCAL
+#define SPHP_GDIR_LOCAL 1  // tuning: 0 = k-major orders still stage their geometry (MODE 0)
+#endif
 #ifndef SPHP_SI_Q
 #define SPHP_SI_Q 0  // tuning: another Q with the padded dense plane pitch
 #endif
@@ -263,6 +266,10 @@ struct HexHelmEO {
   // and slower at Q = 10 (P=8 3.34 -> 3.66 ms: the rotation selects cost
   // more than the conflicts): natural order there.
   static constexpr bool EFAST = (Q == 7 && NE == 2 && SPHP_Q7_EFAST);
+  // k-major METRIC points (metric_slot): the local operator then reads the
+  // geometry from global memory (pipeline MODE 7) instead of staging it
+  static constexpr bool KMAJ = GK == SPHP_GEOM_METRIC && metric_kmajor(Q);
+  static constexpr bool GDIR_LOCAL = KMAJ && SPHP_GDIR_LOCAL;
   static constexpr int JROT = (Q == 7 && !EFAST) ? 1 : 0;
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
@@ -330,37 +337,48 @@ struct HexHelmEO {
       load_row<Q>(W0 + row, u);
       X::template deriv<false, false>(tab, u, d2);
       if constexpr (GK == SPHP_GEOM_METRIC) {
-        const double* gr = geo + e * GEO + ij * Q;
+        // the (i, j) row of metric component c: contiguous in point order, or
+        // one value per k plane (k-major, metric_slot): lanes on consecutive
+        // (i, j) then read consecutive doubles (coalesced from global memory)
+        const double* gr = geo + e * GEO + (KMAJ ? ij : ij * Q);
+        auto geo_row = [&](int c, double* x) {
+          if constexpr (KMAJ) {
+#pragma unroll
+            for (int k = 0; k < Q; ++k) x[k] = gr[c * CS + k * Q * Q];
+          } else {
+            load_row<Q>(gr + c * CS, x);
+          }
+        };
         load_row<Q>(W2 + row2, d);
-        load_row<Q>(gr + 0 * CS, g);
+        geo_row(0, g);
 #pragma unroll
         for (int k = 0; k < Q; ++k) f0[k] = g[k] * d[k];
-        load_row<Q>(gr + 1 * CS, g);
+        geo_row(1, g);
 #pragma unroll
         for (int k = 0; k < Q; ++k) f1[k] = g[k] * d[k];
         double h[Q];
         load_row<Q>(W1 + row, h);
 #pragma unroll
         for (int k = 0; k < Q; ++k) f0[k] = fma(g[k], h[k], f0[k]);
-        load_row<Q>(gr + 2 * CS, g);
+        geo_row(2, g);
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
           f2[k] = g[k] * d[k];
           f0[k] = fma(g[k], d2[k], f0[k]);
         }
-        load_row<Q>(gr + 3 * CS, g);
+        geo_row(3, g);
 #pragma unroll
         for (int k = 0; k < Q; ++k) f1[k] = fma(g[k], h[k], f1[k]);
-        load_row<Q>(gr + 4 * CS, g);
+        geo_row(4, g);
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
           f1[k] = fma(g[k], d2[k], f1[k]);
           f2[k] = fma(g[k], h[k], f2[k]);
         }
-        load_row<Q>(gr + 5 * CS, g);
+        geo_row(5, g);
 #pragma unroll
         for (int k = 0; k < Q; ++k) f2[k] = fma(g[k], d2[k], f2[k]);
-        load_row<Q>(gr + 6 * CS, g);
+        geo_row(6, g);
 #pragma unroll
         for (int k = 0; k < Q; ++k) u[k] = lam * g[k] * u[k];
       } else {

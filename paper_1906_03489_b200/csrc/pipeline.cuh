@@ -129,6 +129,7 @@ struct DevArgs {
 // MODE 3: periodic hex, all elements in order: gather in, local block out.
 // MODE 4: explicit map, all elements in order: gather in, local block out.
 // MODE 6: MODE 5 with the geometry read from global memory (L2 prefetch).
+// MODE 7: MODE 0 with the geometry read from global memory (L2 prefetch).
 // MODE 5: periodic hex, all elements in order, by entity class: the tile's
 //         27 class ranges of x arrive by TMA bulk copies into a class-
 //         staged input, results leave by 27 bulk stores into the class-major
@@ -137,13 +138,17 @@ struct DevArgs {
 // Gathering modes need IN == OUT == nmodes.
 template <int MODE>
 struct ModeTraits {
-  static constexpr bool GATHER = MODE != 0;
+  static constexpr bool LOCAL = MODE == 0 || MODE == 7;
+  static constexpr bool GATHER = !LOCAL;
   static constexpr bool PERIODIC = MODE == 1 || MODE == 3;
   static constexpr bool EXPLICIT = MODE == 2 || MODE == 4;
   static constexpr bool SCATTER = MODE == 1 || MODE == 2;
-  static constexpr bool CONTIG = MODE == 0 || MODE >= 3;
+  static constexpr bool CONTIG = LOCAL || MODE >= 3;
   static constexpr bool CLASS = MODE == 5 || MODE == 6;
-  static constexpr bool GDIR = MODE == 6;  // class, geometry read from global memory
+  // geometry read from global memory in the compute (L2-prefetched one tile
+  // ahead) instead of staged in shared memory: MODE 6 (class), MODE 7 (local;
+  // full tiles only, the launcher takes MODE 0 for a partial last tile)
+  static constexpr bool GDIR = MODE == 6 || MODE == 7;
 };
 // ---------------------------------------------------------------------------
 // preferred number of input stages: Op::NSTP when the Op declares it, else 1
@@ -193,7 +198,7 @@ struct Scaffold {
   // global start is odd so both ends share 16-byte alignment (an Op staging
   // it in its work area, OUT_OFF, leaves at least one spare double there)
 #ifndef SPHP_NO_BULK_OUT
-  static constexpr bool BULK_OUT = MODE == 0;
+  static constexpr bool BULK_OUT = ModeTraits<MODE>::LOCAL;
 #else
   static constexpr bool BULK_OUT = false;  // tuning build: plain store loop
 #endif
@@ -202,7 +207,7 @@ struct Scaffold {
   // assembled-mode integer tables (in doubles): per stage ids + entities,
   // current-tile copies, and the per-mode code table
   static constexpr int ENT = ModeTraits<MODE>::PERIODIC ? 27 : 0;
-  static constexpr int ITAB = (MODE == 0 || CLS) ? 0 : even_up(NE * (2 + ENT)) / 2 + 1;
+  static constexpr int ITAB = (ModeTraits<MODE>::LOCAL || CLS) ? 0 : even_up(NE * (2 + ENT)) / 2 + 1;
   // MODE 5 int tables: per-mode input / output positions (2 * IN), per
   // class slot base, Z offset, geometry and first 16-byte chunk (5 * 27 + 1)
   // (PV tile-parity variants of the positions and of the chunk prefix)
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
   };
 
   // schedule slot -> tile (MODE 0 may walk the tiles in reverse)
-  auto phys = [&](int ts) { return (MODE == 0 && a.reverse) ? ntiles - 1 - ts : ts; };
+  auto phys = [&](int ts) { return (MT::LOCAL && a.reverse) ? ntiles - 1 - ts : ts; };
   // thread 0: TMA bulk copies of the tile of schedule slot ts into stage s
   auto issue_local = [&](int ts, int s) {
     if (ts >= ntiles) return;
@@ -381,6 +386,12 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
     if (!in_window(t, a0, a1, off)) return;  // synchronous at consumption
     uint32_t bytes_in = (uint32_t)(a1 - a0);
     uint32_t bytes_g = (uint32_t)(sizeof(double) * r * GEO);
+    if constexpr (S::GDIR) {
+      mbar_expect_tx(&bar[s], bytes_in);
+      bulk_g2s(in_s, reinterpret_cast<const char*>(a.in) + a0, bytes_in, &bar[s]);
+      if (GEO > 0) bulk_prefetch_l2(a.geom + w0 * a.gstride, bytes_g);
+      return;
+    }
     mbar_expect_tx(&bar[s], bytes_in + bytes_g);
     bulk_g2s(in_s, reinterpret_cast<const char*>(a.in) + a0, bytes_in, &bar[s]);
     if (GEO > 0) {
@@ -554,7 +565,7 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
   if (MT::CLASS) {
     issue_x(blockIdx.x);
     if (tid == 0) issue_geo(blockIdx.x, 0);
-  } else if (MODE == 0) {
+  } else if (MT::LOCAL) {
     if (tid == 0) {
       issue_local(blockIdx.x, 0);
       if (NST == 2) issue_local(blockIdx.x + G, 1);
@@ -583,7 +594,7 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
       }
       // the previous tile's bulk stores must have read the output buffer
       if (tid == 0) bulk_wait_read0();
-    } else if (MODE == 0) {
+    } else if (MT::LOCAL) {
       int64_t a0, a1;
       int off;
       if (in_window(t, a0, a1, off)) {
@@ -592,7 +603,7 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
         in_p = in_s + off;
       } else {
         for (int i = tid; i < r * IN; i += NT) in_s[i] = a.in[w0 * IN + i];
-        if constexpr (GEO > 0) {
+        if constexpr (GEO > 0 && !S::GDIR) {
           for (int i = tid; i < r * GEO; i += NT) {
             int e = i / GEO, c = i - e * GEO;
             geo_s[e * GEO_S + c] = a.geom[(w0 + e) * a.gstride + a.goff + c];
@@ -601,7 +612,7 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
       }
       // zero the unused tail of a partial tile (its results are discarded)
       for (int i = r * IN + tid; i < NE * IN; i += NT) in_s[(in_p - in_s) + i] = 0.0;
-      if (GEO > 0)
+      if (GEO > 0 && !S::GDIR)
         for (int i = r * GEO_S + tid; i < NE * GEO_S; i += NT) geo_s[i] = 0.0;
       // the previous tile's bulk store must have read the output buffer
       if (S::BULK_OUT && tid == 0) bulk_wait_read0();
@@ -634,7 +645,7 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
           fence_proxy_async();
           issue_geo(ts + NST * G, s);
         }
-      } else if (MODE == 0) {
+      } else if (MT::LOCAL) {
         if (tid == 0) {
           fence_proxy_async();
           issue_local(ts + NST * G, s);
@@ -662,7 +673,8 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
       Op::compute(in_p, geo_p, work, out_c, a.lam, release, pre_out, c_tab, cin_io, cout_io, after_in);
       fence_proxy_async();
     } else {
-      Op::compute(in_p, geo_s, work, out_t, a.lam, release, pre_out, c_tab);
+      const double* geo_p = S::GDIR ? a.geom + w0 * a.gstride : geo_s;
+      Op::compute(in_p, geo_p, work, out_t, a.lam, release, pre_out, c_tab);
       if (bulk_out) fence_proxy_async();  // this thread's buffer writes -> async proxy
     }
     __syncthreads();
@@ -757,7 +769,7 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
       __syncthreads();
     }
   }
-  if (MODE != 0) cp_async_wait<0>();
+  if (!MT::LOCAL) cp_async_wait<0>();
   if (S::BULK_OUT && tid == 0) bulk_wait0();
   if (MT::CLASS && tid == 0) bulk_wait0();
 }
