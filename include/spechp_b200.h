@@ -97,6 +97,13 @@ int sphp_abi_version(void);
 const char* sphp_last_error(void);
 /* number of SMs of the current device, 0 if none (used by the autotuner)   */
 int sphp_device_sm_count(void);
+/* stage plan of the fused hex Helmholtz for nmodes = M, npoints = Q per
+ * direction: 0 K-row, 1 J-pencil, 2 skewed Q = 4, 3 i-column;
+ * local_launch = 1: the plan of block-in / block-out applies (sphp_apply),
+ * which at some orders differs from the one every assembled apply uses (all
+ * assembly algorithms of a map return bitwise the same vector).  Results of
+ * two plans agree to rounding, not bitwise.  -1: no fast kernel.            */
+int sphp_hex_helmholtz_plan(int M, int Q, int local_launch);
 
 /* ---- reference elements: StdExpansion tables ----------------------------
  * replaces stdregions.StdExpansion(shape, basis_keys) (stdregions.py:70-240)

@@ -163,9 +163,32 @@ __device__ __forceinline__ void cp_async_wait() {
 // 128-bit row reads (P = 4 0.613 -> 0.635, P = 8 3.26 -> 3.57 ms with the
 // global reads, 3.30 staged); the class operator with global geometry
 // (MODE 6) loses 7-20 % at every Q >= 5 (profiles/r02_kmajor.log)
-__host__ __device__ constexpr bool metric_kmajor(int Q) { return Q < 32 && ((SPHP_KMAJOR_QMASK >> Q) & 1); }
+// Orders whose fused hex Helmholtz runs the i-column plan (HexHelmCol,
+// hex_ops.cuh): bit Q.  That plan reads the metric in natural point order.
+// Measured (cfg4 64^3, local / class-assembled ms; profiles/r02_col.log):
+// Q = 5 (P = 3) 0.399 -> 0.315 / 0.467 -> 0.388, Q = 7 (P = 5) 1.088 -> 1.045
+// / 1.294 -> 1.204; Q = 6 (P = 4) 0.612 -> 0.591 local but 0.698 -> 0.749
+// assembled (its larger work area drops the class tile to two CTAs per SM):
+// local only there (SPHP_COL_LOCAL_QMASK; Q = 6 keeps natural point order
+// in both plans).  One element per tile at Q >= 8 leaves the column stage
+// too few threads: the row / pencil plans stay (P = 6..8: 1.55 vs 1.50,
+// 2.79 vs 2.25, 3.56 vs 3.27 ms).
+#ifndef SPHP_COL_QMASK
+#define SPHP_COL_QMASK ((1 << 5) | (1 << 7))
+#endif
+#ifndef SPHP_COL_LOCAL_QMASK
+#define SPHP_COL_LOCAL_QMASK (1 << 6)
+#endif
+__host__ __device__ constexpr bool col_plan(int Q) { return Q < 32 && ((SPHP_COL_QMASK >> Q) & 1); }
+// local (block in / block out) launches only; needs natural metric order
+__host__ __device__ constexpr bool col_plan_local(int Q) {
+  return col_plan(Q) || (Q < 32 && Q != 8 && ((SPHP_COL_LOCAL_QMASK >> Q) & 1) && !((SPHP_KMAJOR_QMASK >> Q) & 1));
+}
+__host__ __device__ constexpr bool metric_kmajor(int Q) {
+  return Q < 32 && ((SPHP_KMAJOR_QMASK >> Q) & 1) && !col_plan(Q);
+}
 __host__ __device__ __forceinline__ int metric_slot(int dim, int Q, int pt) {
-  if (dim != 3) return pt;
+  if (dim != 3 || col_plan(Q)) return pt;
   if (metric_kmajor(Q)) {
     const int ij = pt / Q, k = pt - ij * Q;
     return k * Q * Q + ij;

@@ -25,10 +25,46 @@ template <class Op>
 constexpr bool gdir_local_impl(...) { return false; }
 
 // tile-shape variants: (input stages, shared-memory budget per CTA)
+constexpr int pow2_floor(int x) { return x >= 8 ? 8 : (x >= 4 ? 4 : (x >= 2 ? 2 : 1)); }
+// the i-column plan runs element-fastest lanes over NE = 1, 2, 4 or 8
+// elements; SPHP_COL_NE_<M> pins the local tile of one order (tuning)
+template <int M, int Q, int GK, int NSTP, int BUDGET, bool COL>
+constexpr int helm_ne() {
+  using Probe = HexHelmSel<M, Q, GK, 1, 32, NSTP, COL>;
+  constexpr int ne = choose_ne(8 * per_elem_doubles<Probe>(NSTP), Q * Q, BUDGET);
+  return COL ? pow2_floor(ne) : ne;
+}
+template <int M, int Q, int GK, int NSTP, int NE>
+static cudaError_t helm_variant_ne(const OpArgs& oa, cudaStream_t s) {
+  constexpr int NT = choose_nt(NE, Q * Q);
+  if (oa.mode == AsmMode::LOCAL && !oa.asm_plan) {
+    using Op = HexHelmLocal<M, Q, GK, NE, NT, NSTP>;
+    if constexpr (Scaffold<Op, 0>::SMEM_BYTES > 227 * 1024)
+      return cudaErrorNotSupported;
+    else
+      return launch_pipe<Op, 0>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
+  }
+  using Op = HexHelm<M, Q, GK, NE, NT, NSTP>;
+  if constexpr (Scaffold<Op, 3>::SMEM_BYTES > 227 * 1024) {
+    return cudaErrorNotSupported;
+  } else {
+    return launch_mode<Op>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
+  }
+}
+// local launches of an order whose local plan differs from its general one
+template <int M, int Q, int GK, int NSTP, int BUDGET>
+static cudaError_t helm_variant_local(const OpArgs& oa, cudaStream_t s) {
+  constexpr int NE = helm_ne<M, Q, GK, NSTP, BUDGET, true>();
+  constexpr int NT = choose_nt(NE, Q * Q);
+  using Op = HexHelmLocal<M, Q, GK, NE, NT, NSTP>;
+  return launch_pipe<Op, 0>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
+}
 template <int M, int Q, int GK, int NSTP, int BUDGET>
 static cudaError_t helm_variant(const OpArgs& oa, cudaStream_t s) {
-  using Probe = HexHelm<M, Q, GK, 1, 32, NSTP>;
-  constexpr int NE = choose_ne(8 * per_elem_doubles<Probe>(NSTP), Q * Q, BUDGET);
+  if constexpr (col_plan_local(Q) != col_plan(Q)) {
+    if (oa.mode == AsmMode::LOCAL && !oa.asm_plan) return helm_variant_local<M, Q, GK, NSTP, BUDGET>(oa, s);
+  }
+  constexpr int NE = helm_ne<M, Q, GK, NSTP, BUDGET, col_plan(Q)>();
   constexpr int NT = choose_nt(NE, Q * Q);
   using Op = HexHelm<M, Q, GK, NE, NT, NSTP>;
   if constexpr (gdir_local_impl<Op>(0)) {
@@ -66,7 +102,9 @@ static int helm_variant_env() {
 #endif
 template <int M, int Q, int GK>
 constexpr int class_mode() {
-  return (GK == SPHP_GEOM_METRIC && ((M == 3 && Q == 4) || (SPHP_CLASS_GDIR && metric_kmajor(Q)))) ? 6 : 5;
+  return (GK == SPHP_GEOM_METRIC && !col_plan(Q) && ((M == 3 && Q == 4) || (SPHP_CLASS_GDIR && metric_kmajor(Q))))
+             ? 6
+             : 5;
 }
 template <int M, int Q, int GK, int NE>
 constexpr size_t class_smem() {
@@ -91,7 +129,7 @@ constexpr int class_ne() {
   // measured (tools/time_phases.py, cfg4 64^3, METRIC, Q = P + 2): P = 2..8
   // -> 4, 8, 4, 2, 1, 1, 1 (residency alone picks 2 at P = 3 and 1 at P = 5,
   // 9-10 % slower there; 8 vs 4 at P = 3: -1.4 %)
-  if (GK == SPHP_GEOM_METRIC && Q == M + 1) return M == 4 ? 8 : (M <= 5 ? 4 : (M == 6 ? 2 : 1));
+  if (GK == SPHP_GEOM_METRIC && Q == M + 1) return (M == 4 && !col_plan(Q)) ? 8 : (M <= 5 ? 4 : (M == 6 ? 2 : 1));
   int best = 1, score = class_resident<M, Q, GK, 1>();
   if (class_resident<M, Q, GK, 2>() > score) best = 2, score = class_resident<M, Q, GK, 2>();
   if (class_resident<M, Q, GK, 4>() > score) best = 4, score = class_resident<M, Q, GK, 4>();
@@ -100,9 +138,27 @@ constexpr int class_ne() {
 #endif
 }
 
+template <int M, int Q, int GK, int NE>
+static cudaError_t helm_class_ne(const OpArgs& oa, cudaStream_t s);
 template <int M, int Q, int GK>
 static cudaError_t helm_class(const OpArgs& oa, cudaStream_t s) {
-  constexpr int NE = class_ne<M, Q, GK>();
+#ifdef SPHP_TUNING
+  static const int ne_env = [] {
+    const char* e = getenv("SPHP_CLASS_NE_ENV");
+    return e ? atoi(e) : 0;
+  }();
+  switch (ne_env) {
+    case 1: return helm_class_ne<M, Q, GK, 1>(oa, s);
+    case 2: return helm_class_ne<M, Q, GK, 2>(oa, s);
+    case 4: return helm_class_ne<M, Q, GK, 4>(oa, s);
+    case 8: return helm_class_ne<M, Q, GK, 8>(oa, s);
+    default: break;
+  }
+#endif
+  return helm_class_ne<M, Q, GK, class_ne<M, Q, GK>()>(oa, s);
+}
+template <int M, int Q, int GK, int NE>
+static cudaError_t helm_class_ne(const OpArgs& oa, cudaStream_t s) {
   if constexpr (M < 3 || class_smem<M, Q, GK, NE>() > 227 * 1024) {
     return cudaErrorNotSupported;  // not even a two-element tile fits: split
   } else {
@@ -125,6 +181,10 @@ static cudaError_t helm_go(const OpArgs& oa, cudaStream_t s) {
       case 2: return helm_variant<M, Q, GK, 1, 55 * 1024>(oa, s);
       case 3: return helm_variant<M, Q, GK, 2, 74 * 1024>(oa, s);
       case 4: return helm_variant<M, Q, GK, 1, 110 * 1024>(oa, s);
+      case 11: return helm_variant_ne<M, Q, GK, 1, 1>(oa, s);
+      case 12: return helm_variant_ne<M, Q, GK, 1, 2>(oa, s);
+      case 14: return helm_variant_ne<M, Q, GK, 1, 4>(oa, s);
+      case 18: return helm_variant_ne<M, Q, GK, 1, 8>(oa, s);
       default: break;
     }
 #endif

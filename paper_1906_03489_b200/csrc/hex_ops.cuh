@@ -234,6 +234,7 @@ template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
 struct HexHelmEO {
   static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
   static constexpr int NSTP = NSTP_;
+  static constexpr bool GEO_HOOK = true;  // compute() calls geo_ready() before its first geometry read
   static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
   static constexpr int IN = M3, OUT = M3;
   static constexpr int CS = pt_stride(Q3);
@@ -274,11 +275,11 @@ struct HexHelmEO {
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
 
-  template <class R, class W, class IO = BlockIO, class H = NoHook>
+  template <class R, class W, class IO = BlockIO, class H = NoHook, class GH = NoHook>
   __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
                                  double* __restrict__ work, double* __restrict__ out, double lam,
                                  R release, W pre_out, const double* tab, IO io = IO(),
-                                 IO oio = IO(), H after_in = H()) {
+                                 IO oio = IO(), H after_in = H(), GH geo_ready = GH()) {
     double* W0 = work;
     double* W1 = work + NE * SE;
     double* W2 = work + 2 * NE * SE;
@@ -328,6 +329,7 @@ struct HexHelmEO {
       Rot<Q>::template store<Q>(W1 + e * SE + i * SI + k, tau, r);
     }
     __syncthreads();
+    geo_ready();  // the staged geometry is first read here (pipeline: GEO_HOOK)
     // S5: k rows
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       int e = w / (Q * Q), ij = w - e * (Q * Q), i = ij / Q, j = ij - i * Q;
@@ -467,6 +469,7 @@ template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
 struct HexHelmJEO {
   static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
   static constexpr int NSTP = NSTP_;
+  static constexpr bool GEO_HOOK = true;  // compute() calls geo_ready() before its first geometry read
   static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
   static constexpr int IN = M3, OUT = M3;
   static constexpr int CS = pt_stride(Q3);
@@ -478,11 +481,11 @@ struct HexHelmJEO {
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
 
-  template <class R, class W, class IO = BlockIO, class H = NoHook>
+  template <class R, class W, class IO = BlockIO, class H = NoHook, class GH = NoHook>
   __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
                                  double* __restrict__ work, double* __restrict__ out, double lam,
                                  R release, W pre_out, const double* tab, IO io = IO(),
-                                 IO oio = IO(), H after_in = H()) {
+                                 IO oio = IO(), H after_in = H(), GH geo_ready = GH()) {
     double* W0 = work;
     double* W1 = work + NE * SW;
     double* W2 = work + 2 * NE * SW;
@@ -523,6 +526,7 @@ struct HexHelmJEO {
       st_pencil<Q, 1>(W1 + e * SW + ij * QK, r);
     }
     __syncthreads();
+    geo_ready();  // the staged geometry is first read here (pipeline: GEO_HOOK)
     SPHP_FOR_ITEMS(NE * Q * Q, w) {  // S5 pencil along j: pointwise, t = mass + D1^T f1
       int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
       const int base = e * SW + i * Q * QK + k;
@@ -652,6 +656,7 @@ struct HexHelmQ4 {
   static_assert(Q_ == 4 && M_ <= 4, "skewed layout is for Q = 4");
   static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
   static constexpr int NSTP = NSTP_;
+  static constexpr bool GEO_HOOK = true;  // compute() calls geo_ready() before its first geometry read
   static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
   static constexpr int IN = M3, OUT = M3;
   static constexpr int CS = pt_stride(Q3);
@@ -662,11 +667,11 @@ struct HexHelmQ4 {
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
 
-  template <class R, class W, class IO = BlockIO, class H = NoHook>
+  template <class R, class W, class IO = BlockIO, class H = NoHook, class GH = NoHook>
   __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
                                  double* __restrict__ work, double* __restrict__ out, double lam,
                                  R release, W pre_out, const double* tab, IO io = IO(),
-                                 IO oio = IO(), H after_in = H()) {
+                                 IO oio = IO(), H after_in = H(), GH geo_ready = GH()) {
     double* W0 = work;
     double* W1 = work + NE * ES;
     double* W2 = work + 2 * NE * ES;
@@ -737,6 +742,7 @@ struct HexHelmQ4 {
       }
     }
     __syncthreads();
+    geo_ready();  // the staged geometry is first read here (pipeline: GEO_HOOK)
     // S5: pointwise on i-pencils
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
       const int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
@@ -867,13 +873,253 @@ struct HexHelmQ4 {
   }
 };
 
-// variant selection: skewed Q = 4 layout, j-pencil plan at Q % 4 == 0,
-// k-row plan otherwise
+// ===========================================================================
+// Fused Helmholtz, i-column plan (HexHelmCol): the direction i never goes
+// through shared memory.  Sum factorisation runs k, then j, on the small
+// mode-sized tensors; the pointwise stage owns one (j, k) column of the
+// element, interpolates u and the three reference derivatives along i in
+// registers (dB = D B exactly, the modes being polynomials of degree < Q),
+// applies the metric and projects its results back along i before they
+// leave the thread.  No dense Q^3 work tensor exists:
+//   S1 r->k   c[p,q,:]  -> T1 = B_k c, T1d = dB_k c           items (p, q)   A tensors [p][q][k]
+//   S2 q->j   T1, T1d   -> T2 = B_j T1, T2e = dB_j T1, T2f = B_j T1d
+//                                                             items (p, k)   B tensors [p][j][k]
+//   S5 i      u = B_i T2, d0 = dB_i T2, d1 = B_i T2e, d2 = B_i T2f; f = G grad u;
+//             U0 = B_i^T(lam wJ u) + dB_i^T f0, U1 = B_i^T f1, U2 = B_i^T f2
+//                                                             items (j, k)   in place in the B tensors
+//   B1 j->q   V0 = B_j^T U0 + dB_j^T U1, V1 = B_j^T U2         items (p, k)   A tensors
+//   B2 k->r   y = B_k^T V0 + dB_k^T V1                         items (p, q)
+// Shared-memory traffic per element: 2 M^3 + 8 M^2 Q + 12 M Q^2 + 7 Q^3
+// doubles against 2 M^3 + 4 M^2 Q + 4 M Q^2 + 22 Q^3 of the K-row plan
+// (P = 3: -21 %, P = 5: -18 %, P = 8: -15 %), five barriers instead of nine,
+// and every column access of the pointwise stage (work tensors and the
+// staged metric in natural point order) is conflict free at any Q.  Lanes
+// run element-fastest over tiles of NE = 2, 4, 8 elements whose strides are
+// 16 / NE (mod 16) doubles apart: a half-warp is then 16 / NE consecutive
+// items of NE elements, so pitches only need the right residue mod 16 / NE
+// (tools/layout_search_col.py).  More FP64 work (+25 %: four interpolations
+// and three projections per column); the kernels are bound by the
+// shared-memory pipe and HBM, not FP64.
+// ===========================================================================
+struct ColLay {
+  int RA, PA, SEA;  // A tensors: row pitch (k rows), p pitch, element stride
+  int PB, SEB;      // B tensors: p pitch (rows of Q contiguous), element stride
+  int GS;           // staged METRIC stride per element
+  int O2, O5;       // lane orders of S2 / B1 and S5: 0 element-major, 1 element-fastest, 2 (O2) p-fastest
+};
+__host__ __device__ constexpr int with_res16(int lo, int res) {
+  int v = lo;
+  while (((v % 16) + 16) % 16 != res) ++v;
+  return v;
+}
+__host__ __device__ constexpr bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+__host__ __device__ constexpr ColLay col_layout(int M, int Q, int NE, int GEO) {
+  ColLay L{};
+  const bool ef = NE > 1 && NE <= 8 && is_pow2(NE);
+  const int g = ef ? 16 / NE : 16;
+  L.O2 = L.O5 = ef ? 1 : 0;
+  L.RA = Q;
+  // (p, k) -> p * PA + k and p * PB + k stay consecutive mod g
+  L.PA = M * L.RA;
+  while (L.PA % g != Q % g) ++L.PA;
+  L.PB = Q * Q;
+  while (L.PB % g != Q % g) ++L.PB;
+  L.SEA = ef ? with_res16(2 * M * L.PA, g) : 2 * M * L.PA;
+  L.SEB = ef ? with_res16(3 * M * L.PB, g) : 3 * M * L.PB;
+  L.GS = (ef && GEO > 16) ? with_res16(GEO, g) : GEO;
+  // searched (tools/layout_search_col.py)
+  if (M == 4 && Q == 5 && NE == 4) L.PA = 20, L.SEA = 164, L.PB = 25, L.SEB = 300;
+  if (M == 4 && Q == 5 && NE == 8) L.PA = 20, L.SEA = 162, L.PB = 25, L.SEB = 302;
+  if (M == 6 && Q == 7 && NE == 2) L.PA = 47, L.SEA = 568, L.PB = 55, L.SEB = 1000;
+  if (M == 8 && Q == 9 && NE == 1) L.RA = 10, L.PA = 89, L.SEA = 1424, L.PB = 89, L.SEB = 2136;
+  if (M == 9 && Q == 10 && NE == 1) L.RA = 10, L.PA = 105, L.SEA = 1890, L.PB = 105, L.SEB = 2835, L.O2 = 2;
+  if (M == 5 && Q == 6 && NE == 4) L.RA = 7, L.PA = 35, L.SEA = 356, L.PB = 38, L.SEB = 572;
+  if (M == 5 && Q == 6 && NE == 2) L.RA = 9, L.PA = 45, L.SEA = 465, L.PB = 45, L.SEB = 678, L.O2 = 2, L.O5 = 0;
+  return L;
+}
+
 template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
-using HexHelm = typename std::conditional<
-    (Q_ == 4), HexHelmQ4<M_, Q_, GK, NE_, NT_, NSTP_>,
-    typename std::conditional<(Q_ % 4 == 0), HexHelmJEO<M_, Q_, GK, NE_, NT_, NSTP_>,
-                              HexHelmEO<M_, Q_, GK, NE_, NT_, NSTP_>>::type>::type;
+struct HexHelmCol {
+  static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
+  static constexpr int NSTP = NSTP_;
+  static constexpr bool GEO_HOOK = true;  // compute() calls geo_ready() before its first geometry read
+  static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
+  static constexpr int IN = M3, OUT = M3;
+  static constexpr int CS = pt_stride(Q3);
+  static constexpr int GEO = (GK == SPHP_GEOM_METRIC) ? 7 * CS : 10;
+  static constexpr ColLay L = col_layout(M, Q, NE, GEO);
+  static constexpr int RA = L.RA, PA = L.PA, SEA = L.SEA, PB = L.PB, SEB = L.SEB;
+  static constexpr int TA = M * PA, TB = M * PB;  // tensor strides inside an element's region
+  static constexpr int GEO_S = L.GS;
+  static_assert(RA >= Q && PA >= M * RA && SEA >= 2 * TA && PB >= Q * Q && SEB >= 3 * TB, "tensors overlap");
+  static_assert(GEO_S % 2 == 0 && GEO_S >= GEO, "staged geometry stride");
+  static constexpr int WORK = SEA + SEB;
+  static constexpr int OUT_OFF = NE * SEA;  // B2 writes the block into the B region (free after B1)
+  static_assert(NE * SEB >= NE * M3 + 4, "output block does not fit the B region");
+  using T = Tab<M, Q>;
+  using X = EO<M, Q>;
+
+  // item w of a stage over (e, a, b), b in [0, NB): element-major (b
+  // fastest), element-fastest, or element-major with a fastest
+  template <int ORDER, int NA, int NB>
+  __device__ static __forceinline__ void item(int w, int& e, int& a, int& b) {
+    if constexpr (ORDER == 1) {
+      e = w % NE;
+      const int ab = w / NE;
+      a = ab / NB, b = ab - a * NB;
+    } else if constexpr (ORDER == 2) {
+      e = w / (NA * NB);
+      const int ab = w - e * (NA * NB);
+      b = ab / NA, a = ab - b * NA;
+    } else {
+      e = w / (NA * NB);
+      const int ab = w - e * (NA * NB);
+      a = ab / NB, b = ab - a * NB;
+    }
+  }
+
+  template <class R, class W, class IO = BlockIO, class H = NoHook, class GH = NoHook>
+  __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
+                                 double* __restrict__ work, double* __restrict__ out, double lam,
+                                 R release, W pre_out, const double* tab, IO io = IO(),
+                                 IO oio = IO(), H after_in = H(), GH geo_ready = GH()) {
+    double* WA = work;
+    double* WB = work + NE * SEA;
+    // S1: r -> k, value and k-derivative
+    SPHP_FOR_ITEMS(NE * M * M, w) {
+      const int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
+      double x[M], u[Q], d[Q];
+      if constexpr (IO::DENSE)
+        RowRot<M>::load(cin + e * M3 + pq * M, w, x);
+      else
+        io.template load_row<M>(cin, e, pq, x);
+      X::interp_and_deriv(tab, x, u, d);
+      double* a = WA + e * SEA + p * PA + q * RA;
+      st_pencil<Q, 1>(a, u);
+      st_pencil<Q, 1>(a + TA, d);
+    }
+    __syncthreads();
+    after_in();
+    // S2: q -> j
+    SPHP_FOR_ITEMS(NE * M * Q, w) {
+      int e, p, k;
+      item<L.O2, M, Q>(w, e, p, k);
+      const double* a = WA + e * SEA + p * PA + k;
+      double* b = WB + e * SEB + p * PB + k;
+      double x[M], u[Q], d[Q];
+      ld_pencil<M, RA>(a, x);
+      X::interp_and_deriv(tab, x, u, d);
+      st_pencil<Q, Q>(b, u);
+      st_pencil<Q, Q>(b + TB, d);
+      ld_pencil<M, RA>(a + TA, x);
+      X::interp(tab, x, u);
+      st_pencil<Q, Q>(b + 2 * TB, u);
+    }
+    __syncthreads();
+    geo_ready();  // the staged geometry is first read here (pipeline: GEO_HOOK)
+    // S5: columns along i
+    SPHP_FOR_ITEMS(NE * Q * Q, w) {
+      int e, j, k;
+      item<L.O5, Q, Q>(w, e, j, k);
+      const int jk = j * Q + k;
+      double* b = WB + e * SEB + jk;
+      double x[M], u[Q], d0[Q], d1[Q], d2[Q], f0[Q], f1[Q], f2[Q];
+      ld_pencil<M, PB>(b, x);
+      X::interp_and_deriv(tab, x, u, d0);
+      ld_pencil<M, PB>(b + TB, x);
+      X::interp(tab, x, d1);
+      ld_pencil<M, PB>(b + 2 * TB, x);
+      X::interp(tab, x, d2);
+      if constexpr (GK == SPHP_GEOM_METRIC) {
+        const double* gr = geo + e * GEO_S + jk;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          const double g0 = gr[0 * CS + i * Q * Q], g1 = gr[1 * CS + i * Q * Q], g2 = gr[2 * CS + i * Q * Q];
+          f0[i] = fma(g2, d2[i], fma(g1, d1[i], g0 * d0[i]));
+          const double g3 = gr[3 * CS + i * Q * Q], g4 = gr[4 * CS + i * Q * Q];
+          f1[i] = fma(g4, d2[i], fma(g3, d1[i], g1 * d0[i]));
+          const double g5 = gr[5 * CS + i * Q * Q];
+          f2[i] = fma(g5, d2[i], fma(g4, d1[i], g2 * d0[i]));
+          u[i] = lam * gr[6 * CS + i * Q * Q] * u[i];
+        }
+      } else {
+        const double* gg = geo + e * GEO_S;
+        const double det = gg[0];
+        const double* iv = gg + 1;
+        const double a00 = det * (iv[0] * iv[0] + iv[1] * iv[1] + iv[2] * iv[2]);
+        const double a01 = det * (iv[0] * iv[3] + iv[1] * iv[4] + iv[2] * iv[5]);
+        const double a02 = det * (iv[0] * iv[6] + iv[1] * iv[7] + iv[2] * iv[8]);
+        const double a11 = det * (iv[3] * iv[3] + iv[4] * iv[4] + iv[5] * iv[5]);
+        const double a12 = det * (iv[3] * iv[6] + iv[4] * iv[7] + iv[5] * iv[8]);
+        const double a22 = det * (iv[6] * iv[6] + iv[7] * iv[7] + iv[8] * iv[8]);
+        const double wjk = tab[T::W + j] * tab[T::W + k];
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          const double wq = wjk * tab[T::W + i];
+          f0[i] = wq * (a00 * d0[i] + a01 * d1[i] + a02 * d2[i]);
+          f1[i] = wq * (a01 * d0[i] + a11 * d1[i] + a12 * d2[i]);
+          f2[i] = wq * (a02 * d0[i] + a12 * d1[i] + a22 * d2[i]);
+          u[i] = lam * (wq * det) * u[i];
+        }
+      }
+      double c[M];
+      X::project2(tab, u, f0, c);
+      st_pencil<M, PB>(b, c);
+      X::project(tab, f1, c);
+      st_pencil<M, PB>(b + TB, c);
+      X::project(tab, f2, c);
+      st_pencil<M, PB>(b + 2 * TB, c);
+    }
+    __syncthreads();
+    release();
+    // B1: j -> q
+    SPHP_FOR_ITEMS(NE * M * Q, w) {
+      int e, p, k;
+      item<L.O2, M, Q>(w, e, p, k);
+      const double* b = WB + e * SEB + p * PB + k;
+      double* a = WA + e * SEA + p * PA + k;
+      double t[Q], f[Q], c[M];
+      ld_pencil<Q, Q>(b, t);
+      ld_pencil<Q, Q>(b + TB, f);
+      X::project2(tab, t, f, c);
+      st_pencil<M, RA>(a, c);
+      ld_pencil<Q, Q>(b + 2 * TB, t);
+      X::project(tab, t, c);
+      st_pencil<M, RA>(a + TA, c);
+    }
+    pre_out();
+    __syncthreads();
+    // B2: k -> r
+    SPHP_FOR_ITEMS(NE * M * M, w) {
+      const int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
+      const double* a = WA + e * SEA + p * PA + q * RA;
+      double t[Q], f[Q], c[M];
+      ld_pencil<Q, 1>(a, t);
+      ld_pencil<Q, 1>(a + TA, f);
+      X::project2(tab, t, f, c);
+      if constexpr (IO::DENSE)
+        RowRot<M>::store(out + e * M3 + pq * M, w, c);
+      else
+        oio.template store_row<M>(out, e, pq, c);
+    }
+  }
+};
+
+// variant selection: i-column plan where col_plan(Q) (common.cuh), else
+// skewed Q = 4 layout, j-pencil plan at Q % 4 == 0, k-row plan otherwise
+template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_, bool COL>
+using HexHelmSel = typename std::conditional<
+    COL, HexHelmCol<M_, Q_, GK, NE_, NT_, NSTP_>,
+    typename std::conditional<
+        (Q_ == 4), HexHelmQ4<M_, Q_, GK, NE_, NT_, NSTP_>,
+        typename std::conditional<(Q_ % 4 == 0), HexHelmJEO<M_, Q_, GK, NE_, NT_, NSTP_>,
+                                  HexHelmEO<M_, Q_, GK, NE_, NT_, NSTP_>>::type>::type>::type;
+
+template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
+using HexHelm = HexHelmSel<M_, Q_, GK, NE_, NT_, NSTP_, col_plan(Q_)>;
+// the plan of local (block in / block out) launches
+template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
+using HexHelmLocal = HexHelmSel<M_, Q_, GK, NE_, NT_, NSTP_, col_plan_local(Q_)>;
 
 // ===========================================================================
 // BwdTrans (K1): u = (B x B x B)^T c   (collections.py:133-150)

@@ -175,6 +175,16 @@ constexpr auto out_off_impl(int) -> decltype(Op::OUT_OFF, int()) { return Op::OU
 template <class Op>
 constexpr int out_off_impl(...) { return -1; }
 
+// an Op whose compute() takes a geo_ready hook and calls it before its first
+// read of the staged geometry (Op::GEO_HOOK): with one input stage the tile's
+// geometry then completes on its own mbarrier, waited for at the pointwise
+// stage instead of at the top of the tile — its copy has the first
+// contraction stages to land
+template <class Op>
+constexpr auto geo_hook_impl(int) -> decltype(Op::GEO_HOOK, bool()) { return Op::GEO_HOOK; }
+template <class Op>
+constexpr bool geo_hook_impl(...) { return false; }
+
 template <class Op, int MODE>
 struct Scaffold {
   static constexpr int NE = Op::NE, NT = Op::NT;
@@ -226,6 +236,12 @@ struct Scaffold {
   // CTA)
   static constexpr int SMEM_CTAS = (int)(233472 / (SMEM_BYTES + 1024)) < 1 ? 1 : (int)(233472 / (SMEM_BYTES + 1024));
   static constexpr int MIN_CTAS = CLS ? SPHP_CLASS_MINB : 1;
+#ifndef SPHP_NO_GEO_HOOK
+  static constexpr bool GHOOK = geo_hook_impl<Op>(0) && NST == 1 && Op::GEO > 0 && !GDIR &&
+                                (ModeTraits<MODE>::LOCAL || CLS);
+#else
+  static constexpr bool GHOOK = false;  // tuning build: geometry waited for at the top of the tile
+#endif
 };
 
 template <class Op, int MODE>
@@ -392,15 +408,21 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
       if (GEO > 0) bulk_prefetch_l2(a.geom + w0 * a.gstride, bytes_g);
       return;
     }
-    mbar_expect_tx(&bar[s], bytes_in + bytes_g);
+    uint64_t* gbar = S::GHOOK ? &bar[1] : &bar[s];  // GHOOK: NST == 1, bar[1] is the geometry's
+    if constexpr (S::GHOOK) {
+      mbar_expect_tx(&bar[s], bytes_in);
+      mbar_expect_tx(gbar, bytes_g);
+    } else {
+      mbar_expect_tx(&bar[s], bytes_in + bytes_g);
+    }
     bulk_g2s(in_s, reinterpret_cast<const char*>(a.in) + a0, bytes_in, &bar[s]);
     if (GEO > 0) {
       if (a.gstride == GEO && a.goff == 0 && GEO_S == GEO) {
-        bulk_g2s(geo_s, a.geom + w0 * a.gstride, bytes_g, &bar[s]);
+        bulk_g2s(geo_s, a.geom + w0 * a.gstride, bytes_g, gbar);
       } else {
         for (int e = 0; e < r; ++e)
           bulk_g2s(geo_s + e * GEO_S, a.geom + (w0 + e) * a.gstride + a.goff,
-                   (uint32_t)(sizeof(double) * GEO), &bar[s]);
+                   (uint32_t)(sizeof(double) * GEO), gbar);
       }
     }
   };
@@ -551,13 +573,14 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
       bulk_prefetch_l2(a.geom + w0 * a.gstride, (uint32_t)(sizeof(double) * NE * GEO));
       return;
     }
-    mbar_expect_tx(&bar[s], (uint32_t)(sizeof(double) * NE * GEO));
+    uint64_t* gbar = S::GHOOK ? &bar[1] : &bar[s];
+    mbar_expect_tx(gbar, (uint32_t)(sizeof(double) * NE * GEO));
     if (a.gstride == GEO && a.goff == 0 && GEO_S == GEO) {
-      bulk_g2s(geo_s, a.geom + w0 * a.gstride, (uint32_t)(sizeof(double) * NE * GEO), &bar[s]);
+      bulk_g2s(geo_s, a.geom + w0 * a.gstride, (uint32_t)(sizeof(double) * NE * GEO), gbar);
     } else {
       for (int e = 0; e < NE; ++e)
         bulk_g2s(geo_s + e * GEO_S, a.geom + (w0 + e) * a.gstride + a.goff, (uint32_t)(sizeof(double) * GEO),
-                 &bar[s]);
+                 gbar);
     }
   };
 
@@ -586,9 +609,10 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
 
     // ---- obtain the tile's inputs -------------------------------------
     const double* in_p = in_s;
+    bool geo_tma = MT::CLASS;  // GHOOK: this tile's geometry arrives on bar[1]
     if constexpr (MT::CLASS) {
       cp_async_wait<0>();
-      if constexpr (!S::GDIR) {
+      if constexpr (!S::GDIR && !S::GHOOK) {
         mbar_wait(&bar[s], (phase >> s) & 1);
         phase ^= (1u << s);
       }
@@ -601,6 +625,7 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
         mbar_wait(&bar[s], (phase >> s) & 1);
         phase ^= (1u << s);
         in_p = in_s + off;
+        geo_tma = true;
       } else {
         for (int i = tid; i < r * IN; i += NT) in_s[i] = a.in[w0 * IN + i];
         if constexpr (GEO > 0 && !S::GDIR) {
@@ -655,6 +680,16 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
       }
     };
     auto pre_out = [&]() {};
+    // GHOOK: all threads wait for the tile's geometry right before the
+    // pointwise stage (bar[1], parity bit 1 of phase)
+    auto geo_ready = [&]() {
+      if constexpr (S::GHOOK) {
+        if (geo_tma) {
+          mbar_wait(&bar[1], (phase >> 1) & 1);
+          phase ^= 2u;
+        }
+      }
+    };
     const bool bulk_out = S::BULK_OUT && a.use_tma && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0;
     // out_t + i and a.out + w0 * OUT + i agree mod 16 bytes (the buffer
     // starts OUT_OFF doubles into the 16-byte aligned work area)
@@ -670,11 +705,18 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
         cin_io.v = cout_io.v = v;
       }
       const double* geo_p = S::GDIR ? a.geom + (a.e0 + w0) * a.gstride : geo_s;
-      Op::compute(in_p, geo_p, work, out_c, a.lam, release, pre_out, c_tab, cin_io, cout_io, after_in);
+      if constexpr (S::GHOOK)
+        Op::compute(in_p, geo_p, work, out_c, a.lam, release, pre_out, c_tab, cin_io, cout_io, after_in, geo_ready);
+      else
+        Op::compute(in_p, geo_p, work, out_c, a.lam, release, pre_out, c_tab, cin_io, cout_io, after_in);
       fence_proxy_async();
     } else {
       const double* geo_p = S::GDIR ? a.geom + w0 * a.gstride : geo_s;
-      Op::compute(in_p, geo_p, work, out_t, a.lam, release, pre_out, c_tab);
+      if constexpr (S::GHOOK)
+        Op::compute(in_p, geo_p, work, out_t, a.lam, release, pre_out, c_tab, BlockIO(), BlockIO(), NoHook(),
+                    geo_ready);
+      else
+        Op::compute(in_p, geo_p, work, out_t, a.lam, release, pre_out, c_tab);
       if (bulk_out) fence_proxy_async();  // this thread's buffer writes -> async proxy
     }
     __syncthreads();
