@@ -166,7 +166,8 @@ __device__ __forceinline__ void cp_async_wait() {
 // Orders whose fused hex Helmholtz runs the i-column plan (HexHelmCol,
 // hex_ops.cuh): bit Q.  That plan reads the metric in natural point order.
 // Measured (cfg4 64^3, local / class-assembled ms; profiles/r02_col.log):
-// Q = 5 (P = 3) 0.399 -> 0.315 / 0.467 -> 0.388, Q = 7 (P = 5) 1.088 -> 1.045
+// Q = 4 (P = 2) 0.198 -> 0.158 / 0.217 -> 0.181 (against the skewed Q = 4 plan
+// and its global-geometry class launch), Q = 5 (P = 3) 0.399 -> 0.315 / 0.467 -> 0.388, Q = 7 (P = 5) 1.088 -> 1.045
 // / 1.294 -> 1.204; Q = 6 (P = 4) 0.612 -> 0.591 local but 0.698 -> 0.749
 // assembled (its larger work area drops the class tile to two CTAs per SM):
 // local only there (SPHP_COL_LOCAL_QMASK; Q = 6 keeps natural point order
@@ -174,7 +175,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // too few threads: the row / pencil plans stay (P = 6..8: 1.55 vs 1.50,
 // 2.79 vs 2.25, 3.56 vs 3.27 ms).
 #ifndef SPHP_COL_QMASK
-#define SPHP_COL_QMASK ((1 << 5) | (1 << 7))
+#define SPHP_COL_QMASK ((1 << 4) | (1 << 5) | (1 << 7))
 #endif
 #ifndef SPHP_COL_LOCAL_QMASK
 #define SPHP_COL_LOCAL_QMASK (1 << 6)

@@ -129,7 +129,9 @@ constexpr int class_ne() {
   // measured (tools/time_phases.py, cfg4 64^3, METRIC, Q = P + 2): P = 2..8
   // -> 4, 8, 4, 2, 1, 1, 1 (residency alone picks 2 at P = 3 and 1 at P = 5,
   // 9-10 % slower there; 8 vs 4 at P = 3: -1.4 %)
-  if (GK == SPHP_GEOM_METRIC && Q == M + 1) return (M == 4 && !col_plan(Q)) ? 8 : (M <= 5 ? 4 : (M == 6 ? 2 : 1));
+  // i-column plan: P = 2 8 (0.181 vs 0.184 ms at 4), P = 3 4 (0.388 vs 0.397 at 8), P = 5 2
+  if (GK == SPHP_GEOM_METRIC && Q == M + 1 && col_plan(Q)) return M == 3 ? 8 : (M <= 5 ? 4 : (M == 6 ? 2 : 1));
+  if (GK == SPHP_GEOM_METRIC && Q == M + 1) return M == 4 ? 8 : (M <= 5 ? 4 : (M == 6 ? 2 : 1));
   int best = 1, score = class_resident<M, Q, GK, 1>();
   if (class_resident<M, Q, GK, 2>() > score) best = 2, score = class_resident<M, Q, GK, 2>();
   if (class_resident<M, Q, GK, 4>() > score) best = 4, score = class_resident<M, Q, GK, 4>();
