@@ -98,12 +98,11 @@ const char* sphp_last_error(void);
 /* number of SMs of the current device, 0 if none (used by the autotuner)   */
 int sphp_device_sm_count(void);
 /* stage plan of the fused hex Helmholtz for nmodes = M, npoints = Q per
- * direction: 0 K-row, 1 J-pencil, 2 skewed Q = 4, 3 i-column;
- * local_launch = 1: the plan of block-in / block-out applies (sphp_apply),
- * which at some orders differs from the one every assembled apply uses (all
- * assembly algorithms of a map return bitwise the same vector).  Results of
- * two plans agree to rounding, not bitwise.  -1: no fast kernel.            */
-int sphp_hex_helmholtz_plan(int M, int Q, int local_launch);
+ * direction: 0 K-row, 1 J-pencil, 3 i-column;
+ * -1: no fast kernel for the key.  Every launch mode of a key (block in /
+ * block out, class, gathering) runs the same plan, so all assembly
+ * algorithms of a map return bitwise the same vector.                        */
+int sphp_hex_helmholtz_plan(int M, int Q);
 
 /* ---- reference elements: StdExpansion tables ----------------------------
  * replaces stdregions.StdExpansion(shape, basis_keys) (stdregions.py:70-240)

@@ -68,7 +68,7 @@ _SIGS = {
     "sphp_abi_version": (_i, []),
     "sphp_last_error": (C.c_char_p, []),
     "sphp_device_sm_count": (_i, []),
-    "sphp_hex_helmholtz_plan": (_i, [_i, _i, _i]),
+    "sphp_hex_helmholtz_plan": (_i, [_i, _i]),
     "sphp_tables_create": (_i, [_i, _ip, _ip, _ip, _ip, _pp]),
     "sphp_tables_destroy": (_i, [_p]),
     "sphp_tables_query": (_i, [_p, _i, _p, _p, _p, _p, _p]),

@@ -711,10 +711,10 @@ extern "C" {
 int sphp_abi_version(void) { return SPHP_ABI_VERSION; }
 const char* sphp_last_error(void) { return g_err.c_str(); }
 int sphp_device_sm_count(void) { return sm_count(); }
-int sphp_hex_helmholtz_plan(int M, int Q, int local_launch) {
+int sphp_hex_helmholtz_plan(int M, int Q) {
   if (!sphp::fast_key(M, Q) || M > 9) return -1;
-  if (local_launch ? sphp::col_plan_local(Q) : sphp::col_plan(Q)) return 3;
-  return Q == 4 ? 2 : (Q % 4 == 0 ? 1 : 0);
+  if (sphp::col_plan(Q)) return 3;
+  return Q % 4 == 0 ? 1 : 0;
 }
 
 // stdregions.StdExpansion (stdregions.py:70-240)
@@ -1525,7 +1525,6 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
     o.in = w->loc_x.as<double>();
     o.out = w->loc_y.as<double>();
     o.mode = AsmMode::LOCAL;
-    o.asm_plan = 1;
     // the operator walks the elements backwards: it starts on the block the
     // scatter wrote last and ends on the elements the owner sum reads first,
     // both still in L2
@@ -1680,7 +1679,6 @@ int assembled_host_pipelined(sphp_coll* c, const sphp_amap* a, const double* x, 
   }
   OpArgs o = base_args(c);
   o.mode = AsmMode::LOCAL;
-  o.asm_plan = 1;
   // class-range algorithm: the operator reads x and writes Z + y interiors
   // slab by slab, the class owner sum takes the place of owner_periodic_v3
   int ne = 0;

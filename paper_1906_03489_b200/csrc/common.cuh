@@ -165,26 +165,17 @@ __device__ __forceinline__ void cp_async_wait() {
 // (MODE 6) loses 7-20 % at every Q >= 5 (profiles/r02_kmajor.log)
 // Orders whose fused hex Helmholtz runs the i-column plan (HexHelmCol,
 // hex_ops.cuh): bit Q.  That plan reads the metric in natural point order.
-// Measured (cfg4 64^3, local / class-assembled ms; profiles/r02_col.log):
+// Measured (cfg4 64^3, local / class-assembled ms; profiles/r02_col*.log):
 // Q = 4 (P = 2) 0.198 -> 0.158 / 0.217 -> 0.181 (against the skewed Q = 4 plan
-// and its global-geometry class launch), Q = 5 (P = 3) 0.399 -> 0.315 / 0.467 -> 0.388, Q = 7 (P = 5) 1.088 -> 1.045
-// / 1.294 -> 1.204; Q = 6 (P = 4) 0.612 -> 0.591 local but 0.698 -> 0.749
-// assembled (its larger work area drops the class tile to two CTAs per SM):
-// local only there (SPHP_COL_LOCAL_QMASK; Q = 6 keeps natural point order
-// in both plans).  One element per tile at Q >= 8 leaves the column stage
-// too few threads: the row / pencil plans stay (P = 6..8: 1.55 vs 1.50,
-// 2.79 vs 2.25, 3.56 vs 3.27 ms).
+// and its global-geometry class launch), Q = 5 (P = 3) 0.399 -> 0.312 /
+// 0.467 -> 0.370, Q = 6 (P = 4) 0.612 -> 0.567 / 0.691 -> 0.665, Q = 7 (P = 5)
+// 1.088 -> 1.022 / 1.294 -> 1.187.  One element per tile at Q >= 8 leaves the
+// column stage too few threads: the row / pencil plans stay (P = 6..8: 1.54
+// vs 1.50, 2.79 vs 2.25, 3.56 vs 3.27 ms).
 #ifndef SPHP_COL_QMASK
-#define SPHP_COL_QMASK ((1 << 4) | (1 << 5) | (1 << 7))
-#endif
-#ifndef SPHP_COL_LOCAL_QMASK
-#define SPHP_COL_LOCAL_QMASK (1 << 6)
+#define SPHP_COL_QMASK ((1 << 4) | (1 << 5) | (1 << 6) | (1 << 7))
 #endif
 __host__ __device__ constexpr bool col_plan(int Q) { return Q < 32 && ((SPHP_COL_QMASK >> Q) & 1); }
-// local (block in / block out) launches only; needs natural metric order
-__host__ __device__ constexpr bool col_plan_local(int Q) {
-  return col_plan(Q) || (Q < 32 && Q != 8 && ((SPHP_COL_LOCAL_QMASK >> Q) & 1) && !((SPHP_KMAJOR_QMASK >> Q) & 1));
-}
 __host__ __device__ constexpr bool metric_kmajor(int Q) {
   return Q < 32 && ((SPHP_KMAJOR_QMASK >> Q) & 1) && !col_plan(Q);
 }

@@ -37,33 +37,15 @@ constexpr int helm_ne() {
 template <int M, int Q, int GK, int NSTP, int NE>
 static cudaError_t helm_variant_ne(const OpArgs& oa, cudaStream_t s) {
   constexpr int NT = choose_nt(NE, Q * Q);
-  if (oa.mode == AsmMode::LOCAL && !oa.asm_plan) {
-    using Op = HexHelmLocal<M, Q, GK, NE, NT, NSTP>;
-    if constexpr (Scaffold<Op, 0>::SMEM_BYTES > 227 * 1024)
-      return cudaErrorNotSupported;
-    else
-      return launch_pipe<Op, 0>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
-  }
   using Op = HexHelm<M, Q, GK, NE, NT, NSTP>;
-  if constexpr (Scaffold<Op, 3>::SMEM_BYTES > 227 * 1024) {
+  if constexpr (Scaffold<Op, 0>::SMEM_BYTES > 227 * 1024 || Scaffold<Op, 3>::SMEM_BYTES > 227 * 1024) {
     return cudaErrorNotSupported;
   } else {
     return launch_mode<Op>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
   }
 }
-// local launches of an order whose local plan differs from its general one
-template <int M, int Q, int GK, int NSTP, int BUDGET>
-static cudaError_t helm_variant_local(const OpArgs& oa, cudaStream_t s) {
-  constexpr int NE = helm_ne<M, Q, GK, NSTP, BUDGET, true>();
-  constexpr int NT = choose_nt(NE, Q * Q);
-  using Op = HexHelmLocal<M, Q, GK, NE, NT, NSTP>;
-  return launch_pipe<Op, 0>(oa, geom_record<3, Q * Q * Q>(GK), 0, s);
-}
 template <int M, int Q, int GK, int NSTP, int BUDGET>
 static cudaError_t helm_variant(const OpArgs& oa, cudaStream_t s) {
-  if constexpr (col_plan_local(Q) != col_plan(Q)) {
-    if (oa.mode == AsmMode::LOCAL && !oa.asm_plan) return helm_variant_local<M, Q, GK, NSTP, BUDGET>(oa, s);
-  }
   constexpr int NE = helm_ne<M, Q, GK, NSTP, BUDGET, col_plan(Q)>();
   constexpr int NT = choose_nt(NE, Q * Q);
   using Op = HexHelm<M, Q, GK, NE, NT, NSTP>;
@@ -96,15 +78,13 @@ static int helm_variant_env() {
 
 // PERIODIC_CLASS (pipeline MODE 5): tiles of NE consecutive elements of an
 // x-row (NE must divide n)
-// MODE 6 (geometry from global memory, L2-prefetched) at P = 2 / METRIC
+// MODE 6 (geometry from global memory, L2-prefetched): tuning builds only (SPHP_CLASS_GDIR)
 #ifndef SPHP_CLASS_GDIR
 #define SPHP_CLASS_GDIR 0  // tuning: 1 = class mode of k-major METRIC orders reads global geometry too
 #endif
 template <int M, int Q, int GK>
 constexpr int class_mode() {
-  return (GK == SPHP_GEOM_METRIC && !col_plan(Q) && ((M == 3 && Q == 4) || (SPHP_CLASS_GDIR && metric_kmajor(Q))))
-             ? 6
-             : 5;
+  return (GK == SPHP_GEOM_METRIC && !col_plan(Q) && SPHP_CLASS_GDIR && metric_kmajor(Q)) ? 6 : 5;
 }
 template <int M, int Q, int GK, int NE>
 constexpr size_t class_smem() {
@@ -130,7 +110,8 @@ constexpr int class_ne() {
   // -> 4, 8, 4, 2, 1, 1, 1 (residency alone picks 2 at P = 3 and 1 at P = 5,
   // 9-10 % slower there; 8 vs 4 at P = 3: -1.4 %)
   // i-column plan: P = 2 8 (0.181 vs 0.184 ms at 4), P = 3 4 (0.388 vs 0.397 at 8), P = 5 2
-  if (GK == SPHP_GEOM_METRIC && Q == M + 1 && col_plan(Q)) return M == 3 ? 8 : (M <= 5 ? 4 : (M == 6 ? 2 : 1));
+  // P = 4 2 (0.665 vs 0.700 ms at 4: five CTAs per SM)
+  if (GK == SPHP_GEOM_METRIC && Q == M + 1 && col_plan(Q)) return M == 3 ? 8 : (M == 4 ? 4 : (M <= 6 ? 2 : 1));
   if (GK == SPHP_GEOM_METRIC && Q == M + 1) return M == 4 ? 8 : (M <= 5 ? 4 : (M == 6 ? 2 : 1));
   int best = 1, score = class_resident<M, Q, GK, 1>();
   if (class_resident<M, Q, GK, 2>() > score) best = 2, score = class_resident<M, Q, GK, 2>();

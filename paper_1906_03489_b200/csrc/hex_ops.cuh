@@ -622,258 +622,6 @@ struct HexHelmJEO {
 };
 
 // ===========================================================================
-// Fused Helmholtz for Q = 4 (P = 2 at the configs' Q = P + 2): skewed
-// shared-memory layout.  With Q = 4 one (i, j) plane of an element is exactly
-// the 16 eight-byte bank pairs, so every natural layout puts the lanes of one
-// of the three pencil directions on 4 banks (ncu, P = 2 J-plan: 49 % of the
-// shared wavefronts were conflict excess, L1 90 % busy).  Here every work
-// tensor T[a][b][c] (a slowest) lives at
-//     off(a, b, c) = 16 a + 4 ((a + b) & 3) + ((b + c) & 3),
-// whose bank 4((a+b)&3) + ((b+c)&3) is a bijection of the two free indices
-// for each fixed index: pencils along any direction are conflict free.
-// Element tensors are ES = 76 doubles apart (= 12 mod 16): for the M x Q item
-// stages, whose half-warps straddle two elements, the next element's rows
-// then land on the bank rows the current one leaves free.  The pointwise
-// stage runs on i-pencils (lanes (j, k)), the direction in which the staged
-// geometry rows (point (i*Q + j)*Q + k) are conflict free too.
-//   S1 r->k    c -> T1[p][q][k]                 items (p, q)       W0
-//   S2 q->j    T1 -> T2[p][j][k]                items (p, k)       W1
-//   S3 p->i    T2 -> u[i][j][k]                 items (j, k)       W0
-//   S4 d1 = D_j u (items (i, k)) -> W1 | d2 = D_k u (items (i, j)) -> W2
-//   S5 i-pencils: d0 = D_i u in registers, f = G grad u, t = lam wJ u +
-//      D_i^T f0; t -> W0, f1 -> W1, f2 -> W2          items (j, k)
-//   S6 a = D_j^T f1 (items (i, k)) in place in W1 | b = D_k^T f2 (items (i, j)) in W2
-//   S7 i->p    B (t + a + b) -> T2'[p][j][k]    items (j, k)       W0 (in place)
-//   S8 j->q    T2' -> T1'[p][q][k]              items (p, k)       W1
-//   S9 k->r    T1' -> out (the block, staged in W2)
-// ===========================================================================
-__host__ __device__ constexpr int q4_off(int a, int b, int c) {
-  return 16 * a + 4 * ((a + b) & 3) + ((b + c) & 3);
-}
-
-template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
-struct HexHelmQ4 {
-  static_assert(Q_ == 4 && M_ <= 4, "skewed layout is for Q = 4");
-  static constexpr int M = M_, Q = Q_, NE = NE_, NT = NT_;
-  static constexpr int NSTP = NSTP_;
-  static constexpr bool GEO_HOOK = true;  // compute() calls geo_ready() before its first geometry read
-  static constexpr int M3 = M * M * M, Q3 = Q * Q * Q;
-  static constexpr int IN = M3, OUT = M3;
-  static constexpr int CS = pt_stride(Q3);
-  static constexpr int GEO = (GK == SPHP_GEOM_METRIC) ? 7 * CS : 10;
-  static constexpr int ES = 76;  // element stride of a work tensor (= 12 mod 16)
-  static constexpr int WORK = 3 * ES;
-  static constexpr int OUT_OFF = 2 * NE * ES;  // S9 writes the block into W2 (free after S7)
-  using T = Tab<M, Q>;
-  using X = EO<M, Q>;
-
-  template <class R, class W, class IO = BlockIO, class H = NoHook, class GH = NoHook>
-  __device__ static void compute(const double* __restrict__ cin, const double* __restrict__ geo,
-                                 double* __restrict__ work, double* __restrict__ out, double lam,
-                                 R release, W pre_out, const double* tab, IO io = IO(),
-                                 IO oio = IO(), H after_in = H(), GH geo_ready = GH()) {
-    double* W0 = work;
-    double* W1 = work + NE * ES;
-    double* W2 = work + 2 * NE * ES;
-    // S1: r -> k
-    SPHP_FOR_ITEMS(NE * M * M, w) {
-      const int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
-      double x[M], u[Q];
-      if constexpr (IO::DENSE)
-        ld_pencil<M, 1>(cin + e * M3 + pq * M, x);
-      else
-        io.template load_row<M>(cin, e, pq, x);
-      X::interp(tab, x, u);
-      double* d = W0 + e * ES;
-#pragma unroll
-      for (int k = 0; k < Q; ++k) d[q4_off(p, q, k)] = u[k];
-    }
-    __syncthreads();
-    after_in();
-    // S2: q -> j
-    SPHP_FOR_ITEMS(NE * M * Q, w) {
-      const int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
-      const double* s = W0 + e * ES;
-      double x[M], u[Q];
-#pragma unroll
-      for (int q = 0; q < M; ++q) x[q] = s[q4_off(p, q, k)];
-      X::interp(tab, x, u);
-      double* d = W1 + e * ES;
-#pragma unroll
-      for (int j = 0; j < Q; ++j) d[q4_off(p, j, k)] = u[j];
-    }
-    __syncthreads();
-    // S3: p -> i
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      const int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
-      const double* s = W1 + e * ES;
-      double x[M], u[Q];
-#pragma unroll
-      for (int p = 0; p < M; ++p) x[p] = s[q4_off(p, j, k)];
-      X::interp(tab, x, u);
-      double* d = W0 + e * ES;
-#pragma unroll
-      for (int i = 0; i < Q; ++i) d[q4_off(i, j, k)] = u[i];
-    }
-    __syncthreads();
-    // S4: d1 = D_j u -> W1 (items (i, k)), d2 = D_k u -> W2 (items (i, j))
-    SPHP_FOR_ITEMS(2 * NE * Q * Q, w) {
-      const int kind = w >= NE * Q * Q;
-      const int v = w - kind * NE * Q * Q;
-      const int e = v / (Q * Q), ab = v - e * (Q * Q), i = ab / Q, c = ab - i * Q;
-      const double* s = W0 + e * ES;
-      double x[Q], r[Q];
-      if (kind == 0) {
-#pragma unroll
-        for (int j = 0; j < Q; ++j) x[j] = s[q4_off(i, j, c)];
-      } else {
-#pragma unroll
-        for (int k = 0; k < Q; ++k) x[k] = s[q4_off(i, c, k)];
-      }
-      X::template deriv<false, false>(tab, x, r);
-      if (kind == 0) {
-        double* d = W1 + e * ES;
-#pragma unroll
-        for (int j = 0; j < Q; ++j) d[q4_off(i, j, c)] = r[j];
-      } else {
-        double* d = W2 + e * ES;
-#pragma unroll
-        for (int k = 0; k < Q; ++k) d[q4_off(i, c, k)] = r[k];
-      }
-    }
-    __syncthreads();
-    geo_ready();  // the staged geometry is first read here (pipeline: GEO_HOOK)
-    // S5: pointwise on i-pencils
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      const int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
-      double* s0 = W0 + e * ES;
-      double* s1 = W1 + e * ES;
-      double* s2 = W2 + e * ES;
-      double u[Q], d0[Q], d1[Q], d2[Q], f0[Q], t[Q];
-#pragma unroll
-      for (int i = 0; i < Q; ++i) {
-        u[i] = s0[q4_off(i, j, k)];
-        d1[i] = s1[q4_off(i, j, k)];
-        d2[i] = s2[q4_off(i, j, k)];
-      }
-      X::template deriv<false, false>(tab, u, d0);
-      const double* g = geo + e * GEO;
-      double a00 = 0, a01 = 0, a02 = 0, a11 = 0, a12 = 0, a22 = 0, adet = 0;
-      if constexpr (GK == SPHP_GEOM_AFFINE) {
-        const double det = g[0];
-        const double* iv = g + 1;
-        a00 = det * (iv[0] * iv[0] + iv[1] * iv[1] + iv[2] * iv[2]);
-        a01 = det * (iv[0] * iv[3] + iv[1] * iv[4] + iv[2] * iv[5]);
-        a02 = det * (iv[0] * iv[6] + iv[1] * iv[7] + iv[2] * iv[8]);
-        a11 = det * (iv[3] * iv[3] + iv[4] * iv[4] + iv[5] * iv[5]);
-        a12 = det * (iv[3] * iv[6] + iv[4] * iv[7] + iv[5] * iv[8]);
-        a22 = det * (iv[6] * iv[6] + iv[7] * iv[7] + iv[8] * iv[8]);
-        adet = det;
-      }
-#pragma unroll
-      for (int i = 0; i < Q; ++i) {
-        double G00, G01, G02, G11, G12, G22, wj;
-        if constexpr (GK == SPHP_GEOM_METRIC) {
-          const int pt = metric_slot(3, Q, (i * Q + j) * Q + k);
-          G00 = g[0 * CS + pt];
-          G01 = g[1 * CS + pt];
-          G02 = g[2 * CS + pt];
-          G11 = g[3 * CS + pt];
-          G12 = g[4 * CS + pt];
-          G22 = g[5 * CS + pt];
-          wj = g[6 * CS + pt];
-        } else {
-          const double wq = tab[T::W + i] * tab[T::W + j] * tab[T::W + k];
-          G00 = wq * a00;
-          G01 = wq * a01;
-          G02 = wq * a02;
-          G11 = wq * a11;
-          G12 = wq * a12;
-          G22 = wq * a22;
-          wj = wq * adet;
-        }
-        f0[i] = G00 * d0[i] + G01 * d1[i] + G02 * d2[i];
-        const double f1 = G01 * d0[i] + G11 * d1[i] + G12 * d2[i];
-        const double f2 = G02 * d0[i] + G12 * d1[i] + G22 * d2[i];
-        t[i] = lam * wj * u[i];
-        s1[q4_off(i, j, k)] = f1;
-        s2[q4_off(i, j, k)] = f2;
-      }
-      X::template deriv<true, true>(tab, f0, t);  // t += D_i^T f0
-#pragma unroll
-      for (int i = 0; i < Q; ++i) s0[q4_off(i, j, k)] = t[i];
-    }
-    __syncthreads();
-    release();
-    // S6: a = D_j^T f1 in place (items (i, k)), b = D_k^T f2 in place (items (i, j))
-    SPHP_FOR_ITEMS(2 * NE * Q * Q, w) {
-      const int kind = w >= NE * Q * Q;
-      const int v = w - kind * NE * Q * Q;
-      const int e = v / (Q * Q), ab = v - e * (Q * Q), i = ab / Q, c = ab - i * Q;
-      double x[Q], r[Q];
-      if (kind == 0) {
-        double* s = W1 + e * ES;
-#pragma unroll
-        for (int j = 0; j < Q; ++j) x[j] = s[q4_off(i, j, c)];
-        X::template deriv<true, false>(tab, x, r);
-#pragma unroll
-        for (int j = 0; j < Q; ++j) s[q4_off(i, j, c)] = r[j];
-      } else {
-        double* s = W2 + e * ES;
-#pragma unroll
-        for (int k = 0; k < Q; ++k) x[k] = s[q4_off(i, c, k)];
-        X::template deriv<true, false>(tab, x, r);
-#pragma unroll
-        for (int k = 0; k < Q; ++k) s[q4_off(i, c, k)] = r[k];
-      }
-    }
-    __syncthreads();
-    // S7: i -> p on t + a + b; T2' -> W0 (t is read by this lane only: the
-    // (j, k) pencil it overwrites is its own)
-    SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      const int e = w / (Q * Q), jk = w - e * (Q * Q), j = jk / Q, k = jk - j * Q;
-      double* s0 = W0 + e * ES;
-      const double* s1 = W1 + e * ES;
-      const double* s2 = W2 + e * ES;
-      double x[Q], c[M];
-#pragma unroll
-      for (int i = 0; i < Q; ++i) x[i] = s0[q4_off(i, j, k)] + s1[q4_off(i, j, k)] + s2[q4_off(i, j, k)];
-      X::project(tab, x, c);
-#pragma unroll
-      for (int p = 0; p < M; ++p) s0[q4_off(p, j, k)] = c[p];
-    }
-    __syncthreads();
-    // S8: j -> q  (W0 -> W1)
-    SPHP_FOR_ITEMS(NE * M * Q, w) {
-      const int e = w / (M * Q), rem = w - e * (M * Q), p = rem / Q, k = rem - p * Q;
-      const double* s = W0 + e * ES;
-      double x[Q], c[M];
-#pragma unroll
-      for (int j = 0; j < Q; ++j) x[j] = s[q4_off(p, j, k)];
-      X::project(tab, x, c);
-      double* d = W1 + e * ES;
-#pragma unroll
-      for (int q = 0; q < M; ++q) d[q4_off(p, q, k)] = c[q];
-    }
-    pre_out();
-    __syncthreads();
-    // S9: k -> r  (W1 -> out, dense)
-    SPHP_FOR_ITEMS(NE * M * M, w) {
-      const int e = w / (M * M), pq = w - e * (M * M), p = pq / M, q = pq - p * M;
-      const double* s = W1 + e * ES;
-      double x[Q], c[M];
-#pragma unroll
-      for (int k = 0; k < Q; ++k) x[k] = s[q4_off(p, q, k)];
-      X::project(tab, x, c);
-      if constexpr (IO::DENSE)
-        st_pencil<M, 1>(out + e * M3 + pq * M, c);
-      else
-        oio.template store_row<M>(out, e, pq, c);
-    }
-  }
-};
-
-// ===========================================================================
 // Fused Helmholtz, i-column plan (HexHelmCol): the direction i never goes
 // through shared memory.  Sum factorisation runs k, then j, on the small
 // mode-sized tensors; the pointwise stage owns one (j, k) column of the
@@ -928,13 +676,16 @@ __host__ __device__ constexpr ColLay col_layout(int M, int Q, int NE, int GEO) {
   L.SEB = ef ? with_res16(3 * M * L.PB, g) : 3 * M * L.PB;
   L.GS = (ef && GEO > 16) ? with_res16(GEO, g) : GEO;
   // searched (tools/layout_search_col.py)
+#ifndef SPHP_COL_GENERIC
   if (M == 4 && Q == 5 && NE == 4) L.PA = 20, L.SEA = 164, L.PB = 25, L.SEB = 300;
   if (M == 4 && Q == 5 && NE == 8) L.PA = 20, L.SEA = 162, L.PB = 25, L.SEB = 302;
   if (M == 6 && Q == 7 && NE == 2) L.PA = 47, L.SEA = 568, L.PB = 55, L.SEB = 1000;
   if (M == 8 && Q == 9 && NE == 1) L.RA = 10, L.PA = 89, L.SEA = 1424, L.PB = 89, L.SEB = 2136;
   if (M == 9 && Q == 10 && NE == 1) L.RA = 10, L.PA = 105, L.SEA = 1890, L.PB = 105, L.SEB = 2835, L.O2 = 2;
   if (M == 5 && Q == 6 && NE == 4) L.RA = 7, L.PA = 35, L.SEA = 356, L.PB = 38, L.SEB = 572;
-  if (M == 5 && Q == 6 && NE == 2) L.RA = 9, L.PA = 45, L.SEA = 465, L.PB = 45, L.SEB = 678, L.O2 = 2, L.O5 = 0;
+  // (M = 5, Q = 6, NE = 2: the searched pitches (RA 9, PA 45, PB 45: 1.07x the ideal wavefronts) cost a
+  // resident CTA against the rule above, 4 instead of 5 per SM: class P = 4 0.700 vs 0.665 ms)
+#endif
   return L;
 }
 
@@ -1106,20 +857,15 @@ struct HexHelmCol {
 };
 
 // variant selection: i-column plan where col_plan(Q) (common.cuh), else
-// skewed Q = 4 layout, j-pencil plan at Q % 4 == 0, k-row plan otherwise
+// j-pencil plan at Q % 4 == 0, k-row plan otherwise
 template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_, bool COL>
 using HexHelmSel = typename std::conditional<
     COL, HexHelmCol<M_, Q_, GK, NE_, NT_, NSTP_>,
-    typename std::conditional<
-        (Q_ == 4), HexHelmQ4<M_, Q_, GK, NE_, NT_, NSTP_>,
-        typename std::conditional<(Q_ % 4 == 0), HexHelmJEO<M_, Q_, GK, NE_, NT_, NSTP_>,
-                                  HexHelmEO<M_, Q_, GK, NE_, NT_, NSTP_>>::type>::type>::type;
+    typename std::conditional<(Q_ % 4 == 0), HexHelmJEO<M_, Q_, GK, NE_, NT_, NSTP_>,
+                              HexHelmEO<M_, Q_, GK, NE_, NT_, NSTP_>>::type>::type;
 
 template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
 using HexHelm = HexHelmSel<M_, Q_, GK, NE_, NT_, NSTP_, col_plan(Q_)>;
-// the plan of local (block in / block out) launches
-template <int M_, int Q_, int GK, int NE_, int NT_, int NSTP_ = 2>
-using HexHelmLocal = HexHelmSel<M_, Q_, GK, NE_, NT_, NSTP_, col_plan_local(Q_)>;
 
 // ===========================================================================
 // BwdTrans (K1): u = (B x B x B)^T c   (collections.py:133-150)

@@ -46,10 +46,6 @@ struct OpArgs {
   int n;              // PERIODIC: grid size
   int colour;         // PERIODIC: colour id 0..7
   int reverse = 0;    // LOCAL: walk the tiles last to first
-  // LOCAL launch on behalf of an assembled periodic apply (split algorithm):
-  // take the stage plan of the class / gathering launches, so that every
-  // assembly algorithm of a map returns bitwise the same vector
-  int asm_plan = 0;
   // PERIODIC_CLASS: absolute index of the launch's first element (z-slab
   // pipelines), the output block Z (per tile of NE elements: classes 0..25,
   // class-major, NE * (nm - (P-1)^3) doubles; then n^3 (P-1)^3 interior

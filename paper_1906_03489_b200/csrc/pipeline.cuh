@@ -196,9 +196,10 @@ struct Scaffold {
   static constexpr int GEO_S = geo_s_impl<Op>(0);  // even, >= GEO
   // MODE 6 = MODE 5 reading the geometry straight from global memory in the
   // pointwise stage (prefetched into L2 one tile ahead) instead of staging
-  // it: no shared-memory copy, more resident CTAs.  Only wins where the
-  // tile's compute is short enough for L2 latency (P = 2: 0.209 -> 0.198
-  // ms; P = 3..8 lose 10-35 %, tools/time_phases.py)
+  // it: no shared-memory copy, more resident CTAs.  Only won at P = 2 with
+  // the former skewed Q = 4 plan (0.209 -> 0.198 ms; P = 3..8 lose 10-35 %,
+  // tools/time_phases.py); the i-column plan beats both (0.181 ms), so no
+  // default build takes MODE 6 any more (SPHP_CLASS_GDIR tuning builds do)
   static constexpr bool GDIR = ModeTraits<MODE>::GDIR;
   static constexpr int GEO_T = GDIR ? 0 : NE * GEO_S;
   static constexpr int STAGE = IN_T + GEO_T;
