@@ -285,10 +285,31 @@ def create_collection(elements, operator, strategy=Strategy.AUTO, trials=5, warm
     return Collection(elements, operator, strategy, lam=lam)
 
 
+def hbm_peak_gbs():
+    """(GB/s, kind) of the HBM roofline the reports are quoted against:
+    SPHP_HBM_PEAK_GBS, else the driver-measured copy bandwidth in
+    MEASURED_PEAKS.json at the repository root, else the B200 nominal 8 TB/s."""
+    import json
+    import os
+    from pathlib import Path
+    env = os.environ.get("SPHP_HBM_PEAK_GBS")
+    if env:
+        return float(env), "env"
+    p = Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+    except (OSError, ValueError, KeyError):
+        return 8000.0, "nominal"
+
+
 def autotune(elements, operator, trials=5, warmups=2, candidates=None, lam=1.0):
     """Time each GPU strategy on this group and pick the fastest median
     (collections.py:285-313).  Times are CUDA-event device times of one
     apply on a resident `standard_normal` block from `default_rng(0)`.
+    The report keeps the reference's shape (`median_s`, `times_s`,
+    `mac_count` per strategy, collections.py:308-311) extended with
+    `hbm_bytes`, `dof_per_s` (elements x modes per second), `hbm_gbs_achieved`
+    (algorithmic bytes / median) and `roofline_frac` (of `hbm_peak_gbs()`).
     Candidates that cannot run this key are reported with an "error" entry.
     Synchronises the device; must not run concurrently with other timed work.
     """
@@ -298,6 +319,7 @@ def autotune(elements, operator, trials=5, warmups=2, candidates=None, lam=1.0):
     report = {}
     rng = np.random.default_rng(0)
     best, best_time = None, np.inf
+    peak = hbm_peak_gbs()[0]
     for strat in candidates:
         try:
             coll = Collection(elements, operator, strat, lam=lam)
@@ -323,8 +345,11 @@ def autotune(elements, operator, trials=5, warmups=2, candidates=None, lam=1.0):
             continue
         times = [ev[2 * t].elapsed_time(ev[2 * t + 1]) * 1e-3 for t in range(trials)]
         med = float(np.median(times))
+        gbs = coll.hbm_bytes() / med / 1e9
         report[strat.value] = {"median_s": med, "times_s": times, "mac_count": coll.mac_count(),
-                               "hbm_bytes": coll.hbm_bytes()}
+                               "hbm_bytes": coll.hbm_bytes(),
+                               "dof_per_s": coll.num_elements * coll._tables.num_modes / med,
+                               "hbm_gbs_achieved": gbs, "roofline_frac": gbs / peak}
         if med < best_time:
             best, best_time = strat, med
     if best is None:

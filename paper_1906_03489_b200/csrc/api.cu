@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/spechp_b200.h"
 #include "dg.h"
 #include "tri.h"
@@ -23,6 +25,19 @@
 #include "periodic.cuh"
 #include "solver.h"
 #include "tables.h"
+
+// NVTX range around every apply-type entry point (tracing): shows
+// up in nsys timelines and lets ncu filter launches (--nvtx --nvtx-include
+// "sphp_helmholtz_assembled/").  Header-only NVTX v3: a no-op pointer check
+// when no tool is attached.
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 using namespace sphp;
 
@@ -1031,6 +1046,7 @@ int sphp_collection_info(const sphp_coll* c, int64_t* in_size, int64_t* out_size
 
 // collections.Collection.apply (collections.py:189-246)
 int sphp_apply(sphp_coll* c, int64_t E, int64_t n_in, const double* in, double* out, sphp_stream stream) {
+  NvtxRange nvtx_range("sphp_apply");
   if (!c) return fail(SPHP_ERR_BAD_ARG, "null collection");
   if (E != c->E || n_in != c->in_size) {
     char buf[160];
@@ -1052,6 +1068,7 @@ int sphp_apply(sphp_coll* c, int64_t E, int64_t n_in, const double* in, double* 
 
 int sphp_apply_host(sphp_coll* c, int64_t E, int64_t n_in, const double* in, double* out,
                     sphp_stream stream) {
+  NvtxRange nvtx_range("sphp_apply_host");
   if (!c) return fail(SPHP_ERR_BAD_ARG, "null collection");
   if (E != c->E || n_in != c->in_size) return sphp_apply(c, E, n_in, in, out, stream);
   cudaStream_t s = (cudaStream_t)stream;
@@ -1436,6 +1453,7 @@ int sphp_amap_codes(const sphp_amap* a, int64_t* codes) {
 }
 
 int sphp_scatter(const sphp_amap* a, const double* g, double* loc, sphp_stream stream) {
+  NvtxRange nvtx_range("sphp_scatter");
   if (!a || !g || !loc) return fail(SPHP_ERR_BAD_ARG, "null argument");
   if (int rc = amap_device(a)) return rc;
   CK(amap_scatter(a->dev(), g, loc, (cudaStream_t)stream));
@@ -1443,6 +1461,7 @@ int sphp_scatter(const sphp_amap* a, const double* g, double* loc, sphp_stream s
 }
 
 int sphp_assemble(const sphp_amap* a, const double* loc, double* g, sphp_stream stream) {
+  NvtxRange nvtx_range("sphp_assemble");
   if (!a || !g || !loc) return fail(SPHP_ERR_BAD_ARG, "null argument");
   if (int rc = amap_device(a)) return rc;
   return amap_assemble_any(a, loc, g, 0, (cudaStream_t)stream);
@@ -1468,6 +1487,7 @@ static int split_reverse() {
 // assembly.GlobalSystem.apply (assembly.py:177-182), fused
 int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, double* y, int accumulate,
                              sphp_stream stream) {
+  NvtxRange nvtx_range("sphp_helmholtz_assembled");
   if (!c || !a || !x || !y) return fail(SPHP_ERR_BAD_ARG, "null argument");
   if (c->op != SPHP_OP_HELMHOLTZ) return fail(SPHP_ERR_BAD_ARG, "collection is not a Helmholtz operator");
   if (a->E != c->E || a->nm != c->t->nm)
@@ -1581,6 +1601,7 @@ int sphp_helmholtz_assembled(sphp_coll* c, const sphp_amap* a, const double* x, 
 // entry for bench.py: the dominant kernel's time on its own stream.
 int sphp_helmholtz_assembled_phases(sphp_coll* c, const sphp_amap* a, const double* x, double* y,
                                     sphp_stream stream, int max_phases, float* ms, int* nphases) {
+  NvtxRange nvtx_range("sphp_helmholtz_assembled_phases");
   if (!ms || !nphases || max_phases < 1) return fail(SPHP_ERR_BAD_ARG, "null output");
   static thread_local std::vector<cudaEvent_t> ev;
   while ((int)ev.size() < max_phases + 1) {
@@ -1873,6 +1894,7 @@ int sphp_gsys_create(sphp_coll* const* colls, const sphp_amap* const* maps, int 
 }
 
 int sphp_gsys_apply(sphp_gsys* g, const double* x, double* y, sphp_stream stream) {
+  NvtxRange nvtx_range("sphp_gsys_apply");
   if (!g || !x || !y) return fail(SPHP_ERR_BAD_ARG, "null argument");
   cudaStream_t s0 = (cudaStream_t)stream;
   Workspace* w = nullptr;
@@ -1920,6 +1942,7 @@ int sphp_gsys_destroy(sphp_gsys* g) {
 // Periodic split maps take the slab pipeline above.
 int sphp_helmholtz_assembled_host(sphp_coll* c, const sphp_amap* a, const double* x, double* y,
                                   sphp_stream stream) {
+  NvtxRange nvtx_range("sphp_helmholtz_assembled_host");
   if (!c || !a || !x || !y) return fail(SPHP_ERR_BAD_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
   if (c->op == SPHP_OP_HELMHOLTZ && c->strategy == SPHP_STRATEGY_CUDA_SUMFAC && a->periodic &&
@@ -1951,6 +1974,7 @@ int sphp_helmholtz_assembled_host(sphp_coll* c, const sphp_amap* a, const double
 
 // ---- solver support (assembly.py:185-266) ------------------------------------
 int sphp_helmholtz_diagonal(sphp_coll* c, double* out, sphp_stream stream) {
+  NvtxRange nvtx_range("sphp_helmholtz_diagonal");
   if (!c || !out) return fail(SPHP_ERR_BAD_ARG, "null argument");
   if (c->op != SPHP_OP_HELMHOLTZ) return fail(SPHP_ERR_BAD_ARG, "collection is not a Helmholtz operator");
   sphp_tables* t = c->t;
@@ -2011,6 +2035,7 @@ int sphp_cg_init_dev(int64_t n, const double* rhs, const double* dinv, double* x
 
 int sphp_cg_step_dev(int64_t n, const double* p, const double* ap, double* x, double* r, const double* dinv,
                      double* z, double* st, int max_iter, sphp_stream stream) {
+  NvtxRange nvtx_range("sphp_cg_step_dev");
   if (!p || !ap || !x || !r || !dinv || !z || !st) return fail(SPHP_ERR_BAD_ARG, "null argument");
   CK(cg_step_dev(n, p, ap, x, r, dinv, z, const_cast<double*>(p), st, max_iter, (cudaStream_t)stream));
   return SPHP_OK;

@@ -11,9 +11,6 @@
 #pragma once
 #include <type_traits>
 
-#ifndef SPHP_Q7_EFAST
-#define SPHP_Q7_EFAST 1  // tuning: 0 = rotated j-pencils at Q = 7 instead
-#endif
 #ifndef SPHP_GDIR_LOCAL
 #define SPHP_GDIR_LOCAL 1  // tuning: 0 = k-major orders still stage their geometry (MODE 0)
 #endif
@@ -159,53 +156,6 @@ struct RowRot {
 };
 
 
-// Pencils of N values at stride S (one lane per pencil) accessed in the
-// rotated order n = (it + tau) mod N, tau in [0, N) per lane: spreads lanes
-// whose pencils start on the same bank pair (the j-pencil stages at Q = 7,
-// where lane (i, k) starts on bank i + k); registers are put back in order
-// by ceil(log2 N) conditional rotations.
-template <int N>
-struct Rot {
-  template <int SH, bool LEFT>
-  __device__ static __forceinline__ void rot_if(double* x, bool c) {
-    double t[N];
-#pragma unroll
-    for (int r = 0; r < N; ++r) t[r] = LEFT ? x[(r + SH) % N] : x[(r - SH % N + N) % N];
-#pragma unroll
-    for (int r = 0; r < N; ++r) x[r] = c ? t[r] : x[r];
-  }
-  template <bool LEFT>
-  __device__ static __forceinline__ void rot(double* x, int s) {
-    if constexpr (N > 1) rot_if<1, LEFT>(x, s & 1);
-    if constexpr (N > 2) rot_if<2, LEFT>(x, s & 2);
-    if constexpr (N > 4) rot_if<4, LEFT>(x, s & 4);
-    if constexpr (N > 8) rot_if<8, LEFT>(x, s & 8);
-  }
-  template <int S>
-  __device__ static __forceinline__ void load(const double* __restrict__ p, int tau, double* x) {
-#pragma unroll
-    for (int it = 0; it < N; ++it) {
-      int n = it + tau;
-      n -= n >= N ? N : 0;
-      x[it] = p[n * S];
-    }
-    rot<false>(x, tau);  // x[n] = loaded[(n - tau) mod N]
-  }
-  template <int S>
-  __device__ static __forceinline__ void store(double* __restrict__ p, int tau, const double* x) {
-    double xr[N];
-#pragma unroll
-    for (int n = 0; n < N; ++n) xr[n] = x[n];
-    rot<true>(xr, tau);  // xr[it] = x[(it + tau) % N]
-#pragma unroll
-    for (int it = 0; it < N; ++it) {
-      int n = it + tau;
-      n -= n >= N ? N : 0;
-      p[n * S] = xr[it];
-    }
-  }
-};
-
 // ===========================================================================
 // Fused matrix-free Helmholtz (K4): y = sum_ab B_a^T G_ab B_b uhat + lam B^T wJ B uhat
 // (geometry.py:171-184 as one sum-factorised pass; no quadrature data
@@ -240,38 +190,32 @@ struct HexHelmEO {
   static constexpr int CS = pt_stride(Q3);
   static constexpr int GEO = (GK == SPHP_GEOM_METRIC) ? 7 * CS : 10;
   static constexpr int QK = odd_up(Q);
-  // pitches: the mod-16 rule below, except where the wavefront model's
-  // search (tools/layout_search_eo.py, odd Q with the RowRot S1/S9 rows)
-  // found fewer shared-memory wavefronts: P=3 -14 %, P=5 -6 %
-  static constexpr int PP1 = (M == 4 && Q == 5) ? 28 : (M == 6 && Q == 7) ? 42 : pitch_mod16(M * QK, Q);
+  // pitches = Q (mod 16): the (p, k) lanes of the j-pencil stages land on
+  // consecutive banks
+  static constexpr int PP1 = pitch_mod16(M * QK, Q);
   static constexpr int PP2 = pitch_mod16(Q * Q, Q);
   // plane pitch of the dense (i, j, k) work tensors: Q^2 (contiguous), except
-  // Q = 6 and Q = 10 where Q^2 = 4 mod 16 puts the j-pencil lanes (i, k) on
-  // banks 4i + k (ncu P=8: 105 M of 144 M excess wavefronts); SI = Q mod 16
-  // makes them consecutive while the 128-bit k-rows stay conflict free but
-  // for the phases that cross an i.  Measured: P=4 0.636 -> 0.623 ms, P=8
-  // 3.341 -> 3.256 ms.  (Odd Q: the scalar k-rows would conflict instead.)
-  static constexpr int SI = (Q == 6 || Q == 10 || Q == SPHP_SI_Q) ? pitch_mod16(Q * Q, Q) : Q * Q;
+  // Q = 10 where Q^2 = 4 mod 16 puts the j-pencil lanes (i, k) on banks
+  // 4i + k (ncu P=8: 105 M of 144 M excess wavefronts); SI = Q mod 16 makes
+  // them consecutive while the 128-bit k-rows stay conflict free but for the
+  // phases that cross an i.  Measured: P=8 3.341 -> 3.256 ms.  (Odd Q: the
+  // scalar k-rows would conflict instead.)
+  static constexpr int SI = (Q == 10 || Q == SPHP_SI_Q) ? pitch_mod16(Q * Q, Q) : Q * Q;
   // W2 (d0 / f0) never meets a j-pencil: it keeps the contiguous pitch, so
   // its k-rows stay conflict free (wavefront model: -10 % on these accesses)
   static constexpr int SI2 = Q * Q;
-  static constexpr int SE = (M == 4 && Q == 5) ? 157 : (M == 6 && Q == 7) ? 343
-                                                     : even_up(cmax(Q * SI, cmax(M * PP1, M * PP2)));
+  static constexpr int SE = even_up(cmax(Q * SI, cmax(M * PP1, M * PP2)));
   static_assert(SE >= Q * SI && SE >= M * PP1 && SE >= M * PP2, "element tensors overlap");
   static_assert(Q % 2 == 1 || SE % 2 == 0, "128-bit rows need an even element stride");
   static constexpr int WORK = 3 * SE;
   static constexpr int OUT_OFF = NE * SE;  // S9 writes the block into W1 (free after S8)
-  // j-pencil stages S4/S6 in rotated order tau = JROT * i mod Q at Q = 7
-  // (wavefront model tools/bank_sim.py: 2.71x -> 1.84x of the ideal there;
-  // measured P=5 -1 %).  Also modelled better but measured no gain at Q = 6
-  // and slower at Q = 10 (P=8 3.34 -> 3.66 ms: the rotation selects cost
-  // more than the conflicts): natural order there.
-  static constexpr bool EFAST = (Q == 7 && NE == 2 && SPHP_Q7_EFAST);
+  // (j-pencil stages S4/S6 in a rotated order per lane: modelled fewer
+  // wavefronts, measured slower at Q = 10 — P=8 3.34 -> 3.66 ms, the rotation
+  // selects cost more than the conflicts; natural order)
   // k-major METRIC points (metric_slot): the local operator then reads the
   // geometry from global memory (pipeline MODE 7) instead of staging it
   static constexpr bool KMAJ = GK == SPHP_GEOM_METRIC && metric_kmajor(Q);
   static constexpr bool GDIR_LOCAL = KMAJ && SPHP_GDIR_LOCAL;
-  static constexpr int JROT = (Q == 7 && !EFAST) ? 1 : 0;
   using T = Tab<M, Q>;
   using X = EO<M, Q>;
 
@@ -317,16 +261,11 @@ struct HexHelmEO {
     __syncthreads();
     // S4: d1 = D along j
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      // element-fastest lanes at Q = 7 (EFAST): two elements' pencils share
-      // a half-warp, their banks 7 apart (model: 2.71x -> 1.86x of the ideal
-      // wavefronts, as the rotation, without its selects)
-      const int e = EFAST ? w % NE : w / (Q * Q);
-      const int ik = EFAST ? w / NE : w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
+      const int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
       double v[Q], r[Q];
-      const int tau = (JROT * i) % Q;
-      Rot<Q>::template load<Q>(W0 + e * SE + i * SI + k, tau, v);
+      ld_pencil<Q, Q>(W0 + e * SE + i * SI + k, v);
       X::template deriv<false, false>(tab, v, r);
-      Rot<Q>::template store<Q>(W1 + e * SE + i * SI + k, tau, r);
+      st_pencil<Q, Q>(W1 + e * SE + i * SI + k, r);
     }
     __syncthreads();
     geo_ready();  // the staged geometry is first read here (pipeline: GEO_HOOK)
@@ -415,14 +354,12 @@ struct HexHelmEO {
     release();
     // S6: t += D1^T f1 along j
     SPHP_FOR_ITEMS(NE * Q * Q, w) {
-      const int e = EFAST ? w % NE : w / (Q * Q);
-      const int ik = EFAST ? w / NE : w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
+      const int e = w / (Q * Q), ik = w - e * (Q * Q), i = ik / Q, k = ik - i * Q;
       double f[Q], t[Q];
-      const int tau = (JROT * i) % Q;
-      Rot<Q>::template load<Q>(W1 + e * SE + i * SI + k, tau, f);
-      Rot<Q>::template load<Q>(W0 + e * SE + i * SI + k, tau, t);
+      ld_pencil<Q, Q>(W1 + e * SE + i * SI + k, f);
+      ld_pencil<Q, Q>(W0 + e * SE + i * SI + k, t);
       X::template deriv<true, true>(tab, f, t);
-      Rot<Q>::template store<Q>(W0 + e * SE + i * SI + k, tau, t);
+      st_pencil<Q, Q>(W0 + e * SE + i * SI + k, t);
     }
     __syncthreads();
     // S7: i -> p, B t + dB f0

@@ -109,6 +109,10 @@ def test_autotune_report_shape(sp):
     assert set(rep) == {"cuda_sumfac", "cuda_stdmat"}
     for v in rep.values():
         assert len(v["times_s"]) == 3 and v["median_s"] > 0 and v["mac_count"] > 0
+        # the SURVEY §5 extension of the report: rates consistent with the median
+        assert v["dof_per_s"] == pytest.approx(16 * 16 * 25 / v["median_s"])
+        assert v["hbm_gbs_achieved"] == pytest.approx(v["hbm_bytes"] / v["median_s"] / 1e9)
+        assert v["roofline_frac"] == pytest.approx(v["hbm_gbs_achieved"] / sp.collections.hbm_peak_gbs()[0])
     only, rep1 = sp.autotune(batch, sp.OperatorKind.BWD_TRANS, trials=2, warmups=0,
                              candidates=[sp.Strategy.CUDA_STDMAT])
     assert only is sp.Strategy.CUDA_STDMAT and list(rep1) == ["cuda_stdmat"]

@@ -27,6 +27,19 @@ def test_library_exports_every_declared_symbol():
     assert _lib.abi_version() == 1
 
 
+def test_hex_helmholtz_plan_query():
+    """sphp_hex_helmholtz_plan: one of the three stage plans for every fast
+    key (Q = M + 1 or M + 2, M = 2..9), -1 elsewhere; the BASELINE orders
+    P = 2..5 (Q = P + 2) run the i-column plan."""
+    plan = _lib.lib.sphp_hex_helmholtz_plan
+    for m in range(2, 10):
+        for q in (m + 1, m + 2):
+            assert plan(m, q) in (0, 1, 3), (m, q)
+    assert [plan(p + 1, p + 2) for p in (2, 3, 4, 5)] == [3, 3, 3, 3]
+    assert plan(7, 8) == 1 and plan(9, 10) == 0
+    assert plan(5, 9) == -1 and plan(12, 13) == -1 and plan(1, 2) == -1
+
+
 def test_library_is_in_tree_sm100a():
     assert _lib.LIB_PATH.parent == ROOT / "paper_1906_03489_b200"
     blob = _lib.LIB_PATH.read_bytes()
