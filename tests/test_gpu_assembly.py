@@ -262,6 +262,49 @@ def test_class_bitwise_equals_split(sp, n, P):
     assert ys["class"].tobytes() == ys["split"].tobytes()
 
 
+def test_class_and_split_walk_many_tiles_per_cta():
+    """Grid capped at 3 CTAs (SPHP_MAX_GRID is read once per process: a
+    subprocess), so every CTA of the class operator walks hundreds of tiles —
+    the x chunks of the next tile issued after S1, the geometry's own
+    mbarrier waited for at the pointwise stage, the bulk stores drained at
+    the top of the next tile — at every order / stage plan; bitwise equal to
+    the split algorithm under the same cap, and (P = 2, 4, 7) to the oracle."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys; sys.path.insert(0, 'tests'); sys.path.insert(0, '.')
+import numpy as np, torch
+import paper_1906_03489_b200 as sp
+from helpers import assert_parity, oracle_geometry
+from oracle import assembly as oa, ops as oo
+from test_gpu_assembly import oracle_assembled
+n = 8
+for P in (2, 3, 4, 5, 6, 7, 8):
+    exp = sp.make_hex(P, P + 2)
+    batch = sp.ElementBatch.structured(exp, n, kind=sp.GEOM_METRIC, mapping=sp.MAP_HEX_SINE, amp=0.03)
+    coll = sp.Collection(batch, sp.OperatorKind.HELMHOLTZ, sp.Strategy.CUDA_SUMFAC)
+    amap = sp.AssemblyMap.hex_periodic(n, P)
+    x = torch.as_tensor(np.random.default_rng(P).uniform(-1, 1, amap.num_global), device="cuda")
+    out = {}
+    for alg in ("class", "split"):
+        amap.set_algorithm(alg)
+        out[alg] = sp.GlobalHelmholtz([(coll, amap)], amap.num_global).apply(x).cpu().numpy()
+    assert out["class"].tobytes() == out["split"].tobytes(), P
+    if P in (2, 4, 7):
+        oe, inv, wj = oracle_geometry("hex", P, P + 2, n, np.arange(n ** 3), 2, 0.03)
+        ref = oracle_assembled(oa.hex_periodic_map(n, P), [oe] * n ** 3, x.cpu().numpy(), 1.0,
+                               oo.metric_from_inv(wj, inv), wj)
+        assert_parity(out["class"], ref, what=f"grid-capped class apply P{P}")
+print("ok")
+"""
+    env = dict(os.environ, SPHP_MAX_GRID="3")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=900)
+    assert res.returncode == 0 and "ok" in res.stdout, res.stdout + res.stderr
+
+
 @pytest.mark.parametrize("P", [3, 4])
 def test_class_accumulate_and_batches(sp, P):
     """accumulate = 1 (a second batch adds into y): the interiors then go

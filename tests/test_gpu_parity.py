@@ -143,7 +143,8 @@ def test_zero_input_zero_output(sp):
 def test_unaligned_and_tiny_inputs(sp, op, PQ):
     """Inputs not 16-byte aligned take the synchronous (non-TMA) load path;
     E = 1 and E = 2 exercise single partial tiles.  Orders cover the skewed
-    Q=4 plan, the rotated even-M rows (P=3, 7) and the K-row plan."""
+    i-column plan at three tile sizes, the rotated even-M rows (P=3, 7) and
+    the K-row plan."""
     shape, (P, Q) = "hex", PQ
     n = 4
     for E in (1, 2, 37):
@@ -181,7 +182,8 @@ import paper_1906_03489_b200 as sp
 from helpers import OPS, assert_parity, input_size, oracle_apply, oracle_geometry
 from test_gpu_parity import _build
 for op in OPS:
-    for shape, P in (("hex", 3), ("hex", 6), ("quad", 5)):
+    # hex P = 2, 4, 5: the other tile sizes of the i-column plan (Helmholtz only)
+    for shape, P in (("hex", 3), ("hex", 6), ("quad", 5)) + ((("hex", 2), ("hex", 4), ("hex", 5)) if op == "helmholtz" else ()):
         n = 4 if shape == "hex" else 8
         E = n ** (3 if shape == "hex" else 2)
         geom = "metric" if op == "helmholtz" else ("point" if op != "bwdtrans" else "none")
