@@ -500,12 +500,18 @@ def run_ours(args, rank, world, local_rank):
         parity = parity_sample(P, n, x_host.numpy(), y.cpu().numpy(), c.cpu().numpy(), yl.cpu().numpy())
     del c, yl
 
+    plan_names = {0: "k-row", 1: "j-pencil", 3: "i-column"}
+
+    def plan_of(Ps):
+        return plan_names.get(sp._lib.lib.sphp_hex_helmholtz_plan(Ps + 1, Ps + 2), "none")
+
     sweep = None
     if args.sweep:
         sweep = {}
         for Ps in range(2, 9):
             if Ps == P:
-                sweep[str(Ps)] = {"assembled_ms": ms, "local_ms": k_ms}
+                sweep[str(Ps)] = {"assembled_ms": ms, "local_ms": k_ms, "plan": plan_of(Ps),
+                                  "assembled_roofline_frac": workload_bytes(Ps, n) / (ms * 1e-3) / 1e9 / peak}
                 continue
             _, b2, c2, a2 = build(Ps)
             op2 = sp.GlobalHelmholtz([(c2, a2)], a2.num_global)
@@ -523,6 +529,8 @@ def run_ours(args, rank, world, local_rank):
                 "local_hbm_gbs": lb / (t_lo * 1e-3) / 1e9,
                 "local_roofline_frac": lb / (t_lo * 1e-3) / 1e9 / peak,
                 "local_fp64_tflops": helm_flops(Ps, E) / (t_lo * 1e-3) / 1e12,
+                "assembled_roofline_frac": workload_bytes(Ps, n) / (t_as * 1e-3) / 1e9 / peak,
+                "plan": plan_of(Ps),
             }
             del b2, c2, a2, op2, x2, y2, cc, yy
             torch.cuda.empty_cache()

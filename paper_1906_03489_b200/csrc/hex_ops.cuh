@@ -586,6 +586,9 @@ struct HexHelmJEO {
 // and three projections per column); the kernels are bound by the
 // shared-memory pipe and HBM, not FP64.
 // ===========================================================================
+#ifndef SPHP_COL_S5_BYCOMP
+#define SPHP_COL_S5_BYCOMP 1  // 0 (tuning): metric read point by point instead of one component at a time
+#endif
 struct ColLay {
   int RA, PA, SEA;  // A tensors: row pitch (k rows), p pitch, element stride
   int PB, SEB;      // B tensors: p pitch (rows of Q contiguous), element stride
@@ -712,14 +715,55 @@ struct HexHelmCol {
       const int jk = j * Q + k;
       double* b = WB + e * SEB + jk;
       double x[M], u[Q], d0[Q], d1[Q], d2[Q], f0[Q], f1[Q], f2[Q];
+      double g[Q];
+      const double* gr = geo + e * GEO_S + jk;
+      auto comp = [&](int c) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) g[i] = gr[c * CS + i * Q * Q];
+      };
       ld_pencil<M, PB>(b, x);
       X::interp_and_deriv(tab, x, u, d0);
       ld_pencil<M, PB>(b + TB, x);
       X::interp(tab, x, d1);
       ld_pencil<M, PB>(b + 2 * TB, x);
       X::interp(tab, x, d2);
-      if constexpr (GK == SPHP_GEOM_METRIC) {
-        const double* gr = geo + e * GEO_S + jk;
+      if constexpr (GK == SPHP_GEOM_METRIC && SPHP_COL_S5_BYCOMP) {
+        // one metric component at a time: Q independent loads in flight,
+        // then their FMAs (point by point, 7 loads then 9 FMAs, measured
+        // slower: P=4 assembled 0.666 vs 0.646 ms, P=5 local 1.02 vs 0.97;
+        // hoisting the column loads and the first component above the
+        // interpolations as well: no further gain)
+        comp(0);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) f0[i] = g[i] * d0[i];
+        comp(1);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          f1[i] = g[i] * d0[i];
+          f0[i] = fma(g[i], d1[i], f0[i]);
+        }
+        comp(2);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          f2[i] = g[i] * d0[i];
+          f0[i] = fma(g[i], d2[i], f0[i]);
+        }
+        comp(3);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) f1[i] = fma(g[i], d1[i], f1[i]);
+        comp(4);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          f1[i] = fma(g[i], d2[i], f1[i]);
+          f2[i] = fma(g[i], d1[i], f2[i]);
+        }
+        comp(5);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) f2[i] = fma(g[i], d2[i], f2[i]);
+        comp(6);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) u[i] = lam * g[i] * u[i];
+      } else if constexpr (GK == SPHP_GEOM_METRIC) {
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
           const double g0 = gr[0 * CS + i * Q * Q], g1 = gr[1 * CS + i * Q * Q], g2 = gr[2 * CS + i * Q * Q];
