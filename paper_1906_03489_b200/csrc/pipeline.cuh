@@ -70,6 +70,39 @@ struct ClassIO {
       a0 = at(tr[0], e), a1 = at(tr[1], e), a2 = at(tr[2], e);
     }
   }
+  // The M - 2 bubble modes of a row are consecutive doubles of one entity,
+  // and the rows of consecutive lanes (q, q + 1, ...) follow each other at
+  // stride M - 2: for even M - 2 the lanes of a half-warp share bank pairs
+  // (4-way at M = 6: ncu P=5, 11.0 M of this store's 13.6 M wavefronts were
+  // excess).  ROT: each lane walks its tail in the order (it + s) mod (M - 2)
+  // with s from the address bits above the bank index — lanes on the same
+  // bank pair start at different modes — and a log2 chain of conditional
+  // register rotations restores the order (TailRot below).
+#ifndef SPHP_CLASS_ROT
+#define SPHP_CLASS_ROT 1
+#endif
+  template <int N>
+  struct TailRot {
+    static constexpr int NV = (N % 16 == 0) ? 16 : (N % 8 == 0) ? 8 : (N % 4 == 0) ? 4 : (N % 2 == 0) ? 2 : 1;
+    static constexpr bool ON = SPHP_CLASS_ROT && NV > 1 && N > 1;
+    __device__ static __forceinline__ int shift(int a2) { return (a2 >> 4) & (NV - 1); }
+    // x[r] <- x[(r + SH) % N] (LEFT) or x[(r - SH) mod N] where c
+    template <int SH, bool LEFT>
+    __device__ static __forceinline__ void rot_if(double* x, bool c) {
+      double t[N];
+#pragma unroll
+      for (int r = 0; r < N; ++r) t[r] = LEFT ? x[(r + SH) % N] : x[(r - SH % N + N) % N];
+#pragma unroll
+      for (int r = 0; r < N; ++r) x[r] = c ? t[r] : x[r];
+    }
+    template <bool LEFT>
+    __device__ static __forceinline__ void rot(double* x, int s) {
+      if constexpr (NV > 1) rot_if<1 % N, LEFT>(x, s & 1);
+      if constexpr (NV > 2) rot_if<2 % N, LEFT>(x, s & 2);
+      if constexpr (NV > 4) rot_if<4 % N, LEFT>(x, s & 4);
+      if constexpr (NV > 8) rot_if<8 % N, LEFT>(x, s & 8);
+    }
+  };
   template <int M>
   __device__ __forceinline__ void load_row(const double* __restrict__ base, int e, int pq, double* x) const {
     static_assert(M > 2, "class staging needs bubbles (P >= 2)");
@@ -77,8 +110,23 @@ struct ClassIO {
     resolve<M>(e, pq, a0, a1, a2);
     x[0] = base[a0];
     x[1] = base[a1];
+    using TR = TailRot<M - 2>;
+    if constexpr (TR::ON) {
+      const int s = TR::shift(a2);
+      double t[M - 2];
 #pragma unroll
-    for (int r = 2; r < M; ++r) x[r] = base[a2 + r - 2];
+      for (int it = 0; it < M - 2; ++it) {
+        int r = it + s;
+        r -= r >= M - 2 ? M - 2 : 0;
+        t[it] = base[a2 + r];  // t[it] = tail[(it + s) % N]
+      }
+      TR::template rot<false>(t, s);  // tail[r] = t[(r - s) mod N]
+#pragma unroll
+      for (int r = 2; r < M; ++r) x[r] = t[r - 2];
+    } else {
+#pragma unroll
+      for (int r = 2; r < M; ++r) x[r] = base[a2 + r - 2];
+    }
   }
   template <int M>
   __device__ __forceinline__ void store_row(double* __restrict__ base, int e, int pq, const double* c) const {
@@ -86,8 +134,23 @@ struct ClassIO {
     resolve<M>(e, pq, a0, a1, a2);
     base[a0] = c[0];
     base[a1] = c[1];
+    using TR = TailRot<M - 2>;
+    if constexpr (TR::ON) {
+      const int s = TR::shift(a2);
+      double t[M - 2];
 #pragma unroll
-    for (int r = 2; r < M; ++r) base[a2 + r - 2] = c[r];
+      for (int r = 2; r < M; ++r) t[r - 2] = c[r];
+      TR::template rot<true>(t, s);  // t[it] = tail[(it + s) % N]
+#pragma unroll
+      for (int it = 0; it < M - 2; ++it) {
+        int r = it + s;
+        r -= r >= M - 2 ? M - 2 : 0;
+        base[a2 + r] = t[it];
+      }
+    } else {
+#pragma unroll
+      for (int r = 2; r < M; ++r) base[a2 + r - 2] = c[r];
+    }
   }
 };
 
