@@ -569,6 +569,16 @@ __device__ __forceinline__ void owned_sum2(const double* __restrict__ Z, const i
   } else {
     const int t = li / RUN, u = li - t * RUN;
     const int tp = t == 0 ? T - 1 : t - 1;  // tile of the x - 1 neighbour at u < S
+    // even NE: every class run starts on an even double (n, NE * ZS and
+    // NE * class_cb are even, u is), so an unshifted pair is one 16-byte
+    // load; the x-shifted pair too when S is even (both outputs then fall
+    // on the same side of the tile edge).  Half the load instructions: the
+    // kernel ran at 72 % L1TEX with 8-byte loads (ncu, P = 4)
+    constexpr bool VEC0 = NE % 2 == 0, VEC1 = VEC0 && S % 2 == 0;
+    auto ld2 = [&](int o, double& a, double& b) {
+      const double2 q = __ldg(reinterpret_cast<const double2*>(Z + o));
+      a = q.x, b = q.y;
+    };
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       const int bc = Region<R>::b(j) * 2 + Region<R>::c(j);
@@ -580,8 +590,14 @@ __device__ __forceinline__ void owned_sum2(const double* __restrict__ Z, const i
         const int off = zr[bc] + t * REC + cls + u;
         if (Region<R>::a(j)) {
           const int wrapd = zr[bc] + tp * REC + cls + (NE - 1) * S;  // + u: last element of the tile before
-          v0[j] = __ldg(Z + (u >= S ? off - S : wrapd + u));
-          v1[j] = __ldg(Z + (u + 1 >= S ? off + 1 - S : wrapd + u + 1));
+          if constexpr (VEC1) {
+            ld2(u >= S ? off - S : wrapd + u, v0[j], v1[j]);
+          } else {
+            v0[j] = __ldg(Z + (u >= S ? off - S : wrapd + u));
+            v1[j] = __ldg(Z + (u + 1 >= S ? off + 1 - S : wrapd + u + 1));
+          }
+        } else if constexpr (VEC0) {
+          ld2(off, v0[j], v1[j]);
         } else {
           v0[j] = __ldg(Z + off);
           v1[j] = __ldg(Z + off + 1);
@@ -610,6 +626,7 @@ __global__ void __launch_bounds__(CLASS_OWNER_NT, CLASS_OWNER_MINB) class_owner_
   const int64_t N3 = (int64_t)n * n * n;
   const int T = n / NE;  // tiles per row
   const int per_row = n * (G::start(7) + (nreg > 7 ? G::S(7) : 0));
+  const bool y16 = (reinterpret_cast<uintptr_t>(y) & 15) == 0;
   for (int row = row0 + blockIdx.x; row < row1; row += gridDim.x) {
     const int ez = row / n, ey = row - ez * n;
     const int ym = ey == 0 ? n - 1 : ey - 1, zm = ez == 0 ? n - 1 : ez - 1;
@@ -637,8 +654,13 @@ __global__ void __launch_bounds__(CLASS_OWNER_NT, CLASS_OWNER_MINB) class_owner_
         REGION(0) REGION(1) REGION(2) REGION(3) REGION(4) REGION(5) REGION(6) REGION(7)
       }
 #undef REGION
-      y[g] = accumulate ? y[g] + a0 : a0;
-      y[g + 1] = accumulate ? y[g + 1] + a1 : a1;
+      // g is even (n is): one 16-byte store when y is 16-byte aligned
+      if (y16 && !accumulate) {
+        *reinterpret_cast<double2*>(y + g) = make_double2(a0, a1);
+      } else {
+        y[g] = accumulate ? y[g] + a0 : a0;
+        y[g + 1] = accumulate ? y[g + 1] + a1 : a1;
+      }
     }
   }
 }
