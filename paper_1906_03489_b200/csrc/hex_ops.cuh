@@ -11,6 +11,9 @@
 #pragma once
 #include <type_traits>
 
+#ifndef SPHP_JEO_S5_BYCOMP
+#define SPHP_JEO_S5_BYCOMP 1  // 0 (tuning): J-pencil plan's pointwise stage point by point (P=6: 1.506 vs 1.488 ms local, 1.745 vs 1.688 assembled)
+#endif
 #ifndef SPHP_GDIR_LOCAL
 #define SPHP_GDIR_LOCAL 1  // tuning: 0 = k-major orders still stage their geometry (MODE 0)
 #endif
@@ -483,6 +486,49 @@ struct HexHelmJEO {
         a22 = det * (iv[6] * iv[6] + iv[7] * iv[7] + iv[8] * iv[8]);
         adet = det;
       }
+      if constexpr (GK == SPHP_GEOM_METRIC && SPHP_JEO_S5_BYCOMP) {
+        // one metric component at a time (Q independent loads in flight,
+        // then their FMAs), as in the column plan's pointwise stage
+        double d0[Q], d2[Q], f0[Q], f2[Q], gc[Q];
+        ld_pencil<Q, QK>(W2 + base, d0);
+        ld_pencil<Q, QK>(W1 + base, d2);
+        auto comp = [&](int c) {
+#pragma unroll
+          for (int j = 0; j < Q; ++j) gc[j] = g[c * CS + metric_slot(3, Q, (i * Q + j) * Q + k)];
+        };
+        comp(0);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) f0[j] = gc[j] * d0[j];
+        comp(1);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          f1[j] = gc[j] * d0[j];
+          f0[j] = fma(gc[j], d1v[j], f0[j]);
+        }
+        comp(2);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          f2[j] = gc[j] * d0[j];
+          f0[j] = fma(gc[j], d2[j], f0[j]);
+        }
+        comp(3);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) f1[j] = fma(gc[j], d1v[j], f1[j]);
+        comp(4);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          f1[j] = fma(gc[j], d2[j], f1[j]);
+          f2[j] = fma(gc[j], d1v[j], f2[j]);
+        }
+        comp(5);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) f2[j] = fma(gc[j], d2[j], f2[j]);
+        comp(6);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) u[j] = lam * gc[j] * u[j];
+        st_pencil<Q, QK>(W2 + base, f0);
+        st_pencil<Q, QK>(W1 + base, f2);
+      } else {
 #pragma unroll
       for (int j = 0; j < Q; ++j) {
         const double d1 = d1v[j];
@@ -512,6 +558,7 @@ struct HexHelmJEO {
         f1[j] = G01 * d0 + G11 * d1 + G12 * d2;
         W1[base + j * QK] = G02 * d0 + G12 * d1 + G22 * d2;
         u[j] = lam * wj * u[j];
+      }
       }
       X::template deriv<true, true>(tab, f1, u);
       st_pencil<Q, QK>(W0 + base, u);
