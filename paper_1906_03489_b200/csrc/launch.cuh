@@ -75,6 +75,7 @@ cudaError_t launch_pipe(const OpArgs& oa, int64_t gstride, int64_t goff, cudaStr
   a.codes = oa.codes;
   a.ent_g = oa.ent_g;
   a.n = oa.n;
+  a.n_magic = oa.n >= 2 ? (unsigned)((1ull << 32) / (unsigned)oa.n) : 0u;
   a.colour = oa.colour;
   a.reverse = oa.reverse;
   a.e0 = oa.e0;

@@ -172,6 +172,7 @@ struct DevArgs {
   const int* codes;
   const int* ent_g;  // PERIODIC_GATHER: precomputed (E, 27) entity bases, or null
   int n;
+  unsigned n_magic;  // floor(2^32 / n): division by n as a multiply (fast_divn)
   int colour;
   int reverse;  // MODE 0: walk the tiles last to first (L2 reuse, see launch)
   // MODE 5
@@ -180,6 +181,18 @@ struct DevArgs {
   int direct_interior;
 };
 
+
+// x / n and x % n for 0 <= x < 2^31 with magic = floor(2^32 / n), n >= 2:
+// umulhi(x, magic) is the quotient or one less (x (2^32 / n - magic) < 2^32),
+// one correction step.  The class launch does this per tile in every thread.
+__device__ __forceinline__ void fast_divn(int x, int n, unsigned magic, int& q, int& r) {
+  q = (int)__umulhi((unsigned)x, magic);
+  r = x - q * n;
+  if (r >= n) {
+    ++q;
+    r -= n;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // The scaffold.  Op supplies: M, NE, NT, IN, OUT, GEO (staged doubles per
@@ -604,8 +617,10 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
     if (ts < ntiles) {
       double* in_s = stage_base;
       const int w0 = (int)a.e0 + ts * NE;  // 32-bit: n^3 < 2^31
-      const int n = a.n, rowi = w0 / n, ex0 = w0 - rowi * n;
-      const int ez = rowi / n, ey = rowi - ez * n;
+      const int n = a.n;
+      int rowi, ex0, ez, ey;
+      fast_divn(w0, n, a.n_magic, rowi, ex0);
+      fast_divn(rowi, n, a.n_magic, ez, ey);
       const bool wrap = ex0 + NE == n;
       const int v = PV > 1 ? (ex0 & 1) : 0;
 #pragma unroll
@@ -765,7 +780,9 @@ __global__ void __launch_bounds__(Op::NT, (MODE == 5 ? Scaffold<Op, MODE>::MIN_C
       // chunks are issued right after S1 (all of S2..S9 to land)
       auto after_in = [&]() { issue_x(ts + G); };
       if constexpr (PV > 1) {
-        const int v = (int)(((a.e0 + w0) % a.n) & 1);  // parity of the tile's first x
+        int qv, rv;
+        fast_divn((int)(a.e0 + w0), a.n, a.n_magic, qv, rv);
+        const int v = rv & 1;  // parity of the tile's first x
         cin_io.v = cout_io.v = v;
       }
       const double* geo_p = S::GDIR ? a.geom + (a.e0 + w0) * a.gstride : geo_s;
