@@ -40,6 +40,43 @@ def test_hex_helmholtz_plan_query():
     assert plan(5, 9) == -1 and plan(12, 13) == -1 and plan(1, 2) == -1
 
 
+def test_fast_divn_identity():
+    """The class launch's fast_divn (pipeline.cuh): q = umulhi(x, floor(2^32 / n))
+    is x // n or one less, so one correction step gives the exact quotient
+    and remainder — for every mesh size the maps accept (n <= 1024) and
+    every element index below 2^31 (edges of each quotient bucket included)."""
+    rng = np.random.default_rng(7)
+    for n in list(range(2, 130)) + [255, 256, 257, 511, 512, 1000, 1023, 1024]:
+        magic = (1 << 32) // n
+        top = min(n ** 3, 2 ** 31 - 1)
+        x = np.concatenate([rng.integers(0, top, 4000), np.arange(0, min(top, 4 * n)),
+                            np.arange(n, top, max(1, top // 2000)) - 1,
+                            np.arange(n, top, max(1, top // 2000)), [top - 1, top]]).astype(np.uint64)
+        q = (x * np.uint64(magic)) >> np.uint64(32)
+        r = x - q * np.uint64(n)
+        assert np.all((q == x // np.uint64(n)) | (q + np.uint64(1) == x // np.uint64(n))), n
+        fix = r >= n
+        q, r = q + fix, r - fix * np.uint64(n)
+        assert np.array_equal(q, x // np.uint64(n)) and np.array_equal(r, x % np.uint64(n)), n
+
+
+def test_autotune_roofline_peak_source():
+    """hbm_peak_gbs(): SPHP_HBM_PEAK_GBS overrides; otherwise the driver's
+    MEASURED_PEAKS.json at the repository root, else the 8 TB/s nominal."""
+    import os
+    from paper_1906_03489_b200.collections import hbm_peak_gbs
+    old = os.environ.pop("SPHP_HBM_PEAK_GBS", None)
+    try:
+        gbs, kind = hbm_peak_gbs()
+        assert kind in ("measured", "nominal") and 1000.0 < gbs <= 8000.0
+        os.environ["SPHP_HBM_PEAK_GBS"] = "7000"
+        assert hbm_peak_gbs() == (7000.0, "env")
+    finally:
+        os.environ.pop("SPHP_HBM_PEAK_GBS", None)
+        if old is not None:
+            os.environ["SPHP_HBM_PEAK_GBS"] = old
+
+
 def test_library_is_in_tree_sm100a():
     assert _lib.LIB_PATH.parent == ROOT / "paper_1906_03489_b200"
     blob = _lib.LIB_PATH.read_bytes()
