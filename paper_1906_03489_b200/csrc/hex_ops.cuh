@@ -744,13 +744,15 @@ struct HexHelmCol {
       item<L.O2, M, Q>(w, e, p, k);
       const double* a = WA + e * SEA + p * PA + k;
       double* b = WB + e * SEB + p * PB + k;
-      double x[M], u[Q], d[Q];
+      double x[M], xd[M], u[Q], d[Q];
+      // both pencils before any store (the compiler cannot move a load of the
+      // A tensors above a store to the B tensors: same work area)
       ld_pencil<M, RA>(a, x);
+      ld_pencil<M, RA>(a + TA, xd);
       X::interp_and_deriv(tab, x, u, d);
       st_pencil<Q, Q>(b, u);
       st_pencil<Q, Q>(b + TB, d);
-      ld_pencil<M, RA>(a + TA, x);
-      X::interp(tab, x, u);
+      X::interp(tab, xd, u);
       st_pencil<Q, Q>(b + 2 * TB, u);
     }
     __syncthreads();
@@ -857,13 +859,13 @@ struct HexHelmCol {
       item<L.O2, M, Q>(w, e, p, k);
       const double* b = WB + e * SEB + p * PB + k;
       double* a = WA + e * SEA + p * PA + k;
-      double t[Q], f[Q], c[M];
+      double t[Q], f[Q], g[Q], c[M];
       ld_pencil<Q, Q>(b, t);
       ld_pencil<Q, Q>(b + TB, f);
+      ld_pencil<Q, Q>(b + 2 * TB, g);  // before the first store, as in S2
       X::project2(tab, t, f, c);
       st_pencil<M, RA>(a, c);
-      ld_pencil<Q, Q>(b + 2 * TB, t);
-      X::project(tab, t, c);
+      X::project(tab, g, c);
       st_pencil<M, RA>(a + TA, c);
     }
     pre_out();
