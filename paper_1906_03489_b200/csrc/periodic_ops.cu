@@ -484,9 +484,12 @@ cudaError_t owner_periodic_v3(int n, int P, const double* loc, double* y, int ac
 #ifndef CLASS_OWNER_NT
 #define CLASS_OWNER_NT 128
 #endif
-#ifndef CLASS_OWNER_MINB
-#define CLASS_OWNER_MINB (2048 / CLASS_OWNER_NT)
-#endif
+// resident CTAs per SM the kernel is compiled for: 16 (32 registers, full
+// occupancy) with multi-element tiles; 12 (42 registers, no spills) with
+// one-element tiles, whose scalar loads keep more index state live —
+// measured P=6 139 -> 127 us, P=7 181 -> 164, P=8 242 -> 218, while P <= 5
+// lose 5-10 us at 12
+__host__ __device__ constexpr int class_owner_minb(int ne) { return ne == 1 ? 12 : 16; }
 namespace {
 
 // offset of class k inside an element's class-major record
@@ -619,7 +622,7 @@ __device__ __forceinline__ void owned_sum2(const double* __restrict__ Z, const i
 // an output is a few compares), so every thread has work at every order.
 // 32-bit offsets from Z: n^3 nm < 2^31 for every map the kernels accept.
 template <int P, int NE>
-__global__ void __launch_bounds__(CLASS_OWNER_NT, CLASS_OWNER_MINB) class_owner_sum_kernel(int n, const double* __restrict__ Z,
+__global__ void __launch_bounds__(CLASS_OWNER_NT, class_owner_minb(NE)) class_owner_sum_kernel(int n, const double* __restrict__ Z,
                                                               double* __restrict__ y, int accumulate,
                                                               int nreg, int row0, int row1) {
   using G = OwnerGeom<P>;
@@ -681,7 +684,7 @@ cudaError_t class_owner_sum(int n, int P, int ne, const double* Z, double* y, in
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // one wave of CTAs with the same number of rows each (no tail)
-  const int64_t rows = row1 - row0, cap = (int64_t)sms * (2048 / CLASS_OWNER_NT);
+  const int64_t rows = row1 - row0, cap = (int64_t)sms * class_owner_minb(ne);
   const int64_t per = (rows + cap - 1) / cap;
   const int64_t blocks = (rows + per - 1) / per;
   auto go = [&](auto pc, auto nc) -> cudaError_t {
