@@ -78,9 +78,12 @@ static int helm_variant_env() {
 
 // PERIODIC_CLASS (pipeline MODE 5): tiles of NE consecutive elements of an
 // x-row (NE must divide n)
-// MODE 6 (geometry from global memory, L2-prefetched): tuning builds only (SPHP_CLASS_GDIR)
+// MODE 6 (geometry from global memory, L2-prefetched): the k-major orders (SPHP_CLASS_GDIR)
 #ifndef SPHP_CLASS_GDIR
-#define SPHP_CLASS_GDIR 0  // tuning: 1 = class mode of k-major METRIC orders reads global geometry too
+// 1: the class launch of k-major METRIC orders (Q = 9: P = 7) reads the
+// geometry from global memory too (MODE 6) — 2.577 -> 2.534 ms once the
+// per-tile divisions were gone (it lost 8 % before: profiles/r02_kmajor.log)
+#define SPHP_CLASS_GDIR 1
 #endif
 template <int M, int Q, int GK>
 constexpr int class_mode() {

@@ -274,8 +274,8 @@ struct Scaffold {
   // pointwise stage (prefetched into L2 one tile ahead) instead of staging
   // it: no shared-memory copy, more resident CTAs.  Only won at P = 2 with
   // the former skewed Q = 4 plan (0.209 -> 0.198 ms; P = 3..8 lose 10-35 %,
-  // tools/time_phases.py); the i-column plan beats both (0.181 ms), so no
-  // default build takes MODE 6 any more (SPHP_CLASS_GDIR tuning builds do)
+  // tools/time_phases.py); the i-column plan beats both (0.181 ms).  Today
+  // MODE 6 serves the k-major K-row order P = 7 (hex_helm.cu: SPHP_CLASS_GDIR)
   static constexpr bool GDIR = ModeTraits<MODE>::GDIR;
   static constexpr int GEO_T = GDIR ? 0 : NE * GEO_S;
   static constexpr int STAGE = IN_T + GEO_T;
