@@ -2,6 +2,9 @@
 # tuning builds recompiling SEVERAL sources under other macro settings
 # (e.g. a geometry layout shared by producers and consumers)
 #   SRCS="misc.cu solver.cu hex_helm.cu hex_helm1.cu hex_helm2.cu" tools/build_variants_multi.sh name:flags ...
+# The variant libraries land in build/variants/<name>/ (selected at run time
+# with SPHP_LIBRARY_VARIANT=<name>); .gpurunignore keeps that directory off
+# the GPU box, so drop its build/variants/ line while A/B-ing and restore it.
 set -e
 cd "$(dirname "$0")/../paper_1906_03489_b200/csrc"
 make -j8 > /dev/null
